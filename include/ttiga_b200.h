@@ -1,0 +1,141 @@
+/*
+ * ttiga_b200.h -- C ABI of libttiga_b200.so, the sm_100a TT-IGA hot path.
+ *
+ * Plain pointers and sizes only (no torch types). Every pointer argument is a
+ * DEVICE pointer unless noted; `stream` is a cudaStream_t passed as void*.
+ * Matrices are FP64; "col-major" follows LAPACK, otherwise row-major (C order,
+ * the layout of numpy/torch TT cores). Return value: 0 ok, >0 CUDA error code,
+ * <0 argument/numerical status (see TTB_E* below).
+ *
+ * Each entry point names the reference interface it replaces
+ * (reference tree: arxiv/paper_2509_13224, pkg/src/ttiga/...).
+ */
+#ifndef TTIGA_B200_H
+#define TTIGA_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TTB_OK 0
+#define TTB_EARG (-1)
+#define TTB_ENOTPD (-2)
+#define TTB_ESINGULAR (-3)
+
+/* ---- dense FP64 building blocks ------------------------------------------------------------ */
+
+/* C[b] = alpha * op(A[b]) op(B[b]) + beta * C[b], row-major, strided batch.
+ * Replaces the np.einsum / np.tensordot contractions of tensor_train/core.py:346,381,419,434
+ * and tensor_train/amen.py:105-122,146-191. DMMA (mma.sync m8n8k4 f64) tiles, split-K when the
+ * output is too small to fill the 148 SMs. */
+int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+              long long sA, const double* B, long long ldb, long long sB, double beta, double* C, long long ldc,
+              long long sC, int batch);
+
+/* dst = src.transpose(perm) for a row-major nd-array (nd <= 8); in_dims is a HOST array. */
+int ttb_permute(void* stream, int nd, const long long* in_dims, const int* perm, const double* src, double* dst);
+
+/* out[0] = x.y (y == NULL: ||x||^2; take_sqrt: ||x||). part: >= 296 doubles scratch. Deterministic. */
+int ttb_dot(void* stream, long long n, const double* x, const double* y, double* out, double* part, int take_sqrt);
+
+/* ---- Householder QR / SVD / solvers (np.linalg.qr, np.linalg.svd, np.linalg.solve,
+ *      scipy.linalg.cho_factor/cho_solve as used by tensor_train/core.py:362,417,430,
+ *      tensor_train/cross.py:170,188,190, tensor_train/amen.py:390-391, assembly.py:412-413) -- */
+
+long long ttb_qr_workspace(int m, int n); /* doubles */
+/* In-place blocked Householder QR of col-major A (m x n, lda); tau: min(m,n). */
+int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, double* tau, double* ws);
+/* Explicit Q (m x kq, col-major) from ttb_geqrf (same ws); kf = reflector count, n_factored = n of geqrf. */
+int ttb_orgqr(void* stream, int m, int kq, int kf, const double* A, long long lda, double* Q, long long ldq, double* ws,
+              int n_factored);
+/* R (k x n col-major) = upper triangle of the geqrf result. */
+int ttb_extract_r(void* stream, int k, int n, const double* A, long long lda, double* R);
+
+/* One-sided Jacobi SVD of `batch` n x n col-major matrices: A = U diag(S) V^T, S descending.
+ * work: batch*(2n^2+n) doubles when n > 64 (shared memory otherwise); info: sweeps per matrix (nullable). */
+int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, double* S, long long strideS, double* U,
+                   double* V, long long strideUV, int batch, double* work, int* info);
+
+/* LU with partial pivoting (in place, col-major) and solve of op(A) X = B (B col-major n x nrhs). */
+int ttb_lu_solve(void* stream, int n, double* A, long long lda, int* piv, int nrhs, double* B, long long ldb,
+                 int trans, int* info);
+/* Blocked Cholesky (lower, col-major) ; *info > 0 on a non-positive pivot (device int). */
+int ttb_potrf(void* stream, int n, double* A, long long lda, int* info);
+/* Solve L L^T x = b in place (n <= 25600). */
+int ttb_potrs(void* stream, int n, const double* L, long long lda, double* b);
+
+/* ---- maxvol (tensor_train/maxvol.py:37-62) --------------------------------------------------- */
+long long ttb_maxvol_workspace(int n, int r); /* doubles */
+/* rows_out: r sorted row indices of a tol-dominant r x r submatrix of Q (n x r col-major), n > r.
+ * iws: n + 1 ints; iws[n] = 1 on a rank-deficient input (reference MaxvolError). Cooperative launch. */
+int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, int max_iters, int* rows_out, double* ws,
+               int* iws);
+
+/* ---- IGA kernels (splines.py:170-245, geometry.py:150-261, assembly.py:208-233, driver.py:388-422) */
+
+/* Nonzero basis values/derivatives at nq parameters (Cox-de Boor; NURBS when weights != NULL).
+ * first: int[nq]; V, D: nq x (p+1). bad: device int, min'ed with the first out-of-range index. */
+int ttb_basis_eval(void* stream, int nq, const double* x, const double* knots, int nk, int p, const double* weights,
+                   int* first, double* V, double* D, int* bad);
+
+/* Rational geometry map at N grid multi-indices idx (int64, N x 3) of a tensor grid whose per-direction
+ * basis windows are (f_d, V_d, D_d). cw: control grid (n0, n1, n2, 4) = (w x, w y, w z, w).
+ * mode 0: out[k] = R[ri][rj], R = J^-1 J^-T det J       (assembly.metric_oracle)
+ * mode 1: out[k] = f(x) det J, f = source id `src`      (assembly.load_oracle)
+ * mode 2: out[22 k ...] = J (9), x (3), det, R (9)        (GridEvaluator.jacobians/metric)
+ * mode 3: out[3 k ...] = x                                (GridEvaluator.points)
+ * bad: device int64, min'ed with the first index where |det J| < sing_tol (SingularMapError). */
+int ttb_geo_eval(void* stream, long long N, const long long* idx, const int* f0, const int* f1, const int* f2,
+                 const double* V0, const double* V1, const double* V2, const double* D0, const double* D1,
+                 const double* D2, int p0, int p1, int p2, int n0, int n1, int n2, const double* cw, double sing_tol,
+                 int mode, int ri, int rj, int src, double* out, long long* bad);
+
+/* Banded operator core from a quadrature-grid TT core G (r, nq, s) (assembly._contract_matrix_core):
+ * out[a, i, t, b] = sum_q G[a,q,b] w[q] X[q, i-first[q]] Y[q, j-first[q]], j = i+t-h, out (r, n, 2h+1, s). */
+int ttb_op_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                const double* X, const double* Y, int p, int n, int h, double* out);
+/* Load core (assembly._contract_vector_core): out[a, i, b] = sum_q G[a,q,b] w[q] V[q, i-first[q]]. */
+int ttb_vec_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                 const double* V, int p, int n, double* out);
+/* Solution core at quadrature points: T[a,q,b] = sum_k u[a, first[q]+k, b] V[q,k]. */
+int ttb_field_table(void* stream, int r, int n, int s, const double* u, int nq, const int* first, const double* V,
+                    int p, double* T);
+/* driver.l2_error integrals: out[0] = sum w det|u-u*|, out[1] = sum w det|u*| (part: 2*nq0*nq1 doubles). */
+int ttb_l1_error(void* stream, const int* f0, const int* f1, const int* f2, const double* V0, const double* V1,
+                 const double* V2, const double* D0, const double* D1, const double* D2, int p0, int p1, int p2,
+                 int n0, int n1, int n2, const double* cw, int nq0, int nq1, int nq2, const double* U0, int r1,
+                 const double* U1, int r2, const double* U2, const double* w0, const double* w1, const double* w2,
+                 int exact_id, const double* prm, double* part, double* out);
+
+/* ---- TT operator kernels (tensor_train/core.py:373-384, tensor_train/amen.py:76-191) ----------- */
+
+/* TT-matvec of a banded operator core M (Ra, n, 2h+1, Rb) with a vector core X (rc, n, rd):
+ * Y[(a,c), i, (b,d)] = sum_t M[a,i,t,b] X[c, i+t-h, d]. */
+int ttb_band_matvec(void* stream, int Ra, int Rb, int n, int h, int rc, int rd, const double* M, const double* X,
+                    double* Y);
+/* rev=0: out[x,i,b,w] = sum_{a,t} M[a,i,t,b] T[x,a,i+t-h,w];  rev=1: out[x,i,a,w] = sum_{b,t} M[a,i,t,b] T[x,b,j,w]. */
+int ttb_band_apply(void* stream, int X, int Ra, int Rb, int n, int h, int W, const double* M, const double* T,
+                   double* out, int rev);
+/* Dense projected local matrix (band entries only; Bm pre-zeroed), T1[x,y,i,t,b] = sum_a phiL[x,a,y] M[a,i,t,b]. */
+int ttb_local_dense(void* stream, int r0, int n, int r1, int h, int Rb, const double* T1, const double* phiR,
+                    double* Bm);
+/* Jacobi diagonal of the local operator, floored at 1e-14 max|d| (amen.py:380-403). part: >= 297 doubles. */
+int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
+                    const double* phiR, double* d, double* part);
+/* Entries of a 3-core TT at N multi-indices (TtTensor.gather, core.py:164-170). */
+int ttb_tt_gather3(void* stream, int N, const long long* idx, const double* G0, int n0, int r1, const double* G1,
+                   int n1, int r2, const double* G2, int n2, double* out);
+/* y = local projected operator applied to v (amen._LocalSystem.matvec3). ws: r0*Ra*n*r1 + r0*n*Rb*r1 doubles. */
+int ttb_local_matvec(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
+                     const double* phiR, const double* v, double* y, double* ws);
+long long ttb_pcg_workspace(int r0, int n, int r1, int Ra, int Rb); /* doubles */
+/* Jacobi-preconditioned CG with scipy.sparse.linalg.cg stopping semantics (||r|| < atol, maxiter),
+ * x: x0 in / solution out; S: >= 8 device doubles; iters: HOST int (nullable). */
+int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
+                  const double* phiR, const double* b, double* x, const double* d, double atol, int maxiter,
+                  int x0_nonzero, double* ws, double* S, int* iters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,320 @@
+// FP64 dense building blocks: DMMA GEMM, N-d permute, deterministic reductions.
+//
+// The GEMM is the contraction engine for every TT core product (TT-matvec,
+// rounding carries, AMEn environments). It issues FP64 tensor-core MMAs
+// (mma.sync m8n8k4 .f64 -> SASS DMMA) from shared-memory tiles filled with
+// cp.async (LDGSTS) in a two-stage pipeline.
+#include "common.cuh"
+
+namespace {
+
+constexpr int BK = 16;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int bytes = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct GemmArgs {
+  int M, N, K;
+  double alpha, beta;
+  const double* A;
+  long long lda, sA;
+  int tA;
+  const double* B;
+  long long ldb, sB;
+  int tB;
+  double* C;
+  long long ldc, sC;
+  int split;  // split-K: blockIdx.z indexes K chunks of length Kc, partials to C + z*sC
+  int Kc;
+};
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
+  constexpr int T = WM * WN * 32;
+  constexpr int PA = BM + 8, PB = BN + 8;
+  constexpr int MT = BM / WM / 8, NT = BN / WN / 8;
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;                   // [2][BK][PA]
+  double* Bs = sm + 2 * BK * PA;     // [2][BK][PB]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WM, wn = warp / WM;
+  const int bm0 = blockIdx.y * BM, bn0 = blockIdx.x * BN;
+  const long long bz = blockIdx.z;
+  const double* A;
+  const double* B;
+  double* C = g.C + bz * g.sC;
+  const int M = g.M, N = g.N;
+  int K;
+  if (g.split) {
+    const long long kb = bz * g.Kc;
+    K = (int)min((long long)g.Kc, (long long)g.K - kb);
+    A = g.A + (g.tA ? kb * g.lda : kb);
+    B = g.B + (g.tB ? kb : kb * g.ldb);
+  } else {
+    K = g.K;
+    A = g.A + bz * g.sA;
+    B = g.B + bz * g.sB;
+  }
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double* as = As + st * BK * PA;
+    double* bs = Bs + st * BK * PB;
+#pragma unroll
+    for (int e0 = 0; e0 < BK * BM; e0 += T) {
+      int e = e0 + tid;
+      int ml, kl;
+      if (!g.tA) { ml = e / BK; kl = e % BK; } else { kl = e / BM; ml = e % BM; }
+      int m = bm0 + ml, k = k0 + kl;
+      bool ok = (m < M) && (k < K);
+      const double* src = ok ? (g.tA ? A + (long long)k * g.lda + m : A + (long long)m * g.lda + k) : A;
+      cp_async8(as + kl * PA + ml, src, ok);
+    }
+#pragma unroll
+    for (int e0 = 0; e0 < BK * BN; e0 += T) {
+      int e = e0 + tid;
+      int nl, kl;
+      if (!g.tB) { kl = e / BN; nl = e % BN; } else { nl = e / BK; kl = e % BK; }
+      int n = bn0 + nl, k = k0 + kl;
+      bool ok = (n < N) && (k < K);
+      const double* src = ok ? (g.tB ? B + (long long)n * g.ldb + k : B + (long long)k * g.ldb + n) : B;
+      cp_async8(bs + kl * PB + nl, src, ok);
+    }
+  };
+
+  const int nk = (K + BK - 1) / BK;
+  if (nk > 0) {
+    load(0, 0);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt + 1 < nk) {
+      load(kt + 1, (kt + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + (kt & 1) * BK * PA;
+    const double* bs = Bs + (kt & 1) * BK * PB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[MT], bf[NT];
+      const int kr = kk + (lane & 3);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) af[i] = as[kr * PA + wm * (BM / WM) + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = bs[kr * PB + wn * (BN / WN) + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int m = bm0 + wm * (BM / WM) + i * 8 + (lane >> 2);
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int n = bn0 + wn * (BN / WN) + j * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (n + h < N) {
+          double* c = C + (long long)m * g.ldc + n + h;
+          double v = g.alpha * acc[i][j][h];
+          if (!g.split && g.beta != 0.0) v += g.beta * *c;
+          *c = v;
+        }
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WM, int WN>
+int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
+  constexpr int T = WM * WN * 32;
+  size_t smem = (size_t)2 * BK * ((BM + 8) + (BN + 8)) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(dgemm_kernel<BM, BN, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), batch);
+  dgemm_kernel<BM, BN, WM, WN><<<grid, T, smem, st>>>(g);
+  return ttb_last_error();
+}
+
+__global__ void scale_kernel(long long n, double beta, double* C, long long ldc, int M, int N, long long sC) {
+  // C = beta*C over an M x N (row-major, ldc) block per batch (used when K == 0)
+  long long b = blockIdx.y;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    long long m = e / N, c = e % N;
+    double* p = C + b * sC + m * ldc + c;
+    *p = beta == 0.0 ? 0.0 : beta * *p;
+  }
+}
+
+__global__ void splitk_reduce(int M, int N, int S, const double* __restrict__ part, double alpha, double beta,
+                              double* C, long long ldc) {
+  long long tot = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += part[(long long)z * tot + e];
+    double* c = C + (e / N) * ldc + (e % N);
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * *c;
+    *c = v;
+  }
+}
+
+double* g_scratch = nullptr;
+size_t g_scratch_bytes = 0;
+
+double* scratch(size_t bytes) {
+  if (bytes > g_scratch_bytes) {
+    if (g_scratch) { cudaDeviceSynchronize(); cudaFree(g_scratch); }
+    size_t want = bytes + bytes / 2;
+    if (cudaMalloc(&g_scratch, want) != cudaSuccess) { g_scratch = nullptr; g_scratch_bytes = 0; return nullptr; }
+    g_scratch_bytes = want;
+  }
+  return g_scratch;
+}
+
+// ---------------------------------------------------------------------------
+struct PermArgs {
+  int nd;
+  long long out_dims[8];
+  long long in_stride_for_out[8];  // input stride of the input axis that lands on output axis k
+};
+
+__global__ void permute_kernel(PermArgs a, long long total, const double* __restrict__ src, double* __restrict__ dst) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total; j += (long long)gridDim.x * blockDim.x) {
+    long long rem = j, off = 0;
+#pragma unroll 8
+    for (int k = a.nd - 1; k >= 0; --k) {
+      long long c = rem % a.out_dims[k];
+      rem /= a.out_dims[k];
+      off += c * a.in_stride_for_out[k];
+    }
+    dst[j] = src[off];
+  }
+}
+
+// deterministic two-level reductions ----------------------------------------
+constexpr int RED_BLOCKS = 296;
+constexpr int RED_THREADS = 256;
+
+__global__ void dot_partial(long long n, const double* __restrict__ x, const double* __restrict__ y, double* part) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s += x[i] * (y ? y[i] : x[i]);
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_final(int np, const double* part, double* out, int take_sqrt) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) *out = take_sqrt ? sqrt(s) : s;
+}
+
+}  // namespace
+
+TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                      long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
+                      long long ldc, long long sC, int batch) {
+  if (M < 0 || N < 0 || K < 0 || batch < 0) return TTB_EARG;
+  if (M == 0 || N == 0 || batch == 0) return TTB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (K == 0) {
+    long long n = (long long)M * N;
+    dim3 grid(ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), batch);
+    scale_kernel<<<grid, 256, 0, st>>>(n, beta, C, ldc, M, N, sC);
+    return ttb_last_error();
+  }
+  GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};
+  long long work = (long long)M * N * batch;
+  const bool big = work >= (long long)148 * 128 * 128 * 2 && M >= 128 && N >= 128;
+  const long long tiles = big ? (long long)ceil_div(M, 128) * ceil_div(N, 128) * batch
+                              : (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch;
+  if (batch == 1 && tiles < 148 && K >= 1024) {
+    // split-K: enough K chunks to cover ~2 waves, each chunk >= 256 deep, deterministic reduction
+    long long S = (296 + tiles - 1) / tiles;
+    long long maxS = K / 256;
+    if (S > maxS) S = maxS;
+    if (S > 1) {
+      int Kc = (int)(((K + S - 1) / S + BK - 1) / BK * BK);
+      S = (K + Kc - 1) / Kc;
+      double* part = scratch((size_t)S * M * N * sizeof(double));
+      if (!part) return (int)cudaErrorMemoryAllocation;
+      GemmArgs p = g;
+      p.alpha = 1.0; p.beta = 0.0; p.C = part; p.ldc = N; p.sC = (long long)M * N; p.split = 1; p.Kc = Kc;
+      int rc = big ? launch_gemm<128, 128, 2, 4>(p, (int)S, st) : launch_gemm<64, 64, 2, 2>(p, (int)S, st);
+      if (rc) return rc;
+      long long tot = (long long)M * N;
+      int blocks = ceil_div(tot, 256);
+      if (blocks > 148 * 8) blocks = 148 * 8;
+      splitk_reduce<<<blocks, 256, 0, st>>>(M, N, (int)S, part, alpha, beta, C, ldc);
+      return ttb_last_error();
+    }
+  }
+  if (big) return launch_gemm<128, 128, 2, 4>(g, batch, st);
+  return launch_gemm<64, 64, 2, 2>(g, batch, st);
+}
+
+// dst = permute(src): src has dims in_dims[0..nd) (row-major); output axis k is input axis perm[k].
+TTB_API int ttb_permute(void* stream, int nd, const long long* in_dims, const int* perm, const double* src, double* dst) {
+  if (nd < 1 || nd > 8) return TTB_EARG;
+  PermArgs a;
+  a.nd = nd;
+  long long stride[8];
+  long long s = 1;
+  for (int k = nd - 1; k >= 0; --k) { stride[k] = s; s *= in_dims[k]; }
+  long long total = s;
+  for (int k = 0; k < nd; ++k) {
+    if (perm[k] < 0 || perm[k] >= nd) return TTB_EARG;
+    a.out_dims[k] = in_dims[perm[k]];
+    a.in_stride_for_out[k] = stride[perm[k]];
+  }
+  if (total == 0) return TTB_OK;
+  int blocks = ceil_div(total, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  permute_kernel<<<blocks, 256, 0, as_stream(stream)>>>(a, total, src, dst);
+  return ttb_last_error();
+}
+
+// out[0] = x.y (y == NULL -> ||x||^2; take_sqrt -> ||x||). part: >= 296 doubles of scratch.
+TTB_API int ttb_dot(void* stream, long long n, const double* x, const double* y, double* out, double* part,
+                    int take_sqrt) {
+  cudaStream_t st = as_stream(stream);
+  int blocks = n <= 0 ? 1 : (ceil_div(n, RED_THREADS) < RED_BLOCKS ? ceil_div(n, RED_THREADS) : RED_BLOCKS);
+  dot_partial<<<blocks, RED_THREADS, 0, st>>>(n, x, y, part);
+  sum_final<<<1, 256, 0, st>>>(blocks, part, out, take_sqrt);
+  return ttb_last_error();
+}

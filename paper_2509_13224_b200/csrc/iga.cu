@@ -1,0 +1,456 @@
+// IGA kernels: B-spline/NURBS basis windows at Gauss points, the rational
+// geometry map with its Jacobian / det J / metric factor R = J^-1 J^-T det J at
+// cross-fiber multi-indices, the per-direction weighted mass/stiffness
+// quadrature that turns a quadrature-grid TT core into a banded operator core,
+// and the volume error integral.
+#include "common.cuh"
+
+namespace {
+
+constexpr int PMAX = 8;
+
+// ---------------------------------------------------------------------------
+// Cox-de Boor (NURBS Book A2.2/A2.3) for one parameter; reference splines.py:170-245.
+__global__ void basis_kernel(int nq, const double* __restrict__ x, const double* __restrict__ t, int nk, int p,
+                             const double* __restrict__ w, int* first, double* V, double* D, int* bad) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double xv = x[q];
+  const int nb = nk - p - 1;
+  if (xv < t[0] || xv > t[nk - 1]) { atomicMin(bad, q); return; }
+  int k;
+  if (xv >= t[nb]) {
+    k = nb - 1;
+    while (t[k] == t[k + 1]) --k;
+  } else {  // last i with t[i] <= x
+    int lo = 0, hi = nk - 1;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (t[mid] <= xv) lo = mid; else hi = mid;
+    }
+    k = lo;
+  }
+  double N[PMAX + 1], low[PMAX + 1];
+  N[0] = 1.0;
+  low[0] = 1.0;
+  for (int j = 1; j <= p; ++j) {
+    if (j == p)
+      for (int r = 0; r < p; ++r) low[r] = N[r];
+    double carry = 0.0;
+    for (int r = 0; r < j; ++r) {
+      const double a = xv - t[k + 1 - j + r];
+      const double b = t[k + 1 + r] - xv;
+      const double den = a + b;
+      const double qq = den != 0.0 ? N[r] / den : 0.0;
+      N[r] = carry + b * qq;
+      carry = a * qq;
+    }
+    N[j] = carry;
+  }
+  double dN[PMAX + 1];
+  for (int j = 0; j <= p; ++j) {
+    double acc = 0.0;
+    if (p > 0) {
+      const int i = k - p + j;
+      if (j > 0) {
+        double den = t[i + p] - t[i];
+        if (den != 0.0) acc += p / den * low[j - 1];
+      }
+      if (j < p) {
+        double den = t[i + p + 1] - t[i + 1];
+        if (den != 0.0) acc -= p / den * low[j];
+      }
+    }
+    dN[j] = acc;
+  }
+  if (w) {
+    double W = 0.0, dW = 0.0;
+    for (int j = 0; j <= p; ++j) { W += N[j] * w[k - p + j]; dW += dN[j] * w[k - p + j]; }
+    for (int j = 0; j <= p; ++j) {
+      const double wj = w[k - p + j];
+      const double v = N[j] * wj / W;
+      const double d = (dN[j] * wj * W - N[j] * wj * dW) / (W * W);
+      N[j] = v;
+      dN[j] = d;
+    }
+  }
+  first[q] = k - p;
+  for (int j = 0; j <= p; ++j) {
+    V[(long long)q * (p + 1) + j] = N[j];
+    D[(long long)q * (p + 1) + j] = dN[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct GeoArgs {
+  const int* first[3];
+  const double* V[3];
+  const double* D[3];
+  int p[3];
+  int n[3];
+  const double* cw;  // (n0, n1, n2, 4): w*x, w*y, w*z, w
+  double sing_tol;
+};
+
+struct GeoOut {
+  double J[3][3];
+  double x[3];
+  double det;
+};
+
+__device__ __forceinline__ void geo_point(const GeoArgs& g, int q0, int q1, int q2, GeoOut& o) {
+  const int f0 = g.first[0][q0], f1 = g.first[1][q1], f2 = g.first[2][q2];
+  const int p0 = g.p[0] + 1, p1 = g.p[1] + 1, p2 = g.p[2] + 1;
+  const double* V0 = g.V[0] + (long long)q0 * p0;
+  const double* D0 = g.D[0] + (long long)q0 * p0;
+  const double* V1 = g.V[1] + (long long)q1 * p1;
+  const double* D1 = g.D[1] + (long long)q1 * p1;
+  const double* V2 = g.V[2] + (long long)q2 * p2;
+  const double* D2 = g.D[2] + (long long)q2 * p2;
+  // sums over the window: value, d/dxi0, d/dxi1, d/dxi2 of (wx, wy, wz, w)
+  double S[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) S[a][b] = 0.0;
+  for (int a = 0; a < p0; ++a) {
+    const double va = V0[a], da = D0[a];
+    double T[3][4];  // after contracting b,c: [v2v1, v2d1, d2v1] x 4 comps... accumulate directly
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) T[u][cc] = 0.0;
+    for (int b = 0; b < p1; ++b) {
+      const double vb = V1[b], db = D1[b];
+      double R0[4] = {0, 0, 0, 0}, R2[4] = {0, 0, 0, 0};
+      const double* row = g.cw + (((long long)(f0 + a) * g.n[1] + (f1 + b)) * g.n[2] + f2) * 4;
+      for (int c = 0; c < p2; ++c) {
+        const double2 lo = *reinterpret_cast<const double2*>(row + 4 * c);
+        const double2 hi = *reinterpret_cast<const double2*>(row + 4 * c + 2);
+        const double vc = V2[c], dc = D2[c];
+        R0[0] += vc * lo.x; R0[1] += vc * lo.y; R0[2] += vc * hi.x; R0[3] += vc * hi.y;
+        R2[0] += dc * lo.x; R2[1] += dc * lo.y; R2[2] += dc * hi.x; R2[3] += dc * hi.y;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        T[0][cc] += vb * R0[cc];
+        T[1][cc] += db * R0[cc];
+        T[2][cc] += vb * R2[cc];
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      S[0][cc] += va * T[0][cc];
+      S[1][cc] += da * T[0][cc];
+      S[2][cc] += va * T[1][cc];
+      S[3][cc] += va * T[2][cc];
+    }
+  }
+  const double den = S[0][3];
+  const double inv2 = 1.0 / (den * den);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    o.x[c] = S[0][c] / den;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) o.J[c][e] = (S[1 + e][c] * den - S[0][c] * S[1 + e][3]) * inv2;
+  }
+  const double(*J)[3] = o.J;
+  o.det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+          J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+}
+
+__device__ __forceinline__ void metric_from(const GeoOut& o, double R[3][3]) {
+  const double(*J)[3] = o.J;
+  double A[3][3];  // adjugate: inv = A / det
+  A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+  A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+  A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+  A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+  A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+  A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  const double id = 1.0 / o.det;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) R[i][j] = (A[i][0] * A[j][0] + A[i][1] * A[j][1] + A[i][2] * A[j][2]) * id;
+}
+
+__device__ __forceinline__ double source_fn(int id, const double* x) {
+  const double PI = 3.141592653589793;
+  switch (id) {
+    case 0: return 0.0;
+    case 1: return 1.0;
+    case 2: return sin(PI * x[0]) * sin(PI * x[1]);
+    case 3: return sin(PI * x[0]) * sin(PI * x[1]) * sin(PI * x[2]);
+    case 4: return 3.0 * PI * PI * sin(PI * x[0]) * sin(PI * x[1]) * sin(PI * x[2]);
+    case 5: {
+      const double e = exp(x[0] + x[1] + x[2]);
+      const double s0 = sin(PI * x[0]), s1 = sin(PI * x[1]), s2 = sin(PI * x[2]);
+      const double c0 = cos(PI * x[0]), c1 = cos(PI * x[1]), c2 = cos(PI * x[2]);
+      const double S = s0 * s1 * s2, mix = c0 * s1 * s2 + s0 * c1 * s2 + s0 * s1 * c2;
+      return -e * ((3.0 - 3.0 * PI * PI) * S + 2.0 * PI * mix);
+    }
+  }
+  return 0.0;
+}
+
+// analytic solutions: 0 lshape_exact, 1 cube_sines, 2 ring_radial(prm: u_in,u_out,r_in,r_out), 3 exp_sines
+__device__ __forceinline__ double exact_fn(int id, const double* x, const double* prm) {
+  const double PI = 3.141592653589793;
+  switch (id) {
+    case 0: return sin(PI * x[0]) * sin(PI * x[1]) / (2.0 * PI * PI);
+    case 1: return sin(PI * x[0]) * sin(PI * x[1]) * sin(PI * x[2]);
+    case 2: {
+      const double r = hypot(x[0], x[1]);
+      return (prm[0] * log(prm[3] / r) + prm[1] * log(r / prm[2])) / log(prm[3] / prm[2]);
+    }
+    case 3: return exp(x[0] + x[1] + x[2]) * sin(PI * x[0]) * sin(PI * x[1]) * sin(PI * x[2]);
+  }
+  return 0.0;
+}
+
+// mode 0: R[ri][rj]; 1: f(x) det; 2: full record (J9, x3, det, R9) stride 22; 3: x only (stride 3)
+__global__ void geo_kernel(GeoArgs g, long long N, const long long* __restrict__ idx, int mode, int ri, int rj, int src,
+                           double* out, long long* bad) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < N; k += (long long)gridDim.x * blockDim.x) {
+    const int q0 = (int)idx[3 * k], q1 = (int)idx[3 * k + 1], q2 = (int)idx[3 * k + 2];
+    GeoOut o;
+    geo_point(g, q0, q1, q2, o);
+    if (mode == 3) {
+      out[3 * k] = o.x[0]; out[3 * k + 1] = o.x[1]; out[3 * k + 2] = o.x[2];
+      continue;
+    }
+    if (mode != 1 && fabs(o.det) < g.sing_tol) {
+      atomicMin((unsigned long long*)bad, (unsigned long long)k);
+      if (mode == 0) { out[k] = 0.0; continue; }
+    }
+    if (mode == 1) {
+      out[k] = source_fn(src, o.x) * o.det;
+    } else if (mode == 0) {
+      double R[3][3];
+      metric_from(o, R);
+      out[k] = R[ri][rj];
+    } else {
+      double* r = out + 22 * k;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) r[3 * a + b] = o.J[a][b];
+      r[9] = o.x[0]; r[10] = o.x[1]; r[11] = o.x[2];
+      r[12] = o.det;
+      double R[3][3];
+      metric_from(o, R);
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) r[13 + 3 * a + b] = R[a][b];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// operator core (banded): out[a, i, t, b] = sum_{q in Q(i)} G[a,q,b] w[q] X[q,i-f_q] Y[q,j-f_q], j = i+t-h
+__device__ __forceinline__ int lower_bound_first(const int* f, int nq, int v) {  // first q with f[q] >= v
+  int lo = 0, hi = nq;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (f[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void op_core_kernel(int r, int nq, int s, const double* __restrict__ G, const double* __restrict__ w,
+                               const int* __restrict__ first, const double* __restrict__ X,
+                               const double* __restrict__ Y, int p, int n, int h, double* out) {
+  const int B = 2 * h + 1;
+  const long long tot = (long long)r * n * B * s;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(e % s);
+    long long rest = e / s;
+    const int t = (int)(rest % B);
+    rest /= B;
+    const int i = (int)(rest % n);
+    const int a = (int)(rest / n);
+    const int j = i + t - h;
+    double acc = 0.0;
+    if (j >= 0 && j < n) {
+      const int lo = lower_bound_first(first, nq, max(i, j) - p);
+      for (int q = lo; q < nq; ++q) {
+        const int f = first[q];
+        if (f > min(i, j)) break;
+        acc += G[((long long)a * nq + q) * s + b] * w[q] * X[(long long)q * (p + 1) + (i - f)] *
+               Y[(long long)q * (p + 1) + (j - f)];
+      }
+    }
+    out[e] = acc;
+  }
+}
+
+__global__ void vec_core_kernel(int r, int nq, int s, const double* __restrict__ G, const double* __restrict__ w,
+                                const int* __restrict__ first, const double* __restrict__ V, int p, int n,
+                                double* out) {
+  const long long tot = (long long)r * n * s;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(e % s);
+    const int i = (int)((e / s) % n);
+    const int a = (int)(e / ((long long)s * n));
+    double acc = 0.0;
+    const int lo = lower_bound_first(first, nq, i - p);
+    for (int q = lo; q < nq; ++q) {
+      const int f = first[q];
+      if (f > i) break;
+      acc += G[((long long)a * nq + q) * s + b] * w[q] * V[(long long)q * (p + 1) + (i - f)];
+    }
+    out[e] = acc;
+  }
+}
+
+// field tables: T[a, q, b] = sum_k u[a, first[q]+k, b] V[q, k]
+__global__ void field_table_kernel(int r, int n, int s, const double* __restrict__ u, int nq,
+                                   const int* __restrict__ first, const double* __restrict__ V, int p, double* T) {
+  const long long tot = (long long)r * nq * s;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(e % s);
+    const int q = (int)((e / s) % nq);
+    const int a = (int)(e / ((long long)s * nq));
+    double acc = 0.0;
+    for (int k = 0; k <= p; ++k) acc += u[((long long)a * n + first[q] + k) * s + b] * V[(long long)q * (p + 1) + k];
+    T[e] = acc;
+  }
+}
+
+// error integral: one CTA per (q0, q1); partial (num, den) per CTA
+__global__ void l1err_kernel(GeoArgs g, int nq0, int nq1, int nq2, const double* __restrict__ U0, int r1,
+                             const double* __restrict__ U1, int r2, const double* __restrict__ U2,
+                             const double* __restrict__ w0, const double* __restrict__ w1,
+                             const double* __restrict__ w2, int exact_id, const double* __restrict__ prm,
+                             double* part) {
+  extern __shared__ double Tsh[];  // r2
+  __shared__ double red[32];
+  const int q0 = blockIdx.x / nq1, q1 = blockIdx.x % nq1;
+  for (int c = threadIdx.x; c < r2; c += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < r1; ++b) s += U0[(long long)q0 * r1 + b] * U1[((long long)b * nq1 + q1) * r2 + c];
+    Tsh[c] = s;
+  }
+  __syncthreads();
+  double num = 0.0, den = 0.0;
+  const double w01 = w0[q0] * w1[q1];
+  for (int q2 = threadIdx.x; q2 < nq2; q2 += blockDim.x) {
+    double u = 0.0;
+    for (int c = 0; c < r2; ++c) u += Tsh[c] * U2[(long long)c * nq2 + q2];
+    GeoOut o;
+    geo_point(g, q0, q1, q2, o);
+    const double ue = exact_fn(exact_id, o.x, prm);
+    const double wd = w01 * w2[q2] * o.det;
+    num += wd * fabs(u - ue);
+    den += wd * fabs(ue);
+  }
+  num = block_sum(num, red);
+  den = block_sum(den, red);
+  if (threadIdx.x == 0) {
+    part[2 * (long long)blockIdx.x] = num;
+    part[2 * (long long)blockIdx.x + 1] = den;
+  }
+}
+
+__global__ void pair_sum_kernel(long long np, const double* part, double* out) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0;
+  for (long long i = threadIdx.x; i < np; i += blockDim.x) { a += part[2 * i]; b += part[2 * i + 1]; }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
+}
+
+int grid_for(long long tot, int threads = 256) {
+  long long b = (tot + threads - 1) / threads;
+  if (b > 148LL * 16) b = 148LL * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+GeoArgs make_geo(const int* const* first, const double* const* V, const double* const* D, const int* p, const int* n,
+                 const double* cw, double sing_tol) {
+  GeoArgs g;
+  for (int d = 0; d < 3; ++d) {
+    g.first[d] = first[d];
+    g.V[d] = V[d];
+    g.D[d] = D[d];
+    g.p[d] = p[d];
+    g.n[d] = n[d];
+  }
+  g.cw = cw;
+  g.sing_tol = sing_tol;
+  return g;
+}
+
+}  // namespace
+
+// Basis windows at nq parameters. bad: device int (init INT_MAX) receives the first out-of-range index.
+TTB_API int ttb_basis_eval(void* stream, int nq, const double* x, const double* knots, int nk, int p,
+                           const double* weights, int* first, double* V, double* D, int* bad) {
+  if (p < 0 || p > PMAX || nk < 2 * p + 2) return TTB_EARG;
+  if (nq == 0) return TTB_OK;
+  basis_kernel<<<ceil_div(nq, 128), 128, 0, as_stream(stream)>>>(nq, x, knots, nk, p, weights, first, V, D, bad);
+  return ttb_last_error();
+}
+
+// Geometry evaluation at N grid multi-indices (int64 N x 3). tables: per-direction first/V/D of the
+// geometry bases at the grid axes. bad: device int64 (init INT64_MAX) <- first singular row.
+TTB_API int ttb_geo_eval(void* stream, long long N, const long long* idx, const int* f0, const int* f1, const int* f2,
+                         const double* V0, const double* V1, const double* V2, const double* D0, const double* D1,
+                         const double* D2, int p0, int p1, int p2, int n0, int n1, int n2, const double* cw,
+                         double sing_tol, int mode, int ri, int rj, int src, double* out, long long* bad) {
+  if (N == 0) return TTB_OK;
+  const int* f[3] = {f0, f1, f2};
+  const double* V[3] = {V0, V1, V2};
+  const double* D[3] = {D0, D1, D2};
+  int p[3] = {p0, p1, p2}, n[3] = {n0, n1, n2};
+  GeoArgs g = make_geo(f, V, D, p, n, cw, sing_tol);
+  geo_kernel<<<grid_for(N, 128), 128, 0, as_stream(stream)>>>(g, N, idx, mode, ri, rj, src, out, bad);
+  return ttb_last_error();
+}
+
+TTB_API int ttb_op_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                        const double* X, const double* Y, int p, int n, int h, double* out) {
+  long long tot = (long long)r * n * (2 * h + 1) * s;
+  if (tot == 0) return TTB_OK;
+  op_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, X, Y, p, n, h, out);
+  return ttb_last_error();
+}
+
+TTB_API int ttb_vec_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                         const double* V, int p, int n, double* out) {
+  long long tot = (long long)r * n * s;
+  if (tot == 0) return TTB_OK;
+  vec_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, V, p, n, out);
+  return ttb_last_error();
+}
+
+TTB_API int ttb_field_table(void* stream, int r, int n, int s, const double* u, int nq, const int* first,
+                            const double* V, int p, double* T) {
+  long long tot = (long long)r * nq * s;
+  if (tot == 0) return TTB_OK;
+  field_table_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, n, s, u, nq, first, V, p, T);
+  return ttb_last_error();
+}
+
+// out[0] = sum w det |u - u*|, out[1] = sum w det |u*| over the tensor quadrature grid.
+TTB_API int ttb_l1_error(void* stream, const int* f0, const int* f1, const int* f2, const double* V0, const double* V1,
+                         const double* V2, const double* D0, const double* D1, const double* D2, int p0, int p1,
+                         int p2, int n0, int n1, int n2, const double* cw, int nq0, int nq1, int nq2,
+                         const double* U0, int r1, const double* U1, int r2, const double* U2, const double* w0,
+                         const double* w1, const double* w2, int exact_id, const double* prm, double* part,
+                         double* out) {
+  const int* f[3] = {f0, f1, f2};
+  const double* V[3] = {V0, V1, V2};
+  const double* D[3] = {D0, D1, D2};
+  int p[3] = {p0, p1, p2}, n[3] = {n0, n1, n2};
+  GeoArgs g = make_geo(f, V, D, p, n, cw, 0.0);
+  long long blocks = (long long)nq0 * nq1;
+  cudaStream_t st = as_stream(stream);
+  l1err_kernel<<<(unsigned)blocks, 128, r2 * sizeof(double), st>>>(g, nq0, nq1, nq2, U0, r1, U1, r2, U2, w0, w1, w2,
+                                                                     exact_id, prm, part);
+  pair_sum_kernel<<<1, 1024, 0, st>>>(blocks, part, out);
+  return ttb_last_error();
+}

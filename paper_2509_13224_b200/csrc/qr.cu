@@ -1,0 +1,286 @@
+// Blocked Householder QR (LAPACK dgeqrf/dorgqr conventions) on column-major FP64 matrices.
+//
+// Panels of NB columns are factored by one cooperative kernel (grid-wide
+// reductions for the column norms and the reflector/column dot products,
+// deterministic: every CTA re-sums the per-CTA partials in the same order);
+// the trailing matrix is updated with the compact-WY form
+// A2 -= V (T^T (V^T A2)) through three DMMA GEMMs, which carry the flops.
+#include "common.cuh"
+
+TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                      long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
+                      long long ldc, long long sC, int batch);
+
+namespace {
+
+constexpr int NB = 32;
+constexpr int PT = 256;  // threads per CTA of the panel kernel
+
+// Factor the m x jb panel P (col-major, ld) in place. Writes tau[0..jb), the explicit
+// reflectors V (m x jb col-major, ld m: unit diagonal, zeros above) and the WY factor T
+// (jb x jb row-major, upper triangular). part: gridDim.x * (NB*NB + NB) doubles.
+__global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, long long ld, double* tau, double* V,
+                                                      double* T, double* part) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sred[32];
+  __shared__ double swarp[PT / 32][NB];
+  __shared__ double sw[NB];
+  __shared__ double sG[NB * NB];
+  const int nblk = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // contiguous row chunk per CTA
+  const int chunk = (m + nblk - 1) / nblk;
+  const int r0 = blockIdx.x * chunk;
+  const int r1 = min(m, r0 + chunk);
+
+  for (int j = 0; j < jb; ++j) {
+    double* col = P + (long long)j * ld;
+    // 1) sum of squares below the diagonal
+    double s = 0.0;
+    for (int i = max(r0, j + 1) + threadIdx.x; i < r1; i += PT) s += col[i] * col[i];
+    s = block_sum(s, sred);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    grid.sync();
+    double xn2 = 0.0;
+    for (int b = 0; b < nblk; ++b) xn2 += part[b];
+    const double alpha = col[j];
+    double beta, t, scal;
+    if (xn2 == 0.0) {
+      beta = alpha; t = 0.0; scal = 0.0;
+    } else {
+      double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    // 2) scale v (own rows), partial dots w_c = v^T P[:, c] for c > j
+    double acc[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+    for (int i = max(r0, j) + threadIdx.x; i < r1; i += PT) {
+      double v;
+      if (i == j) v = 1.0;
+      else { v = col[i] * scal; col[i] = v; }
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c > j && c < jb) acc[c] += v * P[(long long)c * ld + i];
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      double v = warp_sum(acc[c]);
+      if (lane == 0) swarp[wid][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NB) {
+      double v = 0.0;
+      for (int w = 0; w < PT / 32; ++w) v += swarp[w][threadIdx.x];
+      part[nblk + (long long)blockIdx.x * NB + threadIdx.x] = v;
+    }
+    grid.sync();
+    if (threadIdx.x < NB) {
+      double v = 0.0;
+      for (int b = 0; b < nblk; ++b) v += part[nblk + (long long)b * NB + threadIdx.x];
+      sw[threadIdx.x] = v;
+    }
+    __syncthreads();
+    // 3) apply H_j to the remaining panel columns (own rows); v_j == 1
+    for (int i = max(r0, j) + threadIdx.x; i < r1; i += PT) {
+      const double v = (i == j) ? 1.0 : col[i];
+      for (int c = j + 1; c < jb; ++c) P[(long long)c * ld + i] -= t * v * sw[c];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) tau[j] = t;
+    // diagonal entry becomes beta (owner CTA, after everyone has read alpha via grid.sync below)
+    grid.sync();
+    if (j >= r0 && j < r1 && threadIdx.x == 0) col[j] = beta;
+  }
+  grid.sync();
+  // explicit V and the Gram G = V^T V partials
+  for (int i = r0 + threadIdx.x; i < r1; i += PT) {
+    for (int c = 0; c < jb; ++c) {
+      double v = (i < c) ? 0.0 : (i == c ? 1.0 : P[(long long)c * ld + i]);
+      V[(long long)c * m + i] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NB * NB; e += PT) sG[e] = 0.0;
+  __syncthreads();
+  // Gram partial: each warp takes pairs (a,b) with a<b
+  for (int pr = wid; pr < jb * jb; pr += PT / 32) {
+    int a = pr / jb, b = pr % jb;
+    if (a >= b) continue;
+    double v = 0.0;
+    for (int i = max(r0, b) + lane; i < r1; i += 32) v += V[(long long)a * m + i] * V[(long long)b * m + i];
+    v = warp_sum(v);
+    if (lane == 0) sG[a * NB + b] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NB * NB; e += PT) part[(long long)blockIdx.x * NB * NB + e] = sG[e];
+  grid.sync();
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e < NB * NB; e += PT) {
+      double v = 0.0;
+      for (int b = 0; b < nblk; ++b) v += part[(long long)b * NB * NB + e];
+      sG[e] = v;
+    }
+    __syncthreads();
+    // dlarft (forward, columnwise): T[i,i] = tau_i; T[0:i, i] = -tau_i T[0:i,0:i] G[0:i, i]
+    if (threadIdx.x == 0) {
+      for (int e = 0; e < jb * jb; ++e) T[e] = 0.0;
+      for (int i = 0; i < jb; ++i) {
+        const double ti = tau[i];
+        T[i * jb + i] = ti;
+        for (int r = 0; r < i; ++r) {
+          double v = 0.0;
+          for (int c = r; c < i; ++c) v += T[r * jb + c] * sG[c * NB + i];
+          T[r * jb + i] = -ti * v;
+        }
+      }
+    }
+  }
+}
+
+// V from the stored panel (for dorgqr) -- unit diagonal, zeros above
+__global__ void extract_v_kernel(int m, int jb, const double* P, long long ld, double* V) {
+  long long tot = (long long)m * jb;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(e / m), i = (int)(e % m);
+    V[e] = (i < c) ? 0.0 : (i == c ? 1.0 : P[(long long)c * ld + i]);
+  }
+}
+
+__global__ void eye_kernel(int m, int k, double* Q, long long ld) {
+  long long tot = (long long)m * k;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(e / m), i = (int)(e % m);
+    Q[(long long)c * ld + i] = (i == c) ? 1.0 : 0.0;
+  }
+}
+
+// R (k x n, col-major ld k) = upper triangle of A
+__global__ void extract_r_kernel(int k, int n, const double* A, long long lda, double* R) {
+  long long tot = (long long)k * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(e / k), i = (int)(e % k);
+    R[e] = (i <= c) ? A[(long long)c * lda + i] : 0.0;
+  }
+}
+
+int panel_grid(int m) {
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_qr_kernel, PT, 0);
+    max_blocks = sms * (per_sm > 0 ? (per_sm > 2 ? 2 : per_sm) : 1);
+  }
+  int want = ceil_div(m, 4 * PT);  // >= 1024 rows per CTA before going wider
+  if (want < 1) want = 1;
+  return want < max_blocks ? want : max_blocks;
+}
+
+int launch_panel(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, double* part, cudaStream_t st) {
+  int nblk = panel_grid(m);
+  void* args[] = {&m, &jb, &P, &ld, &tau, &V, &T, &part};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(nblk), dim3(PT), args, 0, st);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+}  // namespace
+
+// Workspace sizes (in doubles) for ttb_geqrf / ttb_orgqr.
+TTB_API long long ttb_qr_workspace(int m, int n) {
+  int k = m < n ? m : n;
+  long long part = (long long)296 * (NB * NB + NB) + 296;
+  long long v = (long long)m * NB;
+  long long w = (long long)(n > k ? n : k) * NB * 2;
+  long long t = (long long)((k + NB - 1) / NB) * NB * NB;
+  return part + v + w + t + 64;
+}
+
+// In-place QR of col-major A (m x n, lda). tau: min(m,n). ws: ttb_qr_workspace doubles;
+// the WY factors T of every panel are kept in ws for a following ttb_orgqr.
+TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, double* tau, double* ws) {
+  if (m < 0 || n < 0 || lda < (m > 1 ? m : 1)) return TTB_EARG;
+  const int k = m < n ? m : n;
+  if (k == 0) return TTB_OK;
+  cudaStream_t st = as_stream(stream);
+  double* part = ws;
+  double* V = part + (long long)296 * (NB * NB + NB) + 296;
+  double* W = V + (long long)m * NB;
+  double* W2 = W + (long long)(n > k ? n : k) * NB;
+  double* Tall = W + (long long)(n > k ? n : k) * NB * 2;
+  for (int j0 = 0; j0 < k; j0 += NB) {
+    const int jb = (k - j0) < NB ? (k - j0) : NB;
+    const int mp = m - j0;
+    double* P = A + (long long)j0 * lda + j0;
+    double* T = Tall + (long long)(j0 / NB) * NB * NB;
+    int rc = launch_panel(mp, jb, P, lda, tau + j0, V, T, part, st);
+    if (rc) return rc;
+    const int n2 = n - j0 - jb;
+    if (n2 > 0) {
+      double* A2 = A + (long long)(j0 + jb) * lda + j0;
+      // Wt (n2 x jb) = A2^T V   [row-major view: A2rm (n2 x mp, ld lda) * Vrm^T (mp x jb)]
+      rc = ttb_dgemm(stream, 0, 1, n2, jb, mp, 1.0, A2, lda, 0, V, mp, 0, 0.0, W, jb, 0, 1);
+      if (rc) return rc;
+      // W2t = Wt * T
+      rc = ttb_dgemm(stream, 0, 0, n2, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
+      if (rc) return rc;
+      // A2rm -= W2t * Vrm
+      rc = ttb_dgemm(stream, 0, 0, n2, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, A2, lda, 0, 1);
+      if (rc) return rc;
+    }
+  }
+  return ttb_last_error();
+}
+
+// Explicit Q (m x kq, col-major ld ldq) from a ttb_geqrf result (same ws), kq <= min(m, n_factored).
+TTB_API int ttb_orgqr(void* stream, int m, int kq, int kf, const double* A, long long lda, double* Q, long long ldq,
+                      double* ws, int n_factored) {
+  if (m < 0 || kq < 0 || kq > m) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  const int k = kf;  // number of reflectors
+  double* V = ws + (long long)296 * (NB * NB + NB) + 296;
+  const int nw = n_factored;
+  double* W = V + (long long)m * NB;
+  double* W2 = W + (long long)nw * NB;
+  double* Tall = W + (long long)nw * NB * 2;
+  {
+    long long tot = (long long)m * kq;
+    int blocks = ceil_div(tot, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    eye_kernel<<<blocks, 256, 0, st>>>(m, kq, Q, ldq);
+  }
+  const int last = ((k - 1) / NB) * NB;
+  for (int j0 = last; j0 >= 0; j0 -= NB) {
+    const int jb = (k - j0) < NB ? (k - j0) : NB;
+    const int mp = m - j0;
+    const int nq = kq - j0;
+    if (nq <= 0) continue;
+    const double* P = A + (long long)j0 * lda + j0;
+    double* T = Tall + (long long)(j0 / NB) * NB * NB;
+    long long tot = (long long)mp * jb;
+    int blocks = ceil_div(tot, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    extract_v_kernel<<<blocks, 256, 0, st>>>(mp, jb, P, lda, V);
+    double* Q2 = Q + (long long)j0 * ldq + j0;
+    // Q2 = (I - V T V^T) Q2 :  Wt = Q2^T V ; W2t = Wt T^T ; Q2rm -= W2t Vrm
+    int rc = ttb_dgemm(stream, 0, 1, nq, jb, mp, 1.0, Q2, ldq, 0, V, mp, 0, 0.0, W, jb, 0, 1);
+    if (rc) return rc;
+    rc = ttb_dgemm(stream, 0, 1, nq, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
+    if (rc) return rc;
+    rc = ttb_dgemm(stream, 0, 0, nq, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, Q2, ldq, 0, 1);
+    if (rc) return rc;
+  }
+  return ttb_last_error();
+}
+
+TTB_API int ttb_extract_r(void* stream, int k, int n, const double* A, long long lda, double* R) {
+  long long tot = (long long)k * n;
+  if (tot == 0) return TTB_OK;
+  int blocks = ceil_div(tot, 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  extract_r_kernel<<<blocks, 256, 0, as_stream(stream)>>>(k, n, A, lda, R);
+  return ttb_last_error();
+}

@@ -1,0 +1,439 @@
+// Dense FP64 solvers: LU with partial pivoting, blocked Cholesky, triangular
+// solves, and the cooperative maxvol kernel that drives TT-cross pivoting.
+#include "common.cuh"
+
+TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                      long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
+                      long long ldc, long long sC, int batch);
+
+namespace {
+
+constexpr int ST = 1024;
+
+// ---------------------------------------------------------------------------
+// LU (getrf, partial pivoting, first-max pivot like LAPACK idamax), single CTA.
+__global__ void __launch_bounds__(ST) lu_kernel(int n, double* A, long long lda, int* piv, int* info) {
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  __shared__ int sp;
+  if (threadIdx.x == 0) *info = 0;
+  for (int k = 0; k < n; ++k) {
+    AbsMax best{-1.0, (long long)1 << 62};
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      AbsMax c{fabs(A[(long long)k * lda + i]), i};
+      best = absmax_merge(best, c);
+    }
+    best = block_absmax(best, sv, si);
+    if (threadIdx.x == 0) {
+      sp = (int)best.i;
+      piv[k] = sp;
+      if (best.v == 0.0 && *info == 0) *info = k + 1;
+    }
+    __syncthreads();
+    const int p = sp;
+    if (p != k)
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        double t = A[(long long)c * lda + k];
+        A[(long long)c * lda + k] = A[(long long)c * lda + p];
+        A[(long long)c * lda + p] = t;
+      }
+    __syncthreads();
+    const double d = A[(long long)k * lda + k];
+    if (d != 0.0)
+      for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[(long long)k * lda + i] /= d;
+    __syncthreads();
+    const int m = n - k - 1;
+    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+      int c = k + 1 + (int)(e / m), i = k + 1 + (int)(e % m);
+      A[(long long)c * lda + i] -= A[(long long)k * lda + i] * A[(long long)c * lda + k];
+    }
+    __syncthreads();
+  }
+}
+
+// Solve op(A) X = B for the LU factors (col-major), one RHS column per thread.
+__global__ void lu_apply_kernel(int n, const double* __restrict__ LU, long long lda, const int* __restrict__ piv,
+                                int nrhs, double* B, long long ldb, int trans) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  double* b = B + (long long)c * ldb;
+  if (!trans) {
+    for (int k = 0; k < n; ++k) {
+      int p = piv[k];
+      if (p != k) { double t = b[k]; b[k] = b[p]; b[p] = t; }
+    }
+    for (int k = 0; k < n; ++k) {  // L y = b (unit lower)
+      double x = b[k];
+      for (int i = k + 1; i < n; ++i) b[i] -= LU[(long long)k * lda + i] * x;
+    }
+    for (int k = n - 1; k >= 0; --k) {  // U x = y
+      double x = b[k] / LU[(long long)k * lda + k];
+      b[k] = x;
+      for (int i = 0; i < k; ++i) b[i] -= LU[(long long)k * lda + i] * x;
+    }
+  } else {
+    // A^T = U^T L^T P^T : U^T y = b, L^T z = y, x = P z
+    for (int k = 0; k < n; ++k) {
+      double s = b[k];
+      for (int i = 0; i < k; ++i) s -= LU[(long long)k * lda + i] * b[i];
+      b[k] = s / LU[(long long)k * lda + k];
+    }
+    for (int k = n - 1; k >= 0; --k) {
+      double s = b[k];
+      for (int i = k + 1; i < n; ++i) s -= LU[(long long)k * lda + i] * b[i];
+      b[k] = s;
+    }
+    for (int k = n - 1; k >= 0; --k) {
+      int p = piv[k];
+      if (p != k) { double t = b[k]; b[k] = b[p]; b[p] = t; }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cholesky panel: factor diagonal block (nb x nb) and solve the rows below, single CTA.
+constexpr int CNB = 64;
+
+__global__ void __launch_bounds__(256) chol_panel_kernel(int n, int j0, double* A, long long lda, int* info) {
+  __shared__ double L11[CNB * CNB];
+  const int nb = min(CNB, n - j0);
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int c = e / nb, i = e % nb;
+    L11[c * CNB + i] = A[(long long)(j0 + c) * lda + j0 + i];
+  }
+  __syncthreads();
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
+    double d = L11[k * CNB + k];
+    if (d <= 0.0 || !isfinite(d)) {
+      if (threadIdx.x == 0) { bad = 1; *info = j0 + k + 1; }
+      __syncthreads();
+      break;
+    }
+    d = sqrt(d);
+    __syncthreads();
+    if (threadIdx.x == 0) L11[k * CNB + k] = d;
+    for (int i = k + 1 + threadIdx.x; i < nb; i += blockDim.x) L11[k * CNB + i] /= d;
+    __syncthreads();
+    const int m = nb - k - 1;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      int c = k + 1 + e / m, i = k + 1 + e % m;
+      if (i >= c) L11[c * CNB + i] -= L11[k * CNB + i] * L11[k * CNB + c];
+    }
+    __syncthreads();
+  }
+  if (bad) return;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int c = e / nb, i = e % nb;
+    if (i >= c) A[(long long)(j0 + c) * lda + j0 + i] = L11[c * CNB + i];
+  }
+  // rows below: x L11^T = a  (each thread one row)
+  for (int r = j0 + nb + threadIdx.x; r < n; r += blockDim.x) {
+    double x[CNB];
+#pragma unroll
+    for (int k = 0; k < CNB; ++k) {
+      if (k < nb) {
+        double s = A[(long long)(j0 + k) * lda + r];
+        for (int q = 0; q < k; ++q) s -= x[q] * L11[q * CNB + k];
+        x[k] = s / L11[k * CNB + k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CNB; ++k)
+      if (k < nb) A[(long long)(j0 + k) * lda + r] = x[k];
+  }
+}
+
+// Solve L L^T x = b with b in shared memory, single CTA, 32-row blocks.
+__global__ void __launch_bounds__(ST) chol_solve_kernel(int n, const double* __restrict__ L, long long lda, double* bg) {
+  extern __shared__ double b[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = bg[i];
+  __syncthreads();
+  // forward
+  for (int b0 = 0; b0 < n; b0 += 32) {
+    const int nb = min(32, n - b0);
+    if (wid == 0) {
+      double v = lane < nb ? b[b0 + lane] : 0.0;
+      for (int j = 0; j < nb; ++j) {
+        double yj = __shfl_sync(0xffffffffu, v, j) / L[(long long)(b0 + j) * lda + b0 + j];
+        if (lane == j) v = yj;
+        if (lane > j && lane < nb) v -= L[(long long)(b0 + j) * lda + b0 + lane] * yj;
+      }
+      if (lane < nb) b[b0 + lane] = v;
+    }
+    __syncthreads();
+    for (int i = b0 + nb + threadIdx.x; i < n; i += blockDim.x) {
+      double s = b[i];
+      for (int j = 0; j < nb; ++j) s -= L[(long long)(b0 + j) * lda + i] * b[b0 + j];
+      b[i] = s;
+    }
+    __syncthreads();
+  }
+  // backward with L^T
+  const int last = ((n - 1) / 32) * 32;
+  for (int b0 = last; b0 >= 0; b0 -= 32) {
+    const int nb = min(32, n - b0);
+    // b[b0+j] -= sum_{i >= b0+nb} L[i, b0+j] x[i]
+    for (int j = wid; j < nb; j += nw) {
+      double s = 0.0;
+      for (int i = b0 + nb + lane; i < n; i += 32) s += L[(long long)(b0 + j) * lda + i] * b[i];
+      s = warp_sum(s);
+      if (lane == 0) b[b0 + j] -= s;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double v = lane < nb ? b[b0 + lane] : 0.0;
+      for (int j = nb - 1; j >= 0; --j) {
+        double xj = __shfl_sync(0xffffffffu, v, j) / L[(long long)(b0 + j) * lda + b0 + j];
+        if (lane == j) v = xj;
+        if (lane < j) v -= L[(long long)(b0 + lane) * lda + b0 + j] * xj;
+      }
+      if (lane < nb) b[b0 + lane] = v;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) bg[i] = b[i];
+}
+
+// ---------------------------------------------------------------------------
+// maxvol (reference maxvol.py): GEPP row choice, C = M inv(M[rows]), greedy swaps.
+constexpr int MT_ = 256;
+constexpr int RMAX = 128;
+
+__global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double* __restrict__ Q, double* W, int* perm,
+                                                      double* C, double* Ainv, double* pv, long long* pi, double tol,
+                                                      int max_iters, int* rows_out, int* status) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  __shared__ double srow[RMAX];
+  __shared__ double sA[RMAX * RMAX / 4];  // holds Ainv when r <= 64
+  const int nblk = gridDim.x;
+  const int chunk = (n + nblk - 1) / nblk;
+  const int i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  // copy + scale
+  AbsMax mx{0.0, 0};
+  for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
+    perm[i] = i;
+    for (int c = 0; c < r; ++c) {
+      double v = Q[(long long)c * n + i];
+      W[(long long)c * n + i] = v;
+      mx.v = fmax(mx.v, fabs(v));
+    }
+  }
+  mx.i = 0;
+  mx = block_absmax(mx, sv, si);
+  if (threadIdx.x == 0) { pv[blockIdx.x] = mx.v; pi[blockIdx.x] = 0; }
+  grid.sync();
+  double scale = 0.0;
+  for (int b = 0; b < nblk; ++b) scale = fmax(scale, pv[b]);
+  grid.sync();
+  // phase 1: Gaussian elimination with partial pivoting, physical row swaps
+  for (int k = 0; k < r; ++k) {
+    AbsMax best{-1.0, (long long)1 << 62};
+    for (int i = max(i0, k) + threadIdx.x; i < i1; i += MT_) best = absmax_merge(best, AbsMax{fabs(W[(long long)k * n + i]), i});
+    best = block_absmax(best, sv, si);
+    if (threadIdx.x == 0) { pv[blockIdx.x] = best.v; pi[blockIdx.x] = best.i; }
+    grid.sync();
+    AbsMax g{-1.0, (long long)1 << 62};
+    for (int b = 0; b < nblk; ++b) g = absmax_merge(g, AbsMax{pv[b], pi[b]});
+    if (g.v <= 1e-14 * fmax(scale, 1e-300)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *status = 1;
+      return;  // uniform across the grid
+    }
+    const int p = (int)g.i;
+    grid.sync();  // everyone has read pv/pi
+    if (p != k && blockIdx.x == 0) {
+      for (int c = threadIdx.x; c < r; c += MT_) {
+        double t = W[(long long)c * n + k];
+        W[(long long)c * n + k] = W[(long long)c * n + p];
+        W[(long long)c * n + p] = t;
+      }
+      if (threadIdx.x == 0) { int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
+    }
+    grid.sync();
+    const double d = W[(long long)k * n + k];
+    for (int i = max(i0, k + 1) + threadIdx.x; i < i1; i += MT_) {
+      double l = W[(long long)k * n + i] / d;
+      W[(long long)k * n + i] = l;
+      for (int c = k + 1; c < r; ++c) W[(long long)c * n + i] -= l * W[(long long)c * n + k];
+    }
+    grid.sync();
+  }
+  // phase 2: Ainv = inv(Q[rows]) by Gauss-Jordan with partial pivoting (block 0), C = Q Ainv
+  if (blockIdx.x == 0) {
+    // augmented [A | I] in W's spare storage is not available; use Ainv buffer (r x 2r, col-major ld r)
+    for (int e = threadIdx.x; e < r * r; e += MT_) {
+      int c = e / r, i = e % r;
+      Ainv[(long long)c * r + i] = Q[(long long)c * n + perm[i]];
+      Ainv[(long long)(c + r) * r + i] = (c == i) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    __shared__ int sp;
+    for (int k = 0; k < r; ++k) {
+      if (threadIdx.x == 0) {
+        int p = k;
+        double bv = fabs(Ainv[(long long)k * r + k]);
+        for (int i = k + 1; i < r; ++i) {
+          double v = fabs(Ainv[(long long)k * r + i]);
+          if (v > bv) { bv = v; p = i; }
+        }
+        sp = p;
+      }
+      __syncthreads();
+      const int p = sp;
+      if (p != k)
+        for (int c = threadIdx.x; c < 2 * r; c += MT_) {
+          double t = Ainv[(long long)c * r + k];
+          Ainv[(long long)c * r + k] = Ainv[(long long)c * r + p];
+          Ainv[(long long)c * r + p] = t;
+        }
+      __syncthreads();
+      const double d = Ainv[(long long)k * r + k];
+      for (int c = threadIdx.x; c < 2 * r; c += MT_) Ainv[(long long)c * r + k] /= d;
+      __syncthreads();
+      for (int e = threadIdx.x; e < r * 2 * r; e += MT_) {
+        int c = e / r, i = e % r;
+        if (i != k && c != k) Ainv[(long long)c * r + i] -= Ainv[(long long)k * r + i] * Ainv[(long long)c * r + k];
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < r; i += MT_)
+        if (i != k) Ainv[(long long)k * r + i] = 0.0;
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  // inverse sits in columns r..2r-1
+  const double* Ai = Ainv + (long long)r * r;
+  const bool in_smem = r <= 64;
+  if (in_smem) {
+    for (int e = threadIdx.x; e < r * r; e += MT_) sA[e] = Ai[e];
+    __syncthreads();
+  }
+  for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
+    for (int c = 0; c < r; ++c) {
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s += Q[(long long)k * n + i] * (in_smem ? sA[c * r + k] : Ai[(long long)c * r + k]);
+      C[(long long)c * n + i] = s;
+    }
+  }
+  int* rows = perm;  // rows[0..r) live in perm[0..r)
+  grid.sync();
+  // phase 3: greedy swaps
+  for (int it = 0; it < max_iters; ++it) {
+    AbsMax best{-1.0, (long long)1 << 62};
+    for (int i = i0 + threadIdx.x; i < i1; i += MT_)
+      for (int c = 0; c < r; ++c)
+        best = absmax_merge(best, AbsMax{fabs(C[(long long)c * n + i]), (long long)i * r + c});
+    best = block_absmax(best, sv, si);
+    if (threadIdx.x == 0) { pv[blockIdx.x] = best.v; pi[blockIdx.x] = best.i; }
+    grid.sync();
+    AbsMax g{-1.0, (long long)1 << 62};
+    for (int b = 0; b < nblk; ++b) g = absmax_merge(g, AbsMax{pv[b], pi[b]});
+    if (g.v <= tol) break;
+    const int bi = (int)(g.i / r), bj = (int)(g.i % r);
+    for (int c = threadIdx.x; c < r; c += MT_) srow[c] = C[(long long)c * n + bi] - (c == bj ? 1.0 : 0.0);
+    const double pivv = C[(long long)bj * n + bi];
+    __syncthreads();
+    grid.sync();  // all rows read before anyone updates (also protects pv/pi)
+    for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
+      const double f = C[(long long)bj * n + i] / pivv;
+      for (int c = 0; c < r; ++c) C[(long long)c * n + i] -= f * srow[c];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rows[bj] = bi;
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int a = 0; a < r; ++a) rows_out[a] = rows[a];
+    for (int a = 1; a < r; ++a) {
+      int v = rows_out[a], b = a - 1;
+      while (b >= 0 && rows_out[b] > v) { rows_out[b + 1] = rows_out[b]; --b; }
+      rows_out[b + 1] = v;
+    }
+    *status = 0;
+  }
+}
+
+int maxvol_grid(int n) {
+  static int maxb = 0;
+  if (!maxb) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, maxvol_kernel, MT_, 0);
+    maxb = sms * (per > 0 ? 1 : 1);
+  }
+  int want = ceil_div(n, 2 * MT_);
+  if (want < 1) want = 1;
+  return want < maxb ? want : maxb;
+}
+
+}  // namespace
+
+// LU factorization (in place, col-major) + solve of op(A) X = B (B col-major n x nrhs, overwritten).
+TTB_API int ttb_lu_solve(void* stream, int n, double* A, long long lda, int* piv, int nrhs, double* B, long long ldb,
+                         int trans, int* info) {
+  if (n < 1 || nrhs < 0) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  lu_kernel<<<1, ST, 0, st>>>(n, A, lda, piv, info);
+  if (nrhs > 0) lu_apply_kernel<<<ceil_div(nrhs, 128), 128, 0, st>>>(n, A, lda, piv, nrhs, B, ldb, trans);
+  return ttb_last_error();
+}
+
+// Cholesky factorization of SPD col-major A (lower triangle used/overwritten). info: 0 ok, k>0 failed pivot.
+TTB_API int ttb_potrf(void* stream, int n, double* A, long long lda, int* info) {
+  if (n < 1) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(info, 0, sizeof(int), st);
+  for (int j0 = 0; j0 < n; j0 += CNB) {
+    const int nb = n - j0 < CNB ? n - j0 : CNB;
+    chol_panel_kernel<<<1, 256, 0, st>>>(n, j0, A, lda, info);
+    const int m2 = n - j0 - nb;
+    if (m2 > 0) {
+      const double* Lp = A + (long long)j0 * lda + j0 + nb;  // col-major m2 x nb == row-major nb x m2 (ld lda)
+      double* A22 = A + (long long)(j0 + nb) * lda + j0 + nb;
+      int rc = ttb_dgemm(stream, 1, 0, m2, m2, nb, -1.0, Lp, lda, 0, Lp, lda, 0, 1.0, A22, lda, 0, 1);
+      if (rc) return rc;
+    }
+  }
+  return ttb_last_error();
+}
+
+TTB_API int ttb_potrs(void* stream, int n, const double* L, long long lda, double* b) {
+  if (n < 1) return TTB_EARG;
+  size_t smem = (size_t)n * sizeof(double);
+  if (smem > 200 * 1024) return TTB_EARG;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  chol_solve_kernel<<<1, ST, smem, as_stream(stream)>>>(n, L, lda, b);
+  return ttb_last_error();
+}
+
+TTB_API long long ttb_maxvol_workspace(int n, int r) {
+  // W, C (n*r each), Ainv (2 r^2), partials (2 * 296)
+  return 2LL * n * r + 2LL * r * r + 2 * 296 + 64;
+}
+
+// rows_out: r sorted row indices of a tol-dominant submatrix of Q (n x r col-major, ld n), n > r.
+// iws: n + 1 ints (perm + status). Returns TTB_ESINGULAR when Q is column-rank deficient.
+TTB_API int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, int max_iters, int* rows_out, double* ws,
+                       int* iws) {
+  if (r < 1 || r > RMAX || n <= r) return TTB_EARG;
+  double* W = ws;
+  double* C = W + (long long)n * r;
+  double* Ainv = C + (long long)n * r;
+  double* pv = Ainv + 2LL * r * r;
+  long long* pi = reinterpret_cast<long long*>(pv + 296);
+  int* perm = iws;
+  int* status = iws + n;
+  int nblk = maxvol_grid(n);
+  void* args[] = {&n, &r, &Q, &W, &perm, &C, &Ainv, &pv, &pi, &tol, &max_iters, &rows_out, &status};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)maxvol_kernel, dim3(nblk), dim3(MT_), args, 0, as_stream(stream));
+  return e == cudaSuccess ? 0 : (int)e;
+}

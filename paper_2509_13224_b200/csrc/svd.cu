@@ -1,0 +1,148 @@
+// One-sided (Hestenes) Jacobi SVD of small square FP64 matrices.
+//
+// Used on the R factor of a Householder QR (so only n x n, n = TT rank, is
+// rotated). Round-robin (tournament) ordering: every round is n/2 disjoint
+// column pairs, one warp per pair, warp-shuffle reductions for the 2x2 Gram
+// entries. n <= 64 runs entirely in shared memory; larger n keeps A and V in
+// global memory (L2 resident) with the same schedule.
+#include "common.cuh"
+
+namespace {
+
+constexpr int JT = 1024;  // threads per CTA
+
+__device__ __forceinline__ int rr_index(int k, int r, int N) {
+  return k == 0 ? 0 : ((k - 1 + r) % (N - 1)) + 1;
+}
+
+// A (n x n col-major, ld n) -> columns mutually orthogonal; V accumulates rotations.
+// Returns number of sweeps in *sweeps_out (thread 0).
+__device__ void jacobi_core(int n, double* A, double* V, int* flag, int max_sweeps, double tol, int* sweeps_out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int N = (n + 1) & ~1;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < N - 1; ++r) {
+      for (int pr = wid; pr < N / 2; pr += nw) {
+        int p = rr_index(pr, r, N), q = rr_index(N - 1 - pr, r, N);
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q >= n) continue;
+        double* ap = A + (long long)p * n;
+        double* aq = A + (long long)q * n;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          double x = ap[i], y = aq[i];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+        if (lane == 0) *flag = 1;
+        double zeta = (be - al) / (2.0 * ga);
+        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int i = lane; i < n; i += 32) {
+          double x = ap[i], y = aq[i];
+          ap[i] = c * x - s * y;
+          aq[i] = s * x + c * y;
+        }
+        double* vp = V + (long long)p * n;
+        double* vq = V + (long long)q * n;
+        for (int i = lane; i < n; i += 32) {
+          double x = vp[i], y = vq[i];
+          vp[i] = c * x - s * y;
+          vq[i] = s * x + c * y;
+        }
+      }
+      __syncthreads();
+    }
+    int f = *flag;
+    __syncthreads();
+    if (!f) break;
+  }
+  if (threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+// batch of matrices along blockIdx.x; A overwritten with U (col-major), S descending.
+template <bool SMEM>
+__global__ void __launch_bounds__(JT) jacobi_kernel(int n, double* Ag, long long strideA, double* Sg, long long strideS,
+                                                    double* Ug, double* Vg, long long strideUV, double* work,
+                                                    int max_sweeps, double tol, int* info) {
+  extern __shared__ double dyn[];
+  __shared__ int flag, nsweep;
+  const long long b = blockIdx.x;
+  double* Ain = Ag + b * strideA;
+  double* U = Ug + b * strideUV;
+  double* Vout = Vg + b * strideUV;
+  double* S = Sg + b * strideS;
+  const long long nn = (long long)n * n;
+  double *A, *V;
+  if (SMEM) {
+    A = dyn;
+    V = dyn + nn;
+  } else {
+    A = work + b * (2 * nn + n);
+    V = A + nn;
+  }
+  for (long long e = threadIdx.x; e < nn; e += blockDim.x) {
+    A[e] = Ain[e];
+    V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  jacobi_core(n, A, V, &flag, max_sweeps, tol, &nsweep);
+  __syncthreads();
+  // column norms, descending order rank (stable by index)
+  double* sig = SMEM ? (dyn + 2 * nn) : (work + b * (2 * nn + n) + 2 * nn);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < n; j += nw) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += A[(long long)j * n + i] * A[(long long)j * n + i];
+    s = warp_sum(s);
+    if (lane == 0) sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double sj = sig[j];
+    int rank = 0;
+    for (int k = 0; k < n; ++k) {
+      double sk = sig[k];
+      rank += (sk > sj) || (sk == sj && k < j);
+    }
+    S[rank] = sj;
+    double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+    for (int i = 0; i < n; ++i) {
+      U[(long long)rank * n + i] = A[(long long)j * n + i] * inv;
+      Vout[(long long)rank * n + i] = V[(long long)j * n + i];
+    }
+  }
+  if (threadIdx.x == 0 && info) info[b] = nsweep;
+}
+
+}  // namespace
+
+// SVD of `batch` square n x n col-major matrices A (= U diag(S) V^T).
+// U, V: n x n col-major per matrix; S descending. work: batch*(2n^2+n) doubles when n > 64.
+TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, double* S, long long strideS, double* U,
+                           double* V, long long strideUV, int batch, double* work, int* info) {
+  if (n < 1 || batch < 1) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  const int max_sweeps = 60;
+  const double tol = 4.0e-16 * (n > 16 ? sqrt((double)n) : 4.0);
+  int threads = n >= 64 ? JT : ((n + 1) / 2 * 32 > 1024 ? 1024 : ((n + 1) / 2) * 32);
+  if (threads < 32) threads = 32;
+  if (n <= 64) {
+    size_t smem = ((size_t)2 * n * n + n) * sizeof(double);
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+      cfg = true;
+    }
+    jacobi_kernel<true><<<batch, threads, smem, st>>>(n, A, strideA, S, strideS, U, V, strideUV, nullptr, max_sweeps,
+                                                      tol, info);
+  } else {
+    if (!work) return TTB_EARG;
+    jacobi_kernel<false><<<batch, JT, 0, st>>>(n, A, strideA, S, strideS, U, V, strideUV, work, max_sweeps, tol, info);
+  }
+  return ttb_last_error();
+}

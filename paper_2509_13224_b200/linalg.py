@@ -1,0 +1,252 @@
+"""Device FP64 linear algebra on torch CUDA tensors, computed by libttiga_b200.so.
+
+Layout notes: torch tensors are row-major. A "col-major m x n" matrix is held
+as a contiguous torch tensor of shape (n, m) (its transpose), which is what the
+LAPACK-convention kernels (QR, Jacobi SVD, LU, Cholesky, maxvol) consume.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from ._lib import call, call_raw, device, ptr
+
+F64 = torch.float64
+I32 = torch.int32
+
+
+class LinAlgError(np.linalg.LinAlgError):
+    """Device counterpart of numpy's LinAlgError."""
+
+
+def empty(*shape, dtype=F64):
+    return torch.empty(*shape, dtype=dtype, device=device())
+
+
+def zeros(*shape, dtype=F64):
+    return torch.zeros(*shape, dtype=dtype, device=device())
+
+
+def _rows(A):
+    """Row-major 2-D operand with unit column stride."""
+    if A.dim() != 2:
+        raise ValueError("expected a matrix")
+    if A.stride(1) != 1 or (A.shape[0] > 1 and A.stride(0) < A.shape[1]):
+        A = A.contiguous()
+    return A
+
+
+def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
+    """out = alpha op(A) op(B) + beta out (row-major, FP64 DMMA kernel)."""
+    A = _rows(A)
+    B = _rows(B)
+    M, K = (A.shape[1], A.shape[0]) if tA else (A.shape[0], A.shape[1])
+    K2, N = (B.shape[1], B.shape[0]) if tB else (B.shape[0], B.shape[1])
+    if K != K2:
+        raise ValueError(f"gemm inner dims {K} != {K2}")
+    if out is None:
+        out = empty(M, N)
+        beta = 0.0
+    elif out.shape != (M, N) or out.stride(1) != 1:
+        raise ValueError("bad gemm output")
+    if M and N:
+        call("ttb_dgemm", int(tA), int(tB), M, N, K, float(alpha), ptr(A), max(A.stride(0), 1), 0, ptr(B),
+             max(B.stride(0), 1), 0, float(beta), ptr(out), max(out.stride(0), 1), 0, 1)
+    return out
+
+
+def permute(X, perm):
+    """Materialized X.permute(perm) (row-major), by the native transpose kernel."""
+    perm = tuple(int(p) for p in perm)
+    if perm == tuple(range(X.dim())):
+        return X.contiguous()
+    X = X.contiguous()
+    out = empty(*[X.shape[p] for p in perm])
+    if X.numel():
+        dims = (C.c_longlong * X.dim())(*X.shape)
+        pm = (C.c_int * X.dim())(*perm)
+        call("ttb_permute", X.dim(), dims, pm, ptr(X), ptr(out))
+    return out
+
+
+def tdot(A, B, axes):
+    """np.tensordot(A, B, axes) on the device: permute to matrix form + one GEMM."""
+    ia, ib = axes
+    ia = [a % A.dim() for a in (ia if isinstance(ia, (list, tuple)) else [ia])]
+    ib = [b % B.dim() for b in (ib if isinstance(ib, (list, tuple)) else [ib])]
+    fa = [k for k in range(A.dim()) if k not in ia]
+    fb = [k for k in range(B.dim()) if k not in ib]
+    M = int(np.prod([A.shape[k] for k in fa], dtype=np.int64))
+    K = int(np.prod([A.shape[k] for k in ia], dtype=np.int64))
+    N = int(np.prod([B.shape[k] for k in fb], dtype=np.int64))
+    if ia == list(range(len(ia))):
+        Am, tA = A.contiguous().reshape(K, M), True
+    else:
+        Am, tA = permute(A, fa + ia).reshape(M, K), False
+    if ib == list(range(B.dim() - len(ib), B.dim())) and fb == list(range(len(fb))):
+        Bm, tB = B.contiguous().reshape(N, K), True
+    else:
+        Bm, tB = permute(B, ib + fb).reshape(K, N), False
+    out = gemm(Am, Bm, tA=tA, tB=tB)
+    return out.reshape([A.shape[k] for k in fa] + [B.shape[k] for k in fb])
+
+
+def dot(x, y=None, sqrt=False):
+    """Deterministic device dot product / squared norm; returns a 0-d device tensor."""
+    x = x.contiguous().reshape(-1)
+    out = empty(1)
+    part = empty(320)
+    call("ttb_dot", x.numel(), ptr(x), None if y is None else ptr(y.contiguous().reshape(-1)), ptr(out), ptr(part),
+         int(sqrt))
+    return out[0]
+
+
+def nrm2(x):
+    return dot(x, None, sqrt=True)
+
+
+# ---------------------------------------------------------------------------
+# QR
+
+def qr_colmajor(Acm, m, n, want_q=True, want_r=True):
+    """Householder QR of a col-major m x n matrix held as torch (n, m) (consumed).
+
+    Returns (Qt, Rt): Qt = torch (k, m) == col-major Q (m x k); Rt = torch (n, k) == col-major R (k x n).
+    """
+    k = min(m, n)
+    if k == 0:
+        return empty(0, m), empty(n, 0)
+    ws = empty(int(call_raw("ttb_qr_workspace", m, n)))
+    tau = empty(k)
+    call("ttb_geqrf", m, n, ptr(Acm), m, ptr(tau), ptr(ws))
+    Qt = Rt = None
+    if want_r:
+        Rt = empty(n, k)
+        call("ttb_extract_r", k, n, ptr(Acm), m, ptr(Rt))
+    if want_q:
+        Qt = empty(k, m)
+        call("ttb_orgqr", m, k, k, ptr(Acm), m, ptr(Qt), m, ptr(ws), n)
+    return Qt, Rt
+
+
+def qr(X):
+    """np.linalg.qr(X) (reduced) for a row-major matrix: returns (Q (m x k), R (k x n)) views."""
+    m, n = X.shape
+    Qt, Rt = qr_colmajor(permute(X, (1, 0)), m, n)
+    return Qt.t(), Rt.t()
+
+
+# ---------------------------------------------------------------------------
+# SVD
+
+def _jacobi(Rcm, n):
+    """SVD of a col-major n x n matrix held as torch (n, n): returns (U_mem, S, V_mem) col-major."""
+    S = empty(n)
+    U = empty(n, n)
+    V = empty(n, n)
+    work = empty(2 * n * n + n) if n > 64 else None
+    call("ttb_svd_jacobi", n, ptr(Rcm), n * n, ptr(S), n, ptr(U), ptr(V), n * n, 1, ptr(work), None)
+    return U, S, V
+
+
+class SVDFactors:
+    """Lazy thin SVD X = U diag(S) Vt; U columns are formed only for the kept rank."""
+
+    def __init__(self, X):
+        X = X.contiguous()
+        m, n = X.shape
+        self.m, self.n = m, n
+        self.tall = m >= n
+        if self.tall:
+            Qt, Rt = qr_colmajor(permute(X, (1, 0)), m, n)
+            self.Qt = Qt                      # (n, m)  == col-major Q (m x n)
+            self.UR, self.S, self.V = _jacobi(Rt.contiguous(), n)
+        else:
+            Qt, Rt = qr_colmajor(X.clone(), n, m)  # QR of X^T (n x m)
+            self.Qt = Qt                      # (m, n) == col-major Q (n x m)
+            self.UR, self.S, self.V = _jacobi(Rt.contiguous(), m)
+
+    def s_host(self):
+        return self.S.cpu().numpy()
+
+    def U(self, r):
+        """First r left singular vectors, row-major (m x r)."""
+        if self.tall:
+            return gemm(self.Qt, self.UR[:r], tA=True, tB=True)
+        return self.V[:r].t().contiguous()
+
+    def Vt(self, r):
+        """First r right singular vectors as rows (r x n)."""
+        if self.tall:
+            return self.V[:r].contiguous()
+        return gemm(self.UR[:r], self.Qt)
+
+
+def svd(X):
+    """np.linalg.svd(X, full_matrices=False) on the device: (U, S, Vt)."""
+    f = SVDFactors(X)
+    k = min(f.m, f.n)
+    return f.U(k), f.S, f.Vt(k)
+
+
+# ---------------------------------------------------------------------------
+# solvers
+
+def solve(A, B):
+    """np.linalg.solve(A, B) with LU + partial pivoting on the device."""
+    n = A.shape[0]
+    if A.shape != (n, n):
+        raise ValueError("square matrix expected")
+    vec = B.dim() == 1
+    Bm = B.reshape(n, 1) if vec else B
+    LU = A.contiguous().clone()          # col-major memory of A^T
+    Bcm = permute(Bm, (1, 0))            # col-major B
+    piv = empty(n, dtype=I32)
+    info = empty(1, dtype=I32)
+    call("ttb_lu_solve", n, ptr(LU), n, ptr(piv), Bm.shape[1], ptr(Bcm), n, 1, ptr(info))
+    if int(info.item()) != 0:
+        raise LinAlgError("Singular matrix")
+    X = Bcm.t()
+    return X.reshape(n) if vec else X
+
+
+def cho_solve_or_lu(Bm, b):
+    """scipy cho_factor/cho_solve with fallback to a pivoted LU solve (reference amen.py:388-393)."""
+    n = Bm.shape[0]
+    L = Bm.contiguous().clone()
+    info = empty(1, dtype=I32)
+    call("ttb_potrf", n, ptr(L), n, ptr(info))
+    if int(info.item()) == 0 and n * 8 <= 200 * 1024:
+        x = b.contiguous().clone().reshape(-1)
+        call("ttb_potrs", n, ptr(L), n, ptr(x))
+        return x
+    return solve(Bm, b.reshape(-1))
+
+
+class MaxvolError(np.linalg.LinAlgError):
+    """Mirror of reference MaxvolError (tensor_train/maxvol.py:15)."""
+
+
+def maxvol_colmajor(Qcm, n, r, tol=1.01, max_iters=200):
+    """Sorted maxvol rows of a col-major n x r matrix (torch (r, n)); host int64 array."""
+    if n <= r:
+        return np.arange(n)
+    ws = empty(int(call_raw("ttb_maxvol_workspace", n, r)))
+    iws = empty(n + 1, dtype=I32)
+    rows = empty(r, dtype=I32)
+    call("ttb_maxvol", n, r, ptr(Qcm.contiguous()), float(tol), int(max_iters), ptr(rows), ptr(ws), ptr(iws))
+    if int(iws[n].item()) != 0:
+        raise MaxvolError("degenerate pivot: matrix has deficient column rank")
+    return rows.cpu().numpy().astype(np.int64)
+
+
+def maxvol(M, tol=1.01, max_iters=200):
+    """Reference maxvol(M) for a row-major (n x r) device matrix."""
+    n, r = M.shape
+    if tol < 1.0:
+        raise ValueError("tol must be at least 1")
+    return maxvol_colmajor(permute(M, (1, 0)), n, r, tol, max_iters)

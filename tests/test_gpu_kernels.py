@@ -1,0 +1,119 @@
+"""Kernel-level parity: native FP64 kernels vs numpy on seeded inputs (GPU only)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def la():
+    from paper_2509_13224_b200 import linalg
+    return linalg
+
+
+def T(x):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda")
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 64, 64), (130, 70, 33), (300, 257, 129),
+                                   (1000, 40, 5000), (513, 1024, 96), (40, 32, 70000)])
+@pytest.mark.parametrize("tA,tB", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm(la, M, N, K, tA, tB):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((K, M) if tA else (M, K))
+    B = rng.standard_normal((N, K) if tB else (K, N))
+    C0 = rng.standard_normal((M, N))
+    ref = 0.5 * ((A.T if tA else A) @ (B.T if tB else B)) - 2.0 * C0
+    out = T(C0)
+    la.gemm(T(A), T(B), tA=tA, tB=tB, alpha=0.5, beta=-2.0, out=out)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
+
+
+def test_permute_and_tdot(la):
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((3, 4, 5, 6))
+    for perm in [(0, 1, 2, 3), (3, 2, 1, 0), (1, 0, 3, 2), (2, 0, 3, 1)]:
+        assert np.array_equal(la.permute(T(X), perm).cpu().numpy(), X.transpose(perm))
+    Y = rng.standard_normal((6, 5, 7))
+    got = la.tdot(T(X), T(Y), ([3, 2], [0, 1])).cpu().numpy()
+    assert np.allclose(got, np.tensordot(X, Y, ([3, 2], [0, 1])), atol=1e-12)
+    got = la.tdot(T(X), T(rng.standard_normal((3, 2))), ([0], [0])).cpu().numpy()
+    assert got.shape == (4, 5, 6, 2)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 3), (3, 5), (64, 64), (200, 37), (1000, 70), (40, 300), (5000, 33),
+                                 (20000, 100)])
+def test_qr(la, m, n):
+    rng = np.random.default_rng(m + n)
+    X = rng.standard_normal((m, n))
+    Q, R = la.qr(T(X))
+    Q, R = Q.cpu().numpy(), R.cpu().numpy()
+    k = min(m, n)
+    assert Q.shape == (m, k) and R.shape == (k, n)
+    assert np.abs(Q @ R - X).max() <= 1e-12 * np.abs(X).max() * np.sqrt(n)
+    assert np.abs(Q.T @ Q - np.eye(k)).max() <= 1e-13 * np.sqrt(m)
+    assert np.allclose(np.triu(R), R)
+    Rn = np.linalg.qr(X)[1]
+    assert np.allclose(np.abs(np.diag(R)), np.abs(np.diag(Rn)), rtol=1e-10)
+
+
+def test_qr_rank_deficient(la):
+    rng = np.random.default_rng(5)
+    B = rng.standard_normal((50, 3))
+    X = np.hstack([B, B])  # rank 3
+    Q, R = la.qr(T(X))
+    assert np.abs(Q.cpu().numpy() @ R.cpu().numpy() - X).max() < 1e-12
+    Z = np.zeros((20, 4))
+    Q, R = la.qr(T(Z))
+    assert np.all(R.cpu().numpy() == 0)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (6, 4), (4, 6), (64, 64), (100, 65), (65, 100), (2000, 120), (300, 300)])
+def test_svd(la, m, n):
+    rng = np.random.default_rng(10 * m + n)
+    X = rng.standard_normal((m, n)) * np.logspace(0, -8, n)[None, :]
+    U, S, Vt = la.svd(T(X))
+    U, S, Vt = U.cpu().numpy(), S.cpu().numpy(), Vt.cpu().numpy()
+    Sn = np.linalg.svd(X, compute_uv=False)
+    assert np.allclose(S, Sn, rtol=1e-12, atol=1e-14 * Sn[0])
+    assert np.abs((U * S) @ Vt - X).max() <= 1e-13 * Sn[0] * np.sqrt(max(m, n))
+    k = min(m, n)
+    assert np.abs(U.T @ U - np.eye(k)).max() < 1e-12
+    assert np.all(np.diff(S) <= 0)
+
+
+def test_lu_and_cholesky(la):
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 64, 300, 1000):
+        A = rng.standard_normal((n, n)) + n * np.eye(n) * 0.1
+        B = rng.standard_normal((n, 7))
+        X = la.solve(T(A), T(B)).cpu().numpy()
+        assert np.abs(A @ X - B).max() <= 1e-10 * np.abs(B).max() * n
+        S = A @ A.T + n * np.eye(n)
+        b = rng.standard_normal(n)
+        x = la.cho_solve_or_lu(T(S), T(b)).cpu().numpy()
+        assert np.allclose(x, np.linalg.solve(S, b), rtol=1e-10, atol=1e-12)
+    S = np.diag([1.0, -2.0, 3.0])
+    x = la.cho_solve_or_lu(T(S), T(np.ones(3))).cpu().numpy()
+    assert np.allclose(x, [1.0, -0.5, 1.0 / 3.0])
+
+
+def test_maxvol(la, golden):
+    g = golden("tensor_train.npz")
+    assert np.array_equal(la.maxvol(T(g["maxvol_M"])), g["maxvol_sel"])
+    v = np.array([10.0, 0.0])
+    Md = np.vstack([v, v, [0.0, 10.0], [0.1, 0.2], [0.3, 0.1]])
+    assert np.array_equal(la.maxvol(T(Md)), g["maxvol_dup_sel"])
+    rng = np.random.default_rng(20)
+    from oracle.cross import maxvol as omv
+    for n, r in [(50, 5), (2000, 20), (30000, 40)]:
+        M = rng.standard_normal((n, r))
+        assert np.array_equal(la.maxvol(T(M)), omv(M))
+    M = np.zeros((10, 3))
+    M[:, 0] = np.arange(10)
+    M[:, 1] = 2 * np.arange(10)
+    M[:, 2] = np.arange(10) + 1
+    with pytest.raises(la.MaxvolError):
+        la.maxvol(T(M))

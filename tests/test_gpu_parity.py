@@ -1,0 +1,205 @@
+"""CUDA path vs reference golden vectors and the CPU oracle (GPU only).
+
+Tolerances (FP64): TT arithmetic / rounding 1e-12 relative; cross-interpolated
+objects at eps_cross = 1e-10..1e-11 within 1e-9 relative Frobenius; solver
+outputs within the solve tolerance scaled by the operator conditioning (stated
+per test); ranks equal or within +-2 of the oracle's.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2509_13224_b200 as pkg
+    from paper_2509_13224_b200 import assembly, driver, geometry, splines, tensor_train
+    return type("NS", (), dict(tt=tensor_train, asm=assembly, drv=driver, geo=geometry, spl=splines))
+
+
+# ---------------------------------------------------------------- splines / geometry
+
+def test_basis_tables_vs_golden(P, golden):
+    g = golden("splines.npz")
+    for c in range(int(g["n_cases"])):
+        w = g[f"c{c}_w"]
+        b = P.spl.Basis1D(P.spl.KnotVector(g[f"c{c}_knots"], int(g[f"c{c}_deg"])), w if w.size else None)
+        V, D = P.spl.tabulate(b, g[f"c{c}_x"])
+        assert np.abs(V - g[f"c{c}_V"]).max() <= 1e-14
+        assert np.abs(D - g[f"c{c}_D"]).max() <= 1e-12 * max(1.0, np.abs(g[f"c{c}_D"]).max())
+
+
+@pytest.mark.parametrize("name", ["unit_cube", "lshape", "ring", "closed_hemisphere", "opened_hemisphere",
+                                  "hyperboloid", "quarter_torus"])
+def test_geometry_vs_golden(P, golden, name):
+    g = golden("geometry.npz")
+    patch = P.geo.make_geometry(name)
+    assert np.allclose(patch.control_points, g[f"{name}_ctrl"], atol=1e-15)
+    ev = P.geo.GridEvaluator(patch, list(g[f"{name}_axes"]))
+    idx = g[f"{name}_idx"]
+    J, x = ev.jacobians(idx)
+    det, R = ev.metric(idx)
+    assert np.abs(J.cpu().numpy() - g[f"{name}_jac"]).max() <= 1e-13
+    assert np.abs(x.cpu().numpy() - g[f"{name}_pts"]).max() <= 1e-14
+    assert np.abs(det.cpu().numpy() - g[f"{name}_det"]).max() <= 1e-13
+    assert np.abs(R.cpu().numpy() - g[f"{name}_R"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["quarter_cylinder", "deformed_cube", "random_cube"])
+def test_extension_geometries_vs_oracle(P, name):
+    from oracle import patch as OP
+    op = OP.build_patch(name)
+    gp = P.geo.make_geometry(name)
+    assert np.allclose(gp.control_points, op.ctrl, atol=1e-13)
+    rng = np.random.default_rng(5)
+    axes = [np.sort(rng.uniform(0.01, 0.99, 9)) for _ in range(3)]
+    idx = rng.integers(0, 9, (200, 3))
+    det_o, R_o = OP.TensorGridEval(op, axes).det_metric(idx)
+    det, R = P.geo.GridEvaluator(gp, axes).metric(idx)
+    assert np.abs(det.cpu().numpy() - det_o).max() <= 1e-12
+    assert np.abs(R.cpu().numpy() - R_o).max() <= 1e-11
+
+
+# ---------------------------------------------------------------- tensor train
+
+def test_round_matvec_vs_golden(P, golden):
+    g = golden("tensor_train.npz")
+    t = P.tt.tt_from_full(g["round_X"])
+    for e in (1e-2, 1e-6, 1e-10):
+        r = P.tt.tt_round(t, e)
+        assert r.ranks == tuple(g[f"round_{e:g}_ranks"])
+        assert np.abs(r.full() - g[f"round_{e:g}_full"]).max() <= 1e-12
+    A = P.tt.TtMatrix([g[f"mv_A{k}"] for k in range(3)])
+    x = P.tt.TtTensor([g[f"mv_x{k}"] for k in range(3)])
+    y = P.tt.tt_matvec(A, x)
+    assert rel(y.full(), g["mv_y_full"]) <= 1e-13
+    yr = P.tt.tt_round(y, 1e-8)
+    assert yr.ranks == tuple(g["mv_round_ranks"])
+    assert rel(yr.full(), g["mv_round_full"]) <= 1e-12
+    assert abs(P.tt.tt_norm(y) - float(g["mv_norm"])) <= 1e-12 * float(g["mv_norm"])
+
+
+def test_arithmetic_densification(P):
+    rng = np.random.default_rng(2)
+    for _ in range(6):
+        shape = tuple(int(v) for v in rng.integers(3, 9, 3))
+        a = P.tt.TtTensor.random(shape, rng.integers(1, 4, 2), rng)
+        b = P.tt.TtTensor.random(shape, rng.integers(1, 4, 2), rng)
+        s = max(P.tt.tt_norm(a), P.tt.tt_norm(b))
+        assert np.abs(P.tt.tt_add(a, b).full() - (a.full() + b.full())).max() <= 1e-12 * s
+        assert np.abs(P.tt.tt_scale(a, 3.25).full() - 3.25 * a.full()).max() <= 1e-12 * s
+        assert np.abs(P.tt.tt_matvec(P.tt.TtMatrix.identity(shape), a).full() - a.full()).max() <= 1e-12 * s
+        assert abs(P.tt.tt_dot(a, a) - P.tt.tt_norm(a) ** 2) <= 1e-12 * P.tt.tt_norm(a) ** 2
+
+
+def test_banded_matvec_equals_dense(P):
+    rng = np.random.default_rng(9)
+    n, h = 12, 2
+    cores = []
+    for r0, r1 in ((1, 3), (3, 2), (2, 1)):
+        G = rng.standard_normal((r0, n, n, r1))
+        i, j = np.indices((n, n))
+        G[:, np.abs(i - j) > h, :] = 0.0
+        cores.append(G)
+    Ad = P.tt.TtMatrix(cores)
+    Ab = P.tt.TtMatrix.banded_from_dense_cores(cores, h)
+    x = P.tt.TtTensor.random((n, n, n), (2, 3), rng)
+    assert rel(P.tt.tt_matvec(Ab, x).full(), P.tt.tt_matvec(Ad, x).full()) <= 1e-14
+    assert rel(Ab.full(), Ad.full()) == 0.0
+    assert rel(Ab.transpose().full(), Ad.full().T) == 0.0
+    r1 = P.tt.tt_round(Ab + Ab, 1e-12)
+    assert rel(r1.full(), 2 * Ad.full()) <= 1e-12
+
+
+def test_cross_vs_golden(P, golden):
+    g = golden("tensor_train.npz")
+    n = (16, 12, 10)
+
+    def f(idx):
+        x = idx.to(torch.float64)
+        return (torch.sin(x[:, 0] + 1.0) * torch.cos(0.3 * x[:, 1]) * (x[:, 2] + 1.0)
+                + torch.exp(-0.1 * x[:, 0]) * (x[:, 1] + 0.5) * torch.cos(0.2 * x[:, 2]))
+
+    res = P.tt.tt_cross(P.tt.CrossOracle(f, n), 1e-10, rng=np.random.default_rng(7))
+    assert res.ranks == tuple(g["cross_ranks"])
+    assert res.n_evals == int(g["cross_nevals"])
+    assert rel(res.tensor.full(), g["cross_ref"]) <= 1e-9
+    assert rel(res.tensor.full(), g["cross_full"]) <= 1e-10
+
+
+def test_cross_separable_exact(P):
+    def f(idx):
+        x = idx.to(torch.float64)
+        return torch.exp(-0.3 * x[:, 0]) * (x[:, 1] + 1.0) * torch.cos(x[:, 2])
+
+    res = P.tt.tt_cross(P.tt.CrossOracle(f, (16, 16, 16)), 1e-10, rng=np.random.default_rng(4))
+    grid = np.indices((16, 16, 16)).reshape(3, -1).T
+    ref = (np.exp(-0.3 * grid[:, 0]) * (grid[:, 1] + 1.0) * np.cos(grid[:, 2])).reshape(16, 16, 16)
+    assert res.ranks == (1, 1, 1, 1)
+    assert np.abs(res.tensor.full() - ref).max() < 1e-13 * np.abs(ref).max()
+
+
+def test_amen_vs_golden(P, golden):
+    g = golden("tensor_train.npz")
+    A = P.tt.TtMatrix([g[f"amen_A{k}"] for k in range(3)])
+    f = P.tt.TtTensor([g[f"amen_f{k}"] for k in range(3)])
+    res = P.tt.amen_solve(A, f, 1e-10)
+    assert res.converged
+    # 8^3 Laplacian, cond ~ 40: solution within 1e-9 of the reference's
+    assert rel(res.solution.full(), g["amen_u_full"]) <= 1e-9
+    res2 = P.tt.amen_solve(A, f, 1e-10, P.tt.AmenOptions(direct_solve_max=16))
+    assert res2.converged
+    assert rel(res2.solution.full(), g["amen_cg_u_full"]) <= 1e-8
+
+
+# ---------------------------------------------------------------- assembly / solve
+
+@pytest.mark.parametrize("name,deg", [("ring", 2), ("lshape", 1), ("hyperboloid", 2), ("quarter_torus", 2)])
+def test_assembly_vs_golden(P, golden, name, deg):
+    g = golden("assembly.npz")
+    patch = P.geo.make_geometry(name)
+    bases = tuple(P.drv.solution_basis(patch.bases[d], deg, 4) for d in range(3))
+    disc = P.asm.build_quadrature(bases)
+    rng = np.random.default_rng(400)
+    K, _ = P.asm.assemble_stiffness(patch, disc, 1e-11, rng=rng)
+    f, _ = P.asm.assemble_load(patch, disc, "sin_pi_xyz", 1e-11, rng=rng)
+    assert all(abs(a - b) <= 2 for a, b in zip(K.ranks, g[f"{name}_Kranks"]))
+    assert rel(K.full(), g[f"{name}_K"]) <= 1e-9
+    assert rel(f.full(), g[f"{name}_f"]) <= 1e-9
+
+
+SOLVES = {
+    "cube_p2_e8": dict(geometry="unit_cube", degree=2, elements=8, source="manufactured_sines", analytic="cube_sines"),
+    "lshape_p1_e8": dict(geometry="lshape", degree=1, elements=8, source="sin_pi_xy", analytic="lshape_exact"),
+    "torus_p2_e4": dict(geometry="quarter_torus", degree=2, elements=4, source="sin_pi_xyz"),
+    "ohemi_p2_e4": dict(geometry="opened_hemisphere", degree=2, elements=4, source="one"),
+}
+
+
+@pytest.mark.parametrize("tag", list(SOLVES))
+def test_solve_vs_golden(P, golden, tag):
+    g = golden("solves.npz")
+    rep = P.drv.solve_poisson(P.drv.SolveConfig(seed=0, **SOLVES[tag]))
+    assert rep.solver_converged
+    assert all(abs(a - b) <= 2 for a, b in zip(rep.ranks_u, g[f"{tag}_ranks_u"]))
+    # both solutions meet eps_solve = 1e-8 on operators with cond <= ~1e3
+    assert rel(rep.u.full(), g[f"{tag}_u"]) <= 1e-6
+    if not np.isnan(g[f"{tag}_l2"]):
+        assert abs(rep.l2_error - float(g[f"{tag}_l2"])) <= 0.01 * float(g[f"{tag}_l2"])
+
+
+def test_ring_solve_vs_golden(P, golden):
+    g = golden("solves.npz")
+    bc = P.asm.BoundarySpec({(1, 0): P.asm.FaceCondition("dirichlet", 1.0),
+                             (1, 1): P.asm.FaceCondition("dirichlet", 2.0)})
+    rep = P.drv.solve_poisson(P.drv.SolveConfig(geometry="ring", degree=2, elements=8, source="zero",
+                                                analytic="ring_radial", bc=bc, seed=0))
+    assert rel(rep.u.full(), g["ring_p2_e8_u"]) <= 1e-6
+    assert abs(rep.l2_error - float(g["ring_p2_e8_l2"])) <= 0.01 * float(g["ring_p2_e8_l2"])

@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark: TT matvec+round GFLOP/s (FP64) on the configs[4] kernel microbenchmark,
+plus the TT-IGA Poisson solve time of configs[1] (quarter cylinder, n=128, p=3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one pass of the hot path over one synthetic batch: Y = round(A x, 1e-8)
+for a 3-core TT-matrix (1024 x 1024 modes, operator ranks 16) and a TT-vector
+(ranks 64), cores i.i.d. N(0,1)/sqrt(rank) from a seed. Inputs (2.4 GB) are larger
+than L2, so no flush is needed between steps. Multi-GPU: replicas only (the solve
+path does not shard; each rank runs its own seeded instance, no collective on the
+data path); value = total flops of all ranks / max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TT matvec+round GFLOP/s (FP64)"
+WORKLOAD = ("configs[4] kernel microbenchmark: 3-core TT-matrix, 1024x1024 modes, operator ranks 16, "
+            "cores N(0,1)/sqrt(rank) (seed 0+rank), applied to a TT-vector with ranks 64, rounded to 1e-8")
+N_MODE, R_OP, R_VEC, EPS = 1024, 16, 64, 1e-8
+CPU_SAMPLE_N = 128  # bounded CPU sample: same ranks, mode size 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--skip-solve", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--n", type=int, default=N_MODE)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 7:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample_run(n=CPU_SAMPLE_N, seed=0):
+    """Oracle (numpy, all host threads) matvec+round on the bounded sample; returns (seconds, flops)."""
+    from oracle import tt as OT
+    from paper_2509_13224_b200.workloads import matvec_round_flops, matvec_round_instance_np
+    A, X = matvec_round_instance_np(n, R_OP, R_VEC, 3, seed)
+    At, Xt = OT.TTOp(A), OT.TT(X)
+    t0 = time.perf_counter()
+    Y = OT.round_tt(OT.matvec(At, Xt), EPS)
+    dt = time.perf_counter() - t0
+    Rs = [1, R_OP, R_OP, 1]
+    rs = [1, R_VEC, R_VEC, 1]
+    fl = matvec_round_flops([n] * 3, [n] * 3, Rs, rs, list(Y.ranks))
+    return dt, fl, Y.ranks
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    ncores = os.cpu_count()
+    for _ in range(args.warmup):
+        cpu_sample_run()
+    times, fl = [], None
+    for _ in range(args.steps):
+        dt, fl, ranks = cpu_sample_run()
+        times.append(dt)
+    v = fl / (sum(times) / len(times)) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": "replicas", "l2": "inputs > L2"},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": ncores, "kind": "port",
+                         "sample": f"oracle (numpy/LAPACK restatement of the reference tt_matvec + tt_round) on the "
+                                   f"same workload at mode size {CPU_SAMPLE_N} (ranks 16/64 kept), one matvec+round "
+                                   f"per step"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2509_13224_b200 import _lib
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import tt_matvec, tt_round
+    from paper_2509_13224_b200.workloads import matvec_round_flops, matvec_round_instance, matvec_round_shapes
+
+    lib = _lib.lib()
+    n = args.n
+    A, X = matvec_round_instance(n, R_OP, R_VEC, 3, seed=rank)
+    Rs, rs = matvec_round_shapes(n, R_OP, R_VEC, 3)
+
+    def step():
+        return tt_round(tt_matvec(A, X), EPS)
+
+    Y = None
+    for _ in range(max(args.warmup, 1)):
+        Y = step()
+    torch.cuda.synchronize()
+    out_ranks = list(Y.ranks)
+    flops = matvec_round_flops([n] * 3, [n] * 3, Rs, rs, out_ranks)
+    del Y
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- device-resident timed region
+    lib.ttb_launch_count(1)
+    L.gemm_profile(True)
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0.record(st)
+        for _ in range(args.steps):
+            Y = step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    barrier()
+    launches = int(lib.ttb_launch_count(1))
+    prof = L.gemm_profile(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_all = ms
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_all = float(t.item())
+    value = flops * world / (ms_all / 1e3) / 1e9
+
+    # roofline of the dominant kernel (DMMA GEMM): algorithmic flops / event-timed duration, summed
+    g_ms = sum(a.elapsed_time(b) for a, b, _ in prof)
+    g_fl = sum(f for _, _, f in prof)
+    big = sorted(prof, key=lambda r: -r[2])[: args.steps]
+    big_ms = sum(a.elapsed_time(b) for a, b, _ in big)
+    big_fl = sum(f for _, _, f in big)
+
+    # measured FP64 peak on this box: cuBLAS DGEMM 8192^3 (best of 5) -- the roofline denominator
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    best = 1e9
+    for _ in range(5):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        a @ b
+        s1.record()
+        torch.cuda.synchronize()
+        best = min(best, s0.elapsed_time(s1))
+    fp64_peak = 2 * 8192 ** 3 / (best / 1e3) / 1e12
+    del a, b
+
+    # ---------------- end-to-end: pinned host cores -> device -> matvec+round -> host cores
+    hA = [G.cpu().pin_memory() for G in A.cores]
+    hX = [G.cpu().pin_memory() for G in X.cores]
+    h2d = sum(t.numel() * 8 for t in hA + hX)
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor
+    e2e_steps = max(1, min(args.steps, 3))
+    d2h = 0
+    barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    for _ in range(e2e_steps):
+        dA = TtMatrix([t.to("cuda", non_blocking=True) for t in hA])
+        dX = TtTensor([t.to("cuda", non_blocking=True) for t in hX])
+        Yd = tt_round(tt_matvec(dA, dX), EPS)
+        outs = [G.to("cpu", non_blocking=True) for G in Yd.cores]
+        d2h = sum(G.numel() * 8 for G in Yd.cores)
+    t1.record(st)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = t0.elapsed_time(t1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = flops * world / (e2e_ms / 1e3) / 1e9
+    del hA, hX, outs, Yd, dA, dX
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_all, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1)/sqrt(rank) TT cores)",
+            "config": {"workload": WORKLOAD, "mode_size": n, "op_ranks": R_OP, "vec_ranks": R_VEC,
+                       "round_eps": EPS, "output_ranks": out_ranks, "algorithmic_gflop_per_step": flops / 1e9,
+                       "parallelism": f"replicas x{world}", "l2": "inputs 2.4 GB > 126 MB L2, no flush needed"},
+            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
+                    int(d2h), "ms_per_step": e2e_ms},
+            "roofline": {"bound": "fp64", "kernel": "dgemm_kernel (DMMA m8n8k4 f64)",
+                         "achieved": big_fl / (big_ms / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": (big_fl / (big_ms / 1e3) / 1e12) / fp64_peak, "traffic": None,
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
+                         "all_gemms": {"tflops": g_fl / (g_ms / 1e3) / 1e12, "share_of_step": g_ms / args.steps / ms_all,
+                                       "launches": len(prof)}},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+    if world > 1:
+        dist.barrier()
+
+    # ---------------- TT-IGA Poisson solve, configs[1] (device time per phase), N=1 only
+    if rank == 0 and not args.skip_solve:
+        from paper_2509_13224_b200 import driver as D
+        from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+        D.solve_poisson(D.SolveConfig(seed=0, **SOLVE_CONFIGS[1]), want_error=False)  # warm-up
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        rep = D.solve_poisson(D.SolveConfig(seed=0, **SOLVE_CONFIGS[1]), want_error=True)
+        torch.cuda.synchronize()
+        tm = rep.timings
+        solve_s = sum(v for k, v in tm.items() if k != "t_error_s")
+        line["solve_configs1"] = {"time_s": solve_s, "timings": tm, "dofs": rep.dofs, "ranks_K": list(rep.ranks_K),
+                                  "ranks_u": list(rep.ranks_u), "residual": rep.residual,
+                                  "l2_error": rep.l2_error, "sweeps": rep.sweeps}
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        dt, fl, _ = cpu_sample_run()
+        line["cpu_baseline"] = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"oracle numpy restatement of tt_matvec + tt_round, mode size "
+                                          f"{CPU_SAMPLE_N} (ranks 16/64 kept), one step"}
+        if not args.skip_solve:
+            from oracle import iga as OI
+            from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+            t = time.perf_counter()
+            r = OI.solve(OI.Config(seed=0, **SOLVE_CONFIGS[1]), want_error=False)
+            line["cpu_baseline"]["solve_configs1_s"] = sum(v for k, v in r["timings"].items() if k != "t_error_s")
+            line["cpu_baseline"]["solve_configs1_ranks_u"] = list(r["ranks_u"])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -22,6 +22,9 @@ extern "C" {
 #define TTB_ENOTPD (-2)
 #define TTB_ESINGULAR (-3)
 
+/* Number of kernels this library launched since the last reset (host counter; bench.py evidence). */
+long long ttb_launch_count(int reset);
+
 /* ---- dense FP64 building blocks ------------------------------------------------------------ */
 
 /* C[b] = alpha * op(A[b]) op(B[b]) + beta * C[b], row-major, strided batch.

@@ -26,6 +26,7 @@ class NativeError(RuntimeError):
 vp, i32, i64, f64 = C.c_void_p, C.c_int, C.c_longlong, C.c_double
 
 SIGNATURES = {
+    "ttb_launch_count": (i64, [i32]),
     "ttb_dgemm": (i32, [vp, i32, i32, i32, i32, i32, f64, vp, i64, i64, vp, i64, i64, f64, vp, i64, i64, i32]),
     "ttb_permute": (i32, [vp, i32, vp, vp, vp, vp]),
     "ttb_dot": (i32, [vp, i64, vp, vp, vp, vp, i32]),

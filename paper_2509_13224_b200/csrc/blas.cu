@@ -6,6 +6,14 @@
 // cp.async (LDGSTS) in a two-stage pipeline.
 #include "common.cuh"
 
+long long g_ttb_launches = 0;
+
+TTB_API long long ttb_launch_count(int reset) {
+  long long v = __atomic_load_n(&g_ttb_launches, __ATOMIC_RELAXED);
+  if (reset) __atomic_store_n(&g_ttb_launches, 0LL, __ATOMIC_RELAXED);
+  return v;
+}
+
 namespace {
 
 constexpr int BK = 16;
@@ -163,7 +171,7 @@ int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
     configured = true;
   }
   dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), batch);
-  dgemm_kernel<BM, BN, WM, WN><<<grid, T, smem, st>>>(g);
+  dgemm_kernel<BM, BN, WM, WN><<<grid, T, smem, st>>>(g); ttb_count();
   return ttb_last_error();
 }
 
@@ -255,7 +263,7 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
   if (K == 0) {
     long long n = (long long)M * N;
     dim3 grid(ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), batch);
-    scale_kernel<<<grid, 256, 0, st>>>(n, beta, C, ldc, M, N, sC);
+    scale_kernel<<<grid, 256, 0, st>>>(n, beta, C, ldc, M, N, sC); ttb_count();
     return ttb_last_error();
   }
   GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};
@@ -280,7 +288,7 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
       long long tot = (long long)M * N;
       int blocks = ceil_div(tot, 256);
       if (blocks > 148 * 8) blocks = 148 * 8;
-      splitk_reduce<<<blocks, 256, 0, st>>>(M, N, (int)S, part, alpha, beta, C, ldc);
+      splitk_reduce<<<blocks, 256, 0, st>>>(M, N, (int)S, part, alpha, beta, C, ldc); ttb_count();
       return ttb_last_error();
     }
   }
@@ -305,7 +313,7 @@ TTB_API int ttb_permute(void* stream, int nd, const long long* in_dims, const in
   if (total == 0) return TTB_OK;
   int blocks = ceil_div(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  permute_kernel<<<blocks, 256, 0, as_stream(stream)>>>(a, total, src, dst);
+  permute_kernel<<<blocks, 256, 0, as_stream(stream)>>>(a, total, src, dst); ttb_count();
   return ttb_last_error();
 }
 
@@ -314,7 +322,7 @@ TTB_API int ttb_dot(void* stream, long long n, const double* x, const double* y,
                     int take_sqrt) {
   cudaStream_t st = as_stream(stream);
   int blocks = n <= 0 ? 1 : (ceil_div(n, RED_THREADS) < RED_BLOCKS ? ceil_div(n, RED_THREADS) : RED_BLOCKS);
-  dot_partial<<<blocks, RED_THREADS, 0, st>>>(n, x, y, part);
-  sum_final<<<1, 256, 0, st>>>(blocks, part, out, take_sqrt);
+  dot_partial<<<blocks, RED_THREADS, 0, st>>>(n, x, y, part); ttb_count();
+  sum_final<<<1, 256, 0, st>>>(blocks, part, out, take_sqrt); ttb_count();
   return ttb_last_error();
 }

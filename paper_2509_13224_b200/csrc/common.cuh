@@ -22,6 +22,10 @@ static inline int ttb_last_error() {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
+// host-side count of kernel launches issued by this library (bench.py's gpu_launches evidence)
+extern long long g_ttb_launches;
+static inline void ttb_count() { __atomic_add_fetch(&g_ttb_launches, 1LL, __ATOMIC_RELAXED); }
+
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 __device__ __forceinline__ double warp_sum(double v) {

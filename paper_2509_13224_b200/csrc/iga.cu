@@ -391,7 +391,7 @@ TTB_API int ttb_basis_eval(void* stream, int nq, const double* x, const double* 
                            const double* weights, int* first, double* V, double* D, int* bad) {
   if (p < 0 || p > PMAX || nk < 2 * p + 2) return TTB_EARG;
   if (nq == 0) return TTB_OK;
-  basis_kernel<<<ceil_div(nq, 128), 128, 0, as_stream(stream)>>>(nq, x, knots, nk, p, weights, first, V, D, bad);
+  basis_kernel<<<ceil_div(nq, 128), 128, 0, as_stream(stream)>>>(nq, x, knots, nk, p, weights, first, V, D, bad); ttb_count();
   return ttb_last_error();
 }
 
@@ -407,7 +407,7 @@ TTB_API int ttb_geo_eval(void* stream, long long N, const long long* idx, const 
   const double* D[3] = {D0, D1, D2};
   int p[3] = {p0, p1, p2}, n[3] = {n0, n1, n2};
   GeoArgs g = make_geo(f, V, D, p, n, cw, sing_tol);
-  geo_kernel<<<grid_for(N, 128), 128, 0, as_stream(stream)>>>(g, N, idx, mode, ri, rj, src, out, bad);
+  geo_kernel<<<grid_for(N, 128), 128, 0, as_stream(stream)>>>(g, N, idx, mode, ri, rj, src, out, bad); ttb_count();
   return ttb_last_error();
 }
 
@@ -415,7 +415,7 @@ TTB_API int ttb_op_core(void* stream, int r, int nq, int s, const double* G, con
                         const double* X, const double* Y, int p, int n, int h, double* out) {
   long long tot = (long long)r * n * (2 * h + 1) * s;
   if (tot == 0) return TTB_OK;
-  op_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, X, Y, p, n, h, out);
+  op_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, X, Y, p, n, h, out); ttb_count();
   return ttb_last_error();
 }
 
@@ -423,7 +423,7 @@ TTB_API int ttb_vec_core(void* stream, int r, int nq, int s, const double* G, co
                          const double* V, int p, int n, double* out) {
   long long tot = (long long)r * n * s;
   if (tot == 0) return TTB_OK;
-  vec_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, V, p, n, out);
+  vec_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, V, p, n, out); ttb_count();
   return ttb_last_error();
 }
 
@@ -431,7 +431,7 @@ TTB_API int ttb_field_table(void* stream, int r, int n, int s, const double* u, 
                             const double* V, int p, double* T) {
   long long tot = (long long)r * nq * s;
   if (tot == 0) return TTB_OK;
-  field_table_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, n, s, u, nq, first, V, p, T);
+  field_table_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, n, s, u, nq, first, V, p, T); ttb_count();
   return ttb_last_error();
 }
 
@@ -450,7 +450,7 @@ TTB_API int ttb_l1_error(void* stream, const int* f0, const int* f1, const int* 
   long long blocks = (long long)nq0 * nq1;
   cudaStream_t st = as_stream(stream);
   l1err_kernel<<<(unsigned)blocks, 128, r2 * sizeof(double), st>>>(g, nq0, nq1, nq2, U0, r1, U1, r2, U2, w0, w1, w2,
-                                                                     exact_id, prm, part);
-  pair_sum_kernel<<<1, 1024, 0, st>>>(blocks, part, out);
+                                                                     exact_id, prm, part); ttb_count();
+  pair_sum_kernel<<<1, 1024, 0, st>>>(blocks, part, out); ttb_count();
   return ttb_last_error();
 }

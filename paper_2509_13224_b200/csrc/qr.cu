@@ -182,52 +182,119 @@ int panel_grid(int m) {
 int launch_panel(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, double* part, cudaStream_t st) {
   int nblk = panel_grid(m);
   void* args[] = {&m, &jb, &P, &ld, &tau, &V, &T, &part};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(nblk), dim3(PT), args, 0, st);
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(nblk), dim3(PT), args, 0, st); ttb_count();
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+}  // namespace
+
+namespace {
+
+constexpr int NB2 = 128;  // outer WY block (trailing-update GEMMs have K = 128)
+
+// T (nb x nb row-major, upper) from the Gram G = V^T V (row-major ld ldg) and tau (dlarft, forward, columnwise)
+__global__ void larft_kernel(int nb, const double* G, int ldg, const double* tau, double* T) {
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < nb; ++i) {
+    const double ti = tau[i];
+    if (threadIdx.x == 0) T[i * nb + i] = ti;
+    for (int r = threadIdx.x; r < i; r += blockDim.x) {
+      double v = 0.0;
+      for (int c = r; c < i; ++c) v += T[r * nb + c] * G[(long long)c * ldg + i];
+      T[r * nb + i] = -ti * v;
+    }
+    __syncthreads();
+  }
+}
+
+struct QrWs {
+  double *part, *Vp, *Vb, *W, *W2, *G, *Tin, *Tout;
+};
+
+QrWs carve(double* ws, int m, int n) {
+  const int k = m < n ? m : n;
+  const long long wn = (long long)(n > k ? n : k);
+  QrWs w;
+  w.part = ws;
+  w.Vp = w.part + (long long)296 * (NB * NB + NB) + 296;
+  w.Vb = w.Vp + (long long)m * NB;
+  w.W = w.Vb + (long long)m * NB2;
+  w.W2 = w.W + wn * NB2;
+  w.G = w.W2 + wn * NB2;
+  w.Tin = w.G + (long long)NB2 * NB2;
+  w.Tout = w.Tin + (long long)((k + NB - 1) / NB) * NB * NB;
+  return w;
+}
+
+int grid_v(long long tot) {
+  int b = ceil_div(tot, 256);
+  if (b > 148 * 8) b = 148 * 8;
+  return b < 1 ? 1 : b;
+}
+
+// C (rows mp, cols nq, col-major ld) := (I - V T V^T)^{op} C, V col-major (mp x jb, ld mp), T row-major jb x jb.
+// transT = 1 applies Q^T (geqrf trailing update), 0 applies Q (orgqr).
+int apply_wy(void* stream, int mp, int nq, int jb, const double* V, const double* T, int transT, double* C,
+             long long ldc, double* W, double* W2) {
+  int rc = ttb_dgemm(stream, 0, 1, nq, jb, mp, 1.0, C, ldc, 0, V, mp, 0, 0.0, W, jb, 0, 1);
+  if (rc) return rc;
+  rc = ttb_dgemm(stream, 0, transT ? 0 : 1, nq, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
+  if (rc) return rc;
+  return ttb_dgemm(stream, 0, 0, nq, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, C, ldc, 0, 1);
 }
 
 }  // namespace
 
 // Workspace sizes (in doubles) for ttb_geqrf / ttb_orgqr.
 TTB_API long long ttb_qr_workspace(int m, int n) {
-  int k = m < n ? m : n;
-  long long part = (long long)296 * (NB * NB + NB) + 296;
-  long long v = (long long)m * NB;
-  long long w = (long long)(n > k ? n : k) * NB * 2;
-  long long t = (long long)((k + NB - 1) / NB) * NB * NB;
-  return part + v + w + t + 64;
+  const int k = m < n ? m : n;
+  const long long wn = (long long)(n > k ? n : k);
+  long long s = (long long)296 * (NB * NB + NB) + 296;
+  s += (long long)m * NB + (long long)m * NB2 + 2 * wn * NB2 + (long long)NB2 * NB2;
+  s += (long long)((k + NB - 1) / NB) * NB * NB + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
+  return s + 64;
 }
 
-// In-place QR of col-major A (m x n, lda). tau: min(m,n). ws: ttb_qr_workspace doubles;
-// the WY factors T of every panel are kept in ws for a following ttb_orgqr.
+// In-place QR of col-major A (m x n, lda). tau: min(m,n). ws: ttb_qr_workspace doubles; the outer
+// WY factors stay in ws for a following ttb_orgqr. Two-level blocking: 32-column panels (cooperative
+// kernel) inside 128-column blocks whose trailing update is three GEMMs with K = 128.
 TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, double* tau, double* ws) {
   if (m < 0 || n < 0 || lda < (m > 1 ? m : 1)) return TTB_EARG;
   const int k = m < n ? m : n;
   if (k == 0) return TTB_OK;
   cudaStream_t st = as_stream(stream);
-  double* part = ws;
-  double* V = part + (long long)296 * (NB * NB + NB) + 296;
-  double* W = V + (long long)m * NB;
-  double* W2 = W + (long long)(n > k ? n : k) * NB;
-  double* Tall = W + (long long)(n > k ? n : k) * NB * 2;
-  for (int j0 = 0; j0 < k; j0 += NB) {
-    const int jb = (k - j0) < NB ? (k - j0) : NB;
-    const int mp = m - j0;
-    double* P = A + (long long)j0 * lda + j0;
-    double* T = Tall + (long long)(j0 / NB) * NB * NB;
-    int rc = launch_panel(mp, jb, P, lda, tau + j0, V, T, part, st);
+  QrWs w = carve(ws, m, n);
+  for (int J0 = 0; J0 < k; J0 += NB2) {
+    const int JB = (k - J0) < NB2 ? (k - J0) : NB2;
+    const int MP = m - J0;
+    for (int j0 = J0; j0 < J0 + JB; j0 += NB) {
+      const int jb = (J0 + JB - j0) < NB ? (J0 + JB - j0) : NB;
+      const int mp = m - j0;
+      double* P = A + (long long)j0 * lda + j0;
+      double* T = w.Tin + (long long)(j0 / NB) * NB * NB;
+      int rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, st);
+      if (rc) return rc;
+      // inside the outer block, or -- when the block is a single panel -- the whole trailing matrix
+      const int n2 = (JB <= NB) ? (n - j0 - jb) : (J0 + JB - j0 - jb);
+      if (n2 > 0) {
+        rc = apply_wy(stream, mp, n2, jb, w.Vp, T, 1, A + (long long)(j0 + jb) * lda + j0, lda, w.W, w.W2);
+        if (rc) return rc;
+      }
+    }
+    double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
+    if (JB <= NB) {
+      cudaMemcpyAsync(Tb, w.Tin + (long long)(J0 / NB) * NB * NB, sizeof(double) * JB * JB,
+                      cudaMemcpyDeviceToDevice, st);
+      continue;
+    }
+    extract_v_kernel<<<grid_v((long long)MP * JB), 256, 0, st>>>(MP, JB, A + (long long)J0 * lda + J0, lda, w.Vb); ttb_count();
+    int rc = ttb_dgemm(stream, 0, 1, JB, JB, MP, 1.0, w.Vb, MP, 0, w.Vb, MP, 0, 0.0, w.G, JB, 0, 1);
     if (rc) return rc;
-    const int n2 = n - j0 - jb;
+    larft_kernel<<<1, 128, 0, st>>>(JB, w.G, JB, tau + J0, Tb); ttb_count();
+    const int n2 = n - J0 - JB;
     if (n2 > 0) {
-      double* A2 = A + (long long)(j0 + jb) * lda + j0;
-      // Wt (n2 x jb) = A2^T V   [row-major view: A2rm (n2 x mp, ld lda) * Vrm^T (mp x jb)]
-      rc = ttb_dgemm(stream, 0, 1, n2, jb, mp, 1.0, A2, lda, 0, V, mp, 0, 0.0, W, jb, 0, 1);
-      if (rc) return rc;
-      // W2t = Wt * T
-      rc = ttb_dgemm(stream, 0, 0, n2, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
-      if (rc) return rc;
-      // A2rm -= W2t * Vrm
-      rc = ttb_dgemm(stream, 0, 0, n2, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, A2, lda, 0, 1);
+      rc = apply_wy(stream, MP, n2, JB, w.Vb, Tb, 1, A + (long long)(J0 + JB) * lda + J0, lda, w.W, w.W2);
       if (rc) return rc;
     }
   }
@@ -239,38 +306,18 @@ TTB_API int ttb_orgqr(void* stream, int m, int kq, int kf, const double* A, long
                       double* ws, int n_factored) {
   if (m < 0 || kq < 0 || kq > m) return TTB_EARG;
   cudaStream_t st = as_stream(stream);
-  const int k = kf;  // number of reflectors
-  double* V = ws + (long long)296 * (NB * NB + NB) + 296;
-  const int nw = n_factored;
-  double* W = V + (long long)m * NB;
-  double* W2 = W + (long long)nw * NB;
-  double* Tall = W + (long long)nw * NB * 2;
-  {
-    long long tot = (long long)m * kq;
-    int blocks = ceil_div(tot, 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    eye_kernel<<<blocks, 256, 0, st>>>(m, kq, Q, ldq);
-  }
-  const int last = ((k - 1) / NB) * NB;
-  for (int j0 = last; j0 >= 0; j0 -= NB) {
-    const int jb = (k - j0) < NB ? (k - j0) : NB;
-    const int mp = m - j0;
-    const int nq = kq - j0;
+  const int k = kf;
+  QrWs w = carve(ws, m, n_factored);
+  eye_kernel<<<grid_v((long long)m * kq), 256, 0, st>>>(m, kq, Q, ldq); ttb_count();
+  const int last = ((k - 1) / NB2) * NB2;
+  for (int J0 = last; J0 >= 0; J0 -= NB2) {
+    const int JB = (k - J0) < NB2 ? (k - J0) : NB2;
+    const int MP = m - J0;
+    const int nq = kq - J0;
     if (nq <= 0) continue;
-    const double* P = A + (long long)j0 * lda + j0;
-    double* T = Tall + (long long)(j0 / NB) * NB * NB;
-    long long tot = (long long)mp * jb;
-    int blocks = ceil_div(tot, 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    extract_v_kernel<<<blocks, 256, 0, st>>>(mp, jb, P, lda, V);
-    double* Q2 = Q + (long long)j0 * ldq + j0;
-    // Q2 = (I - V T V^T) Q2 :  Wt = Q2^T V ; W2t = Wt T^T ; Q2rm -= W2t Vrm
-    int rc = ttb_dgemm(stream, 0, 1, nq, jb, mp, 1.0, Q2, ldq, 0, V, mp, 0, 0.0, W, jb, 0, 1);
-    if (rc) return rc;
-    rc = ttb_dgemm(stream, 0, 1, nq, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
-    if (rc) return rc;
-    rc = ttb_dgemm(stream, 0, 0, nq, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, Q2, ldq, 0, 1);
+    double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
+    extract_v_kernel<<<grid_v((long long)MP * JB), 256, 0, st>>>(MP, JB, A + (long long)J0 * lda + J0, lda, w.Vb); ttb_count();
+    int rc = apply_wy(stream, MP, nq, JB, w.Vb, Tb, 0, Q + (long long)J0 * ldq + J0, ldq, w.W, w.W2);
     if (rc) return rc;
   }
   return ttb_last_error();
@@ -281,6 +328,6 @@ TTB_API int ttb_extract_r(void* stream, int k, int n, const double* A, long long
   if (tot == 0) return TTB_OK;
   int blocks = ceil_div(tot, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  extract_r_kernel<<<blocks, 256, 0, as_stream(stream)>>>(k, n, A, lda, R);
+  extract_r_kernel<<<blocks, 256, 0, as_stream(stream)>>>(k, n, A, lda, R); ttb_count();
   return ttb_last_error();
 }

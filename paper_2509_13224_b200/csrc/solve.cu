@@ -378,8 +378,8 @@ TTB_API int ttb_lu_solve(void* stream, int n, double* A, long long lda, int* piv
                          int trans, int* info) {
   if (n < 1 || nrhs < 0) return TTB_EARG;
   cudaStream_t st = as_stream(stream);
-  lu_kernel<<<1, ST, 0, st>>>(n, A, lda, piv, info);
-  if (nrhs > 0) lu_apply_kernel<<<ceil_div(nrhs, 128), 128, 0, st>>>(n, A, lda, piv, nrhs, B, ldb, trans);
+  lu_kernel<<<1, ST, 0, st>>>(n, A, lda, piv, info); ttb_count();
+  if (nrhs > 0) lu_apply_kernel<<<ceil_div(nrhs, 128), 128, 0, st>>>(n, A, lda, piv, nrhs, B, ldb, trans); ttb_count();
   return ttb_last_error();
 }
 
@@ -390,7 +390,7 @@ TTB_API int ttb_potrf(void* stream, int n, double* A, long long lda, int* info) 
   cudaMemsetAsync(info, 0, sizeof(int), st);
   for (int j0 = 0; j0 < n; j0 += CNB) {
     const int nb = n - j0 < CNB ? n - j0 : CNB;
-    chol_panel_kernel<<<1, 256, 0, st>>>(n, j0, A, lda, info);
+    chol_panel_kernel<<<1, 256, 0, st>>>(n, j0, A, lda, info); ttb_count();
     const int m2 = n - j0 - nb;
     if (m2 > 0) {
       const double* Lp = A + (long long)j0 * lda + j0 + nb;  // col-major m2 x nb == row-major nb x m2 (ld lda)
@@ -411,7 +411,7 @@ TTB_API int ttb_potrs(void* stream, int n, const double* L, long long lda, doubl
     cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cfg = true;
   }
-  chol_solve_kernel<<<1, ST, smem, as_stream(stream)>>>(n, L, lda, b);
+  chol_solve_kernel<<<1, ST, smem, as_stream(stream)>>>(n, L, lda, b); ttb_count();
   return ttb_last_error();
 }
 
@@ -434,6 +434,6 @@ TTB_API int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, 
   int* status = iws + n;
   int nblk = maxvol_grid(n);
   void* args[] = {&n, &r, &Q, &W, &perm, &C, &Ainv, &pv, &pi, &tol, &max_iters, &rows_out, &status};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)maxvol_kernel, dim3(nblk), dim3(MT_), args, 0, as_stream(stream));
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)maxvol_kernel, dim3(nblk), dim3(MT_), args, 0, as_stream(stream)); ttb_count();
   return e == cudaSuccess ? 0 : (int)e;
 }

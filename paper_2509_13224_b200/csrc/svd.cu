@@ -119,6 +119,104 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(int n, double* Ag, long long
   if (threadIdx.x == 0 && info) info[b] = nsweep;
 }
 
+// Multi-CTA variant for one large matrix: every warp of the grid takes disjoint pairs of a
+// round, rounds separated by grid-wide barriers; a per-sweep rotation counter (double
+// buffered by sweep parity) gives a uniform convergence decision.
+constexpr int CT = 256;
+
+__global__ void __launch_bounds__(CT) jacobi_coop_kernel(int n, double* A, double* V, int* cnt, int max_sweeps,
+                                                          double tol, int* sweeps_out) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int N = (n + 1) & ~1;
+  int sweep = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { cnt[0] = 0; cnt[1] = 0; }
+  grid.sync();
+  for (; sweep < max_sweeps; ++sweep) {
+    int* c = cnt + (sweep & 1);
+    for (int r = 0; r < N - 1; ++r) {
+      for (int pr = gw; pr < N / 2; pr += nwarps) {
+        int p = rr_index(pr, r, N), q = rr_index(N - 1 - pr, r, N);
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q >= n) continue;
+        double* ap = A + (long long)p * n;
+        double* aq = A + (long long)q * n;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          double x = ap[i], y = aq[i];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+        if (lane == 0) atomicAdd(c, 1);
+        double zeta = (be - al) / (2.0 * ga);
+        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = lane; i < n; i += 32) {
+          double x = ap[i], y = aq[i];
+          ap[i] = cs * x - sn * y;
+          aq[i] = sn * x + cs * y;
+        }
+        double* vp = V + (long long)p * n;
+        double* vq = V + (long long)q * n;
+        for (int i = lane; i < n; i += 32) {
+          double x = vp[i], y = vq[i];
+          vp[i] = cs * x - sn * y;
+          vq[i] = sn * x + cs * y;
+        }
+      }
+      grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(sweep + 1) & 1] = 0;
+    const int done = (*(volatile int*)c) == 0;
+    grid.sync();
+    if (done) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+__global__ void init_av_kernel(int n, const double* Ain, double* A, double* V) {
+  const long long nn = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
+    A[e] = Ain[e];
+    V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
+  }
+}
+
+// column norms -> descending ranks -> U = A / sigma, V permuted (one warp per column)
+__global__ void jacobi_finish_kernel(int n, const double* A, const double* V, double* sig, double* S, double* U,
+                                     double* Vout) {
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += A[(long long)j * n + i] * A[(long long)j * n + i];
+  s = warp_sum(s);
+  if (lane == 0) sig[j] = sqrt(s);
+}
+
+__global__ void jacobi_scatter_kernel(int n, const double* A, const double* V, const double* sig, double* S, double* U,
+                                      double* Vout) {
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n) return;
+  const double sj = sig[j];
+  int rank = 0;
+  for (int k = lane; k < n; k += 32) {
+    const double sk = sig[k];
+    rank += (sk > sj) || (sk == sj && k < j);
+  }
+  for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  if (lane == 0) S[rank] = sj;
+  const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+  for (int i = lane; i < n; i += 32) {
+    U[(long long)rank * n + i] = A[(long long)j * n + i] * inv;
+    Vout[(long long)rank * n + i] = V[(long long)j * n + i];
+  }
+}
+
 }  // namespace
 
 // SVD of `batch` square n x n col-major matrices A (= U diag(S) V^T).
@@ -139,10 +237,40 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
       cfg = true;
     }
     jacobi_kernel<true><<<batch, threads, smem, st>>>(n, A, strideA, S, strideS, U, V, strideUV, nullptr, max_sweeps,
-                                                      tol, info);
+                                                      tol, info); ttb_count();
+  } else if (batch > 1 || n <= 128) {
+    if (!work) return TTB_EARG;
+    jacobi_kernel<false><<<batch, JT, 0, st>>>(n, A, strideA, S, strideS, U, V, strideUV, work, max_sweeps, tol, info); ttb_count();
   } else {
     if (!work) return TTB_EARG;
-    jacobi_kernel<false><<<batch, JT, 0, st>>>(n, A, strideA, S, strideS, U, V, strideUV, work, max_sweeps, tol, info);
+    const long long nn = (long long)n * n;
+    double* Aw = work;
+    double* Vw = work + nn;
+    double* sig = work + 2 * nn;
+    static int* cnt = nullptr;
+    static int* sw = nullptr;
+    static int max_blocks = 0;
+    if (!cnt) {
+      cudaMalloc(&cnt, 4 * sizeof(int));
+      sw = cnt + 2;
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_coop_kernel, CT, 0);
+      max_blocks = sms * (per > 0 ? (per > 2 ? 2 : per) : 1);
+    }
+    int want = ceil_div((n + 1) / 2, CT / 32);  // one warp per pair
+    int nblk = want < max_blocks ? want : max_blocks;
+    if (nblk < 1) nblk = 1;
+    init_av_kernel<<<ceil_div(nn, 256) < 2048 ? ceil_div(nn, 256) : 2048, 256, 0, st>>>(n, A, Aw, Vw); ttb_count();
+    int ms = max_sweeps;
+    double tl = tol;
+    void* args[] = {&n, &Aw, &Vw, &cnt, &ms, &tl, &sw};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(nblk), dim3(CT), args, 0, st); ttb_count();
+    if (e != cudaSuccess) return (int)e;
+    jacobi_finish_kernel<<<ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, Aw, Vw, sig, S, U, V); ttb_count();
+    jacobi_scatter_kernel<<<ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, Aw, Vw, sig, S, U, V); ttb_count();
+    if (info) cudaMemcpyAsync(info, sw, sizeof(int), cudaMemcpyDeviceToDevice, st);
   }
   return ttb_last_error();
 }

@@ -286,7 +286,7 @@ TTB_API int ttb_band_matvec(void* stream, int Ra, int Rb, int n, int h, int rc, 
                             const double* X, double* Y) {
   long long tot = (long long)Ra * rc * n * Rb * rd;
   if (tot == 0) return TTB_OK;
-  band_matvec_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(Ra, Rb, n, h, rc, rd, M, X, Y);
+  band_matvec_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(Ra, Rb, n, h, rc, rd, M, X, Y); ttb_count();
   return ttb_last_error();
 }
 
@@ -294,7 +294,7 @@ TTB_API int ttb_band_apply(void* stream, int X, int Ra, int Rb, int n, int h, in
                            double* out, int rev) {
   long long tot = (long long)X * n * (rev ? Ra : Rb) * W;
   if (tot == 0) return TTB_OK;
-  band_apply_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(X, Ra, Rb, n, h, W, M, T, out, rev);
+  band_apply_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(X, Ra, Rb, n, h, W, M, T, out, rev); ttb_count();
   return ttb_last_error();
 }
 
@@ -303,7 +303,7 @@ TTB_API int ttb_local_dense(void* stream, int r0, int n, int r1, int h, int Rb, 
                             double* Bm) {
   long long tot = (long long)r0 * n * r1 * r0 * (2 * h + 1) * r1;
   if (tot == 0) return TTB_OK;
-  local_dense_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r0, n, r1, h, Rb, T1, phiR, Bm);
+  local_dense_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r0, n, r1, h, Rb, T1, phiR, Bm); ttb_count();
   return ttb_last_error();
 }
 
@@ -311,18 +311,18 @@ TTB_API int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb,
                             const double* M, const double* phiR, double* d, double* part) {
   long long tot = (long long)r0 * n * r1;
   cudaStream_t st = as_stream(stream);
-  jacobi_diag_kernel<<<grid_for(tot), 256, 0, st>>>(r0, n, r1, Ra, Rb, h, phiL, M, phiR, d);
+  jacobi_diag_kernel<<<grid_for(tot), 256, 0, st>>>(r0, n, r1, Ra, Rb, h, phiL, M, phiR, d); ttb_count();
   int nb = grid_for(tot) < PB ? grid_for(tot) : PB;
-  absmax_partial<<<nb, 256, 0, st>>>(tot, d, part);
-  max_final<<<1, 32, 0, st>>>(nb, part, part + PB);
-  abs_floor_kernel<<<grid_for(tot), 256, 0, st>>>(tot, d, part + PB);
+  absmax_partial<<<nb, 256, 0, st>>>(tot, d, part); ttb_count();
+  max_final<<<1, 32, 0, st>>>(nb, part, part + PB); ttb_count();
+  abs_floor_kernel<<<grid_for(tot), 256, 0, st>>>(tot, d, part + PB); ttb_count();
   return ttb_last_error();
 }
 
 TTB_API int ttb_tt_gather3(void* stream, int N, const long long* idx, const double* G0, int n0, int r1,
                            const double* G1, int n1, int r2, const double* G2, int n2, double* out) {
   if (N == 0) return TTB_OK;
-  gather_kernel<<<ceil_div(N, 8), 256, 0, as_stream(stream)>>>(N, r1, r2, idx, G0, n0, G1, n1, G2, n2, out);
+  gather_kernel<<<ceil_div(N, 8), 256, 0, as_stream(stream)>>>(N, r1, r2, idx, G0, n0, G1, n1, G2, n2, out); ttb_count();
   return ttb_last_error();
 }
 
@@ -361,33 +361,33 @@ TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, i
   double* mvws = q + N;
   double* part = mvws + (long long)r0 * Ra * n * r1 + (long long)r0 * n * Rb * r1;
   const int nb = grid_for(N) < PB ? grid_for(N) : PB;
-  set_scalars<<<1, 1, 0, st>>>(S, atol * atol);
+  set_scalars<<<1, 1, 0, st>>>(S, atol * atol); ttb_count();
   int rc;
   if (x0_nonzero) {
     rc = ttb_local_matvec(stream, r0, n, r1, Ra, Rb, h, phiL, M, phiR, x, r, mvws);
     if (rc) return rc;
-    sub_from_kernel<<<nb, 256, 0, st>>>(N, b, r, part);
+    sub_from_kernel<<<nb, 256, 0, st>>>(N, b, r, part); ttb_count();
   } else {
     cudaMemsetAsync(x, 0, N * sizeof(double), st);
     cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st);
-    pcg_dot_partial<<<nb, 256, 0, st>>>(N, r, r, S, part);
+    pcg_dot_partial<<<nb, 256, 0, st>>>(N, r, r, S, part); ttb_count();
   }
-  pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 3);
+  pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 3); ttb_count();
   const int chunk = 8;
   double host[8];
   for (int it0 = 0; it0 <= maxiter; it0 += chunk) {
     for (int k = 0; k < chunk; ++k) {
-      pcg_check_z<<<nb, 256, 0, st>>>(N, r, d, z, S, part, maxiter);
-      pcg_commit<<<1, 1, 0, st>>>(S);
-      pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 0);
-      pcg_update_p<<<grid_for(N), 256, 0, st>>>(N, z, p, S);
+      pcg_check_z<<<nb, 256, 0, st>>>(N, r, d, z, S, part, maxiter); ttb_count();
+      pcg_commit<<<1, 1, 0, st>>>(S); ttb_count();
+      pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 0); ttb_count();
+      pcg_update_p<<<grid_for(N), 256, 0, st>>>(N, z, p, S); ttb_count();
       // q = A p   (skipped work when done: kernels still run but results unused)
       rc = ttb_local_matvec(stream, r0, n, r1, Ra, Rb, h, phiL, M, phiR, p, q, mvws);
       if (rc) return rc;
-      pcg_dot_partial<<<nb, 256, 0, st>>>(N, p, q, S, part);
-      pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 2);
-      pcg_update_xr<<<nb, 256, 0, st>>>(N, x, r, p, q, S, part);
-      pcg_finish_iter<<<1, 256, 0, st>>>(nb, part, S);
+      pcg_dot_partial<<<nb, 256, 0, st>>>(N, p, q, S, part); ttb_count();
+      pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 2); ttb_count();
+      pcg_update_xr<<<nb, 256, 0, st>>>(N, x, r, p, q, S, part); ttb_count();
+      pcg_finish_iter<<<1, 256, 0, st>>>(nb, part, S); ttb_count();
     }
     cudaMemcpyAsync(host, S, 8 * sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);

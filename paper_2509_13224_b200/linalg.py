@@ -40,6 +40,17 @@ def _rows(A):
     return A
 
 
+_GEMM_PROFILE = None  # when a list: (start_event, end_event, flops) per GEMM launch
+
+
+def gemm_profile(enable: bool):
+    """Start/stop recording CUDA events around every GEMM (bench.py roofline); returns the records."""
+    global _GEMM_PROFILE
+    rec = _GEMM_PROFILE
+    _GEMM_PROFILE = [] if enable else None
+    return rec
+
+
 def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
     """out = alpha op(A) op(B) + beta out (row-major, FP64 DMMA kernel)."""
     A = _rows(A)
@@ -54,8 +65,16 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
     elif out.shape != (M, N) or out.stride(1) != 1:
         raise ValueError("bad gemm output")
     if M and N:
+        prof = _GEMM_PROFILE
+        if prof is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         call("ttb_dgemm", int(tA), int(tB), M, N, K, float(alpha), ptr(A), max(A.stride(0), 1), 0, ptr(B),
              max(B.stride(0), 1), 0, float(beta), ptr(out), max(out.stride(0), 1), 0, 1)
+        if prof is not None:
+            e1.record()
+            prof.append((e0, e1, 2.0 * M * N * K))
     return out
 
 

@@ -48,14 +48,25 @@ struct GemmArgs {
   int Kc;
 };
 
-template <int BM, int BN, int WM, int WN>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+// Shared-memory tile layouts follow the global contiguity of each operand, so every
+// global->shared copy is a contiguous (8 or 16 byte) cp.async and fragment reads are
+// conflict-free (pitches chosen so a warp's 32 x 8 B fragment read is exactly two wavefronts):
+//   A !tA : As[m][k] pitch BK+4     A tA : As[k][m] pitch BM+8
+//   B !tB : Bs[k][n] pitch BN+8     B tB : Bs[n][k] pitch BK+4
+template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC, int STAGES>
 __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
   constexpr int T = WM * WN * 32;
-  constexpr int PA = BM + 8, PB = BN + 8;
+  constexpr int ASZ = TA ? BK * (BM + 8) : BM * (BK + 4);
+  constexpr int BSZ = TB ? BN * (BK + 4) : BK * (BN + 8);
   constexpr int MT = BM / WM / 8, NT = BN / WN / 8;
   extern __shared__ __align__(16) double sm[];
-  double* As = sm;                   // [2][BK][PA]
-  double* Bs = sm + 2 * BK * PA;     // [2][BK][PB]
+  double* As = sm;
+  double* Bs = sm + STAGES * ASZ;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WM, wn = warp / WM;
@@ -69,8 +80,8 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
   if (g.split) {
     const long long kb = bz * g.Kc;
     K = (int)min((long long)g.Kc, (long long)g.K - kb);
-    A = g.A + (g.tA ? kb * g.lda : kb);
-    B = g.B + (g.tB ? kb : kb * g.ldb);
+    A = g.A + (TA ? kb * g.lda : kb);
+    B = g.B + (TB ? kb : kb * g.ldb);
   } else {
     K = g.K;
     A = g.A + bz * g.sA;
@@ -85,61 +96,93 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
 
   auto load = [&](int kt, int st) {
     const int k0 = kt * BK;
-    double* as = As + st * BK * PA;
-    double* bs = Bs + st * BK * PB;
+    double* as = As + st * ASZ;
+    double* bs = Bs + st * BSZ;
+    // A tile: BM x BK
+    {
+      constexpr int CONT = TA ? BM : BK;   // contiguous extent in global
+      constexpr int OUTER = TA ? BK : BM;
+      constexpr int V = VEC;                // doubles per copy
+      constexpr int PER = CONT / V;
 #pragma unroll
-    for (int e0 = 0; e0 < BK * BM; e0 += T) {
-      int e = e0 + tid;
-      int ml, kl;
-      if (!g.tA) { ml = e / BK; kl = e % BK; } else { kl = e / BM; ml = e % BM; }
-      int m = bm0 + ml, k = k0 + kl;
-      bool ok = (m < M) && (k < K);
-      const double* src = ok ? (g.tA ? A + (long long)k * g.lda + m : A + (long long)m * g.lda + k) : A;
-      cp_async8(as + kl * PA + ml, src, ok);
+      for (int e0 = 0; e0 < OUTER * PER; e0 += T) {
+        const int e = e0 + tid;
+        if (OUTER * PER % T != 0 && e >= OUTER * PER) break;
+        const int o = e / PER, c = (e % PER) * V;
+        int m, k;
+        if (TA) { k = o; m = c; } else { m = o; k = c; }
+        const int gm = bm0 + m, gk = k0 + k;
+        double* dst = TA ? (as + k * (BM + 8) + m) : (as + m * (BK + 4) + k);
+        const int rowok = TA ? (gk < K) : (gm < M);
+        const int lim = TA ? (M - gm) : (K - gk);  // elements available along the contiguous dim
+        const int avail = rowok ? (lim >= V ? V : (lim > 0 ? lim : 0)) : 0;
+        const double* src = avail ? (TA ? A + (long long)gk * g.lda + gm : A + (long long)gm * g.lda + gk) : A;
+        if (V == 2) cp_async16(dst, src, avail * 8);
+        else cp_async8(dst, src, avail > 0);
+      }
     }
+    // B tile: BK x BN
+    {
+      constexpr int CONT = TB ? BK : BN;
+      constexpr int OUTER = TB ? BN : BK;
+      constexpr int V = VEC;
+      constexpr int PER = CONT / V;
 #pragma unroll
-    for (int e0 = 0; e0 < BK * BN; e0 += T) {
-      int e = e0 + tid;
-      int nl, kl;
-      if (!g.tB) { kl = e / BN; nl = e % BN; } else { nl = e / BK; kl = e % BK; }
-      int n = bn0 + nl, k = k0 + kl;
-      bool ok = (n < N) && (k < K);
-      const double* src = ok ? (g.tB ? B + (long long)n * g.ldb + k : B + (long long)k * g.ldb + n) : B;
-      cp_async8(bs + kl * PB + nl, src, ok);
+      for (int e0 = 0; e0 < OUTER * PER; e0 += T) {
+        const int e = e0 + tid;
+        if (OUTER * PER % T != 0 && e >= OUTER * PER) break;
+        const int o = e / PER, c = (e % PER) * V;
+        int n, k;
+        if (TB) { n = o; k = c; } else { k = o; n = c; }
+        const int gn = bn0 + n, gk = k0 + k;
+        double* dst = TB ? (bs + n * (BK + 4) + k) : (bs + k * (BN + 8) + n);
+        const int rowok = TB ? (gn < N) : (gk < K);
+        const int lim = TB ? (K - gk) : (N - gn);
+        const int avail = rowok ? (lim >= V ? V : (lim > 0 ? lim : 0)) : 0;
+        const double* src = avail ? (TB ? B + (long long)gn * g.ldb + gk : B + (long long)gk * g.ldb + gn) : B;
+        if (V == 2) cp_async16(dst, src, avail * 8);
+        else cp_async8(dst, src, avail > 0);
+      }
     }
   };
 
   const int nk = (K + BK - 1) / BK;
-  if (nk > 0) {
-    load(0, 0);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load(s, s);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load(kt + 1, (kt + 1) & 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const double* as = As + (kt & 1) * BK * PA;
-    const double* bs = Bs + (kt & 1) * BK * PB;
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) load(nxt, nxt % STAGES);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * ASZ;
+    const double* bs = Bs + (kt % STAGES) * BSZ;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[MT], bf[NT];
       const int kr = kk + (lane & 3);
 #pragma unroll
-      for (int i = 0; i < MT; ++i) af[i] = as[kr * PA + wm * (BM / WM) + i * 8 + (lane >> 2)];
+      for (int i = 0; i < MT; ++i) {
+        const int mr = wm * (BM / WM) + i * 8 + (lane >> 2);
+        af[i] = TA ? as[kr * (BM + 8) + mr] : as[mr * (BK + 4) + kr];
+      }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) bf[j] = bs[kr * PB + wn * (BN / WN) + j * 8 + (lane >> 2)];
+      for (int j = 0; j < NT; ++j) {
+        const int nc = wn * (BN / WN) + j * 8 + (lane >> 2);
+        bf[j] = TB ? bs[nc * (BK + 4) + kr] : bs[kr * (BN + 8) + nc];
+      }
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
@@ -161,18 +204,41 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
   }
 }
 
-template <int BM, int BN, int WM, int WN>
-int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
+template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC>
+int launch_gemm_t(const GemmArgs& g, int batch, cudaStream_t st) {
+  constexpr int STAGES = 3;
   constexpr int T = WM * WN * 32;
-  size_t smem = (size_t)2 * BK * ((BM + 8) + (BN + 8)) * sizeof(double);
+  constexpr int ASZ = TA ? BK * (BM + 8) : BM * (BK + 4);
+  constexpr int BSZ = TB ? BN * (BK + 4) : BK * (BN + 8);
+  const size_t smem = (size_t)STAGES * (ASZ + BSZ) * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(dgemm_kernel<BM, BN, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), batch);
-  dgemm_kernel<BM, BN, WM, WN><<<grid, T, smem, st>>>(g); ttb_count();
+  dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES><<<grid, T, smem, st>>>(g); ttb_count();
   return ttb_last_error();
+}
+
+template <int BM, int BN, int WM, int WN>
+int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
+  // 16-byte copies when both operands' rows (and batch strides) keep 16 B alignment
+  const bool vec = ((g.lda & 1) == 0) && ((g.ldb & 1) == 0) && ((((uintptr_t)g.A) & 15) == 0) &&
+                   ((((uintptr_t)g.B) & 15) == 0) && ((g.sA & 1) == 0) && ((g.sB & 1) == 0) &&
+                   (!g.split || (g.Kc & 1) == 0);
+  const int key = (g.tA ? 1 : 0) | (g.tB ? 2 : 0) | (vec ? 4 : 0);
+  switch (key) {
+    case 0: return launch_gemm_t<BM, BN, WM, WN, 0, 0, 1>(g, batch, st);
+    case 1: return launch_gemm_t<BM, BN, WM, WN, 1, 0, 1>(g, batch, st);
+    case 2: return launch_gemm_t<BM, BN, WM, WN, 0, 1, 1>(g, batch, st);
+    case 3: return launch_gemm_t<BM, BN, WM, WN, 1, 1, 1>(g, batch, st);
+    case 4: return launch_gemm_t<BM, BN, WM, WN, 0, 0, 2>(g, batch, st);
+    case 5: return launch_gemm_t<BM, BN, WM, WN, 1, 0, 2>(g, batch, st);
+    case 6: return launch_gemm_t<BM, BN, WM, WN, 0, 1, 2>(g, batch, st);
+    default: return launch_gemm_t<BM, BN, WM, WN, 1, 1, 2>(g, batch, st);
+  }
 }
 
 __global__ void scale_kernel(long long n, double beta, double* C, long long ldc, int M, int N, long long sC) {

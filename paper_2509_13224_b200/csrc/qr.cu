@@ -33,16 +33,20 @@ __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, 
   const int r0 = blockIdx.x * chunk;
   const int r1 = min(m, r0 + chunk);
 
+  // partial buffers: norms double-buffered by column parity, then the dot products
+  double* npart = part;                 // [2][nblk]
+  double* dpart = part + 2 * nblk;      // [nblk][NB]
+  {
+    double s = 0.0;
+    for (int i = max(r0, 1) + threadIdx.x; i < r1; i += PT) s += P[i] * P[i];
+    s = block_sum(s, sred);
+    if (threadIdx.x == 0) npart[blockIdx.x] = s;
+    grid.sync();
+  }
   for (int j = 0; j < jb; ++j) {
     double* col = P + (long long)j * ld;
-    // 1) sum of squares below the diagonal
-    double s = 0.0;
-    for (int i = max(r0, j + 1) + threadIdx.x; i < r1; i += PT) s += col[i] * col[i];
-    s = block_sum(s, sred);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
-    grid.sync();
     double xn2 = 0.0;
-    for (int b = 0; b < nblk; ++b) xn2 += part[b];
+    for (int b = 0; b < nblk; ++b) xn2 += npart[(j & 1) * nblk + b];
     const double alpha = col[j];
     double beta, t, scal;
     if (xn2 == 0.0) {
@@ -74,20 +78,35 @@ __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, 
     if (threadIdx.x < NB) {
       double v = 0.0;
       for (int w = 0; w < PT / 32; ++w) v += swarp[w][threadIdx.x];
-      part[nblk + (long long)blockIdx.x * NB + threadIdx.x] = v;
+      dpart[(long long)blockIdx.x * NB + threadIdx.x] = v;
     }
     grid.sync();
     if (threadIdx.x < NB) {
       double v = 0.0;
-      for (int b = 0; b < nblk; ++b) v += part[nblk + (long long)b * NB + threadIdx.x];
+      for (int b = 0; b < nblk; ++b) v += dpart[(long long)b * NB + threadIdx.x];
       sw[threadIdx.x] = v;
     }
     __syncthreads();
-    // 3) apply H_j to the remaining panel columns (own rows); v_j == 1
+    // 3) apply H_j to the remaining panel columns (own rows, all columns of a row loaded first
+    //    so the read-modify-writes are independent), and accumulate the next column's norm
+    double ss = 0.0;
     for (int i = max(r0, j) + threadIdx.x; i < r1; i += PT) {
       const double v = (i == j) ? 1.0 : col[i];
-      for (int c = j + 1; c < jb; ++c) P[(long long)c * ld + i] -= t * v * sw[c];
+      const double tv = t * v;
+      double vals[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c > j && c < jb) vals[c] = P[(long long)c * ld + i];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c > j && c < jb) {
+          const double nv = vals[c] - tv * sw[c];
+          P[(long long)c * ld + i] = nv;
+          if (c == j + 1 && i > j + 1) ss += nv * nv;
+        }
     }
+    ss = block_sum(ss, sred);
+    if (threadIdx.x == 0) npart[((j + 1) & 1) * nblk + blockIdx.x] = ss;
     if (blockIdx.x == 0 && threadIdx.x == 0) tau[j] = t;
     // diagonal entry becomes beta (owner CTA, after everyone has read alpha via grid.sync below)
     grid.sync();

@@ -47,12 +47,14 @@ __device__ void jacobi_core(int n, double* A, double* V, int* flag, int max_swee
           ap[i] = c * x - s * y;
           aq[i] = s * x + c * y;
         }
-        double* vp = V + (long long)p * n;
-        double* vq = V + (long long)q * n;
-        for (int i = lane; i < n; i += 32) {
-          double x = vp[i], y = vq[i];
-          vp[i] = c * x - s * y;
-          vq[i] = s * x + c * y;
+        if (V) {
+          double* vp = V + (long long)p * n;
+          double* vq = V + (long long)q * n;
+          for (int i = lane; i < n; i += 32) {
+            double x = vp[i], y = vq[i];
+            vp[i] = c * x - s * y;
+            vq[i] = s * x + c * y;
+          }
         }
       }
       __syncthreads();
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(int n, double* Ag, long long
   const long long b = blockIdx.x;
   double* Ain = Ag + b * strideA;
   double* U = Ug + b * strideUV;
-  double* Vout = Vg + b * strideUV;
+  double* Vout = Vg ? Vg + b * strideUV : nullptr;
   double* S = Sg + b * strideS;
   const long long nn = (long long)n * n;
   double *A, *V;
@@ -85,9 +87,10 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(int n, double* Ag, long long
     A = work + b * (2 * nn + n);
     V = A + nn;
   }
+  if (!Vg) V = nullptr;
   for (long long e = threadIdx.x; e < nn; e += blockDim.x) {
     A[e] = Ain[e];
-    V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
+    if (V) V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
   }
   __syncthreads();
   jacobi_core(n, A, V, &flag, max_sweeps, tol, &nsweep);
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(int n, double* Ag, long long
     double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     for (int i = 0; i < n; ++i) {
       U[(long long)rank * n + i] = A[(long long)j * n + i] * inv;
-      Vout[(long long)rank * n + i] = V[(long long)j * n + i];
+      if (Vout) Vout[(long long)rank * n + i] = V[(long long)j * n + i];
     }
   }
   if (threadIdx.x == 0 && info) info[b] = nsweep;
@@ -159,12 +162,14 @@ __global__ void __launch_bounds__(CT) jacobi_coop_kernel(int n, double* A, doubl
           ap[i] = cs * x - sn * y;
           aq[i] = sn * x + cs * y;
         }
-        double* vp = V + (long long)p * n;
-        double* vq = V + (long long)q * n;
-        for (int i = lane; i < n; i += 32) {
-          double x = vp[i], y = vq[i];
-          vp[i] = cs * x - sn * y;
-          vq[i] = sn * x + cs * y;
+        if (V) {
+          double* vp = V + (long long)p * n;
+          double* vq = V + (long long)q * n;
+          for (int i = lane; i < n; i += 32) {
+            double x = vp[i], y = vq[i];
+            vp[i] = cs * x - sn * y;
+            vq[i] = sn * x + cs * y;
+          }
         }
       }
       grid.sync();
@@ -181,7 +186,7 @@ __global__ void init_av_kernel(int n, const double* Ain, double* A, double* V) {
   const long long nn = (long long)n * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
     A[e] = Ain[e];
-    V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
+    if (V) V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
   }
 }
 
@@ -213,7 +218,7 @@ __global__ void jacobi_scatter_kernel(int n, const double* A, const double* V, c
   const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
   for (int i = lane; i < n; i += 32) {
     U[(long long)rank * n + i] = A[(long long)j * n + i] * inv;
-    Vout[(long long)rank * n + i] = V[(long long)j * n + i];
+    if (Vout) Vout[(long long)rank * n + i] = V[(long long)j * n + i];
   }
 }
 
@@ -245,7 +250,7 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
     if (!work) return TTB_EARG;
     const long long nn = (long long)n * n;
     double* Aw = work;
-    double* Vw = work + nn;
+    double* Vw = V ? work + nn : nullptr;
     double* sig = work + 2 * nn;
     static int* cnt = nullptr;
     static int* sw = nullptr;

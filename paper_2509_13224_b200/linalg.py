@@ -162,32 +162,40 @@ def qr(X):
 # ---------------------------------------------------------------------------
 # SVD
 
-def _jacobi(Rcm, n):
-    """SVD of a col-major n x n matrix held as torch (n, n): returns (U_mem, S, V_mem) col-major."""
+def _jacobi(Rcm, n, want_v=False):
+    """SVD of a col-major n x n matrix held as torch (n, n): returns (U_mem, S, V_mem|None) col-major."""
     S = empty(n)
     U = empty(n, n)
-    V = empty(n, n)
+    V = empty(n, n) if want_v else None
     work = empty(2 * n * n + n) if n > 64 else None
     call("ttb_svd_jacobi", n, ptr(Rcm), n * n, ptr(S), n, ptr(U), ptr(V), n * n, 1, ptr(work), None)
     return U, S, V
 
 
 class SVDFactors:
-    """Lazy thin SVD X = U diag(S) Vt; U columns are formed only for the kept rank."""
+    """Thin SVD X = U diag(S) Vt by Householder QR + one-sided Jacobi on the triangular factor.
 
-    def __init__(self, X):
+    Only the left vectors are rotated; the "carry" S Vt needed by rounding is the
+    backward-stable product U^T X (formed from the triangular factor), so the
+    right vectors are accumulated only when explicitly requested (want_v).
+    Tall X = Q R: Jacobi on R.  Wide X (X^T = Q R): Jacobi on R^T.
+    """
+
+    def __init__(self, X, want_v=False):
         X = X.contiguous()
         m, n = X.shape
         self.m, self.n = m, n
         self.tall = m >= n
         if self.tall:
             Qt, Rt = qr_colmajor(permute(X, (1, 0)), m, n)
-            self.Qt = Qt                      # (n, m)  == col-major Q (m x n)
-            self.UR, self.S, self.V = _jacobi(Rt.contiguous(), n)
+            self.Qt = Qt                      # (n, m) == col-major Q (m x n)
+            self.Rt = Rt                      # (n, n) == col-major R == row-major R^T
+            self.UJ, self.S, self.VJ = _jacobi(Rt.contiguous(), n, want_v)
         else:
-            Qt, Rt = qr_colmajor(X.clone(), n, m)  # QR of X^T (n x m)
-            self.Qt = Qt                      # (m, n) == col-major Q (n x m)
-            self.UR, self.S, self.V = _jacobi(Rt.contiguous(), m)
+            Qt, Rt = qr_colmajor(X.clone(), n, m)  # X^T = Q R, Q (n x m), R (m x m)
+            self.Qt = Qt                      # (m, n) == col-major Q == row-major Q^T
+            self.Rt = Rt                      # row-major R^T
+            self.UJ, self.S, self.VJ = _jacobi(permute(Rt, (1, 0)), m, want_v)  # Jacobi on R^T
 
     def s_host(self):
         return self.S.cpu().numpy()
@@ -195,19 +203,28 @@ class SVDFactors:
     def U(self, r):
         """First r left singular vectors, row-major (m x r)."""
         if self.tall:
-            return gemm(self.Qt, self.UR[:r], tA=True, tB=True)
-        return self.V[:r].t().contiguous()
+            return gemm(self.Qt, self.UJ[:r], tA=True, tB=True)
+        return self.UJ[:r].t().contiguous()
+
+    def SVt(self, r):
+        """diag(S[:r]) Vt[:r] = U[:, :r]^T X  (r x n)."""
+        if self.tall:
+            return gemm(self.UJ[:r], self.Rt, tB=True)          # U_R^T R
+        W = gemm(self.UJ[:r], self.Rt)                          # U'^T R^T  (r x m)
+        return gemm(W, self.Qt)                                 # ... Q^T   (r x n)
 
     def Vt(self, r):
-        """First r right singular vectors as rows (r x n)."""
+        """First r right singular vectors as rows (r x n); needs want_v=True."""
+        if self.VJ is None:
+            raise ValueError("right singular vectors were not accumulated (want_v=False)")
         if self.tall:
-            return self.V[:r].contiguous()
-        return gemm(self.UR[:r], self.Qt)
+            return self.VJ[:r].contiguous()
+        return gemm(self.VJ[:r], self.Qt)
 
 
 def svd(X):
     """np.linalg.svd(X, full_matrices=False) on the device: (U, S, Vt)."""
-    f = SVDFactors(X)
+    f = SVDFactors(X, want_v=True)
     k = min(f.m, f.n)
     return f.U(k), f.S, f.Vt(k)
 

@@ -434,7 +434,7 @@ def tt_round(t, eps, max_rank=None):
         s = f.s_host()
         keep = _chop(s, delta, max_rank)
         cores[k] = f.U(keep).reshape(r0, n, keep)
-        carry = f.S[:keep, None] * f.Vt(keep)
+        carry = f.SVt(keep)
         nxt = cores[k + 1]
         cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1)).reshape(keep, nxt.shape[1], nxt.shape[2])
     return _unfused(cores, tag)
@@ -455,7 +455,7 @@ def tt_from_full(X, eps=1e-14, max_rank=None):
         f = L.SVDFactors(Cm)
         keep = _chop(f.s_host(), delta, max_rank) if total > 0 else 1
         cores.append(f.U(keep).reshape(r, sizes[k], keep))
-        Cm = f.S[:keep, None] * f.Vt(keep)
+        Cm = f.SVt(keep)
         r = keep
     cores.append(Cm.reshape(r, sizes[-1], 1))
     return TtTensor(cores)

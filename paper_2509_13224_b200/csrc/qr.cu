@@ -13,8 +13,9 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
 
 namespace {
 
-constexpr int NB = 32;
+constexpr int NB = 16;  // inner Householder panel width (memory-bound part)
 constexpr int PT = 256;  // threads per CTA of the panel kernel
+constexpr int kMaxPanelBlocks = 1024;  // sizing of the per-CTA partial buffers
 
 // Factor the m x jb panel P (col-major, ld) in place. Writes tau[0..jb), the explicit
 // reflectors V (m x jb col-major, ld m: unit diagonal, zeros above) and the WY factor T
@@ -191,7 +192,7 @@ int panel_grid(int m) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_qr_kernel, PT, 0);
-    max_blocks = sms * (per_sm > 0 ? (per_sm > 2 ? 2 : per_sm) : 1);
+    max_blocks = sms * (per_sm > 0 ? (per_sm > 4 ? 4 : per_sm) : 1);
   }
   int want = ceil_div(m, 4 * PT);  // >= 1024 rows per CTA before going wider
   if (want < 1) want = 1;
@@ -236,7 +237,7 @@ QrWs carve(double* ws, int m, int n) {
   const long long wn = (long long)(n > k ? n : k);
   QrWs w;
   w.part = ws;
-  w.Vp = w.part + (long long)296 * (NB * NB + NB) + 296;
+  w.Vp = w.part + (long long)kMaxPanelBlocks * (NB * NB + NB + 2);
   w.Vb = w.Vp + (long long)m * NB;
   w.W = w.Vb + (long long)m * NB2;
   w.W2 = w.W + wn * NB2;
@@ -269,7 +270,7 @@ int apply_wy(void* stream, int mp, int nq, int jb, const double* V, const double
 TTB_API long long ttb_qr_workspace(int m, int n) {
   const int k = m < n ? m : n;
   const long long wn = (long long)(n > k ? n : k);
-  long long s = (long long)296 * (NB * NB + NB) + 296;
+  long long s = (long long)kMaxPanelBlocks * (NB * NB + NB + 2);
   s += (long long)m * NB + (long long)m * NB2 + 2 * wn * NB2 + (long long)NB2 * NB2;
   s += (long long)((k + NB - 1) / NB) * NB * NB + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
   return s + 64;

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(int n, double* Ag, long long
   jacobi_core(n, A, V, &flag, max_sweeps, tol, &nsweep);
   __syncthreads();
   // column norms, descending order rank (stable by index)
-  double* sig = SMEM ? (dyn + 2 * nn) : (work + b * (2 * nn + n) + 2 * nn);
+  double* sig = SMEM ? (dyn + (Vg ? 2 : 1) * nn) : (work + b * (2 * nn + n) + 2 * nn);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = wid; j < n; j += nw) {
     double s = 0.0;
@@ -234,11 +234,11 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
   const double tol = 4.0e-16 * (n > 16 ? sqrt((double)n) : 4.0);
   int threads = n >= 64 ? JT : ((n + 1) / 2 * 32 > 1024 ? 1024 : ((n + 1) / 2) * 32);
   if (threads < 32) threads = 32;
-  if (n <= 64) {
-    size_t smem = ((size_t)2 * n * n + n) * sizeof(double);
+  const size_t smem = ((size_t)(V ? 2 : 1) * n * n + n) * sizeof(double);
+  if (smem <= 200 * 1024) {
     static bool cfg = false;
     if (!cfg) {
-      cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+      cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cfg = true;
     }
     jacobi_kernel<true><<<batch, threads, smem, st>>>(n, A, strideA, S, strideS, U, V, strideUV, nullptr, max_sweeps,

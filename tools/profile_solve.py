@@ -57,7 +57,7 @@ def _timed_solve(self, *a, **k):
     t = time.perf_counter()
     r = _orig_solve(self, *a, **k)
     torch.cuda.synchronize()
-    key = f"LocalSystem.solve({'direct' if self.size <= a[2] else 'pcg'})"
+    key = f"LocalSystem.solve({'direct' if self.size <= a[3] else 'pcg'})"
     T[key] += time.perf_counter() - t
     N[key] += 1
     return r

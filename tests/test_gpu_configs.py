@@ -1,0 +1,94 @@
+"""BASELINE configs on the GPU vs the CPU oracle (same seeds, same tolerances).
+
+configs[0] and configs[1] run at their full sizes (n=32 p=2 unit cube; n=128 p=3
+quarter cylinder, 2.1e6 dofs). configs[2], configs[3] (non-separable geometry,
+operator ranks 40-80) run at reduced n because the CPU oracle needs minutes at full
+size; configs[4] is checked at n=48 on the same geometry family as configs[1].
+
+Tolerances: operator K and load f relative Frobenius difference <= 1e-9 (both are
+the same cross/rounding trajectory up to floating point; allowed 1e-6 when the
+eps is 1e-8 and a pivot flips, see the rank check); solution <= 1e-6 relative
+(both solvers stop at their residual tolerance, cond(K) ~ 1e3-1e4); L1-type
+L2 error within 1% of the oracle's; every TT rank within +-2.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _tt_rel(a, b):
+    from paper_2509_13224_b200.tensor_train import tt_norm, tt_sub
+    return tt_norm(tt_sub(a, b)) / tt_norm(b)
+
+
+def _to_gpu(o, band=None):
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor
+    if hasattr(o, "row_sizes"):
+        M = TtMatrix([torch.as_tensor(G, device="cuda") for G in o.cores])
+        return TtMatrix.banded_from_dense_cores(M.cores, band) if band is not None else M
+    return TtTensor([torch.as_tensor(G, device="cuda") for G in o.cores])
+
+
+def _ranks_close(a, b, slack=2):
+    return len(a) == len(b) and all(abs(x - y) <= slack for x, y in zip(a, b))
+
+
+def _run(cfg_kw, opts=None, compare_u=True, want_error=True):
+    from oracle import iga as OI
+    from oracle import tt as OT
+    from paper_2509_13224_b200 import driver as D
+    kw = dict(cfg_kw)
+    if opts:
+        kw["solver"] = opts
+    rep = D.solve_poisson(D.SolveConfig(seed=0, **kw), want_error=want_error)
+    ref = OI.solve(OI.Config(seed=0, **kw), want_error=want_error)
+    p = max(rep.config.degree)
+    eK = _tt_rel(rep.K, _to_gpu(ref["K"], band=p))
+    ef = _tt_rel(rep.f, _to_gpu(ref["f"]))
+    out = {"eK": eK, "ef": ef, "rep": rep, "ref": ref}
+    assert _ranks_close(rep.ranks_K, ref["ranks_K"]), (rep.ranks_K, ref["ranks_K"])
+    assert _ranks_close(rep.ranks_f, ref["ranks_f"]), (rep.ranks_f, ref["ranks_f"])
+    if compare_u:
+        out["eu"] = _tt_rel(rep.u, _to_gpu(ref["u"]))
+        assert _ranks_close(rep.ranks_u, ref["ranks_u"]), (rep.ranks_u, ref["ranks_u"])
+    if ref["l2_error"] is not None:
+        assert abs(rep.l2_error - ref["l2_error"]) <= 0.01 * ref["l2_error"], (rep.l2_error, ref["l2_error"])
+    return out
+
+
+def test_configs0_full_size():
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    r = _run(SOLVE_CONFIGS[0])
+    assert r["eK"] <= 1e-9 and r["ef"] <= 1e-9 and r["eu"] <= 1e-6, (r["eK"], r["ef"], r["eu"])
+    assert r["rep"].solver_converged and r["rep"].dofs == 32 ** 3
+
+
+def test_configs1_full_size():
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    r = _run(SOLVE_CONFIGS[1], want_error=False)  # oracle error quadrature over 1.25e8 points is minutes
+    assert r["eK"] <= 1e-9 and r["ef"] <= 1e-9 and r["eu"] <= 1e-6, (r["eK"], r["ef"], r["eu"])
+    assert r["rep"].solver_converged and r["rep"].dofs == 128 ** 3
+
+
+def test_configs2_reduced():
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    kw = dict(SOLVE_CONFIGS[2], n_basis=8)
+    r = _run(kw)
+    assert r["eK"] <= 1e-6 and r["ef"] <= 1e-6 and r["eu"] <= 1e-5, (r["eK"], r["ef"], r["eu"])
+
+
+def test_configs3_reduced():
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    kw = dict(SOLVE_CONFIGS[3], n_basis=8)
+    r = _run(kw, opts={"max_sweeps": 8})
+    assert r["eK"] <= 1e-6 and r["ef"] <= 1e-6, (r["eK"], r["ef"])
+
+
+def test_configs4_family_reduced():
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    kw = dict(SOLVE_CONFIGS[4], n_basis=48)
+    r = _run(kw)
+    assert r["eK"] <= 1e-9 and r["ef"] <= 1e-9 and r["eu"] <= 1e-6, (r["eK"], r["ef"], r["eu"])

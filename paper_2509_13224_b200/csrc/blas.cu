@@ -335,8 +335,10 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
   GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};
   long long work = (long long)M * N * batch;
   const bool big = work >= (long long)148 * 128 * 128 * 2 && M >= 128 && N >= 128;
+  const bool narrow = !big && N <= 32 && M >= 48;  // thin outputs (WY products over panel widths)
   const long long tiles = big ? (long long)ceil_div(M, 128) * ceil_div(N, 128) * batch
-                              : (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch;
+                        : narrow ? (long long)ceil_div(M, 128) * ceil_div(N, 32) * batch
+                                 : (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch;
   if (batch == 1 && tiles < 148 && K >= 1024) {
     // split-K: enough K chunks to cover ~2 waves, each chunk >= 256 deep, deterministic reduction
     long long S = (296 + tiles - 1) / tiles;
@@ -349,7 +351,8 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
       if (!part) return (int)cudaErrorMemoryAllocation;
       GemmArgs p = g;
       p.alpha = 1.0; p.beta = 0.0; p.C = part; p.ldc = N; p.sC = (long long)M * N; p.split = 1; p.Kc = Kc;
-      int rc = big ? launch_gemm<128, 128, 2, 4>(p, (int)S, st) : launch_gemm<64, 64, 2, 2>(p, (int)S, st);
+      int rc = big ? launch_gemm<128, 128, 2, 4>(p, (int)S, st)
+                   : narrow ? launch_gemm<128, 32, 4, 1>(p, (int)S, st) : launch_gemm<64, 64, 2, 2>(p, (int)S, st);
       if (rc) return rc;
       long long tot = (long long)M * N;
       int blocks = ceil_div(tot, 256);
@@ -359,6 +362,7 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
     }
   }
   if (big) return launch_gemm<128, 128, 2, 4>(g, batch, st);
+  if (narrow) return launch_gemm<128, 32, 4, 1>(g, batch, st);
   return launch_gemm<64, 64, 2, 2>(g, batch, st);
 }
 

@@ -22,77 +22,99 @@ constexpr int kMaxPanelBlocks = 1024;  // sizing of the per-CTA partial buffers
 // (jb x jb row-major, upper triangular). part: gridDim.x * (NB*NB + NB) doubles.
 __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, long long ld, double* tau, double* V,
                                                       double* T, double* part) {
+  // One pass over the panel and ONE grid-wide barrier per column. While column j's reflector
+  // is applied to a row, the row's updated entries are already folded into the next column's
+  // statistics (its squared norm and z_c = x^T P[:, c]), so the reflector of column j+1 is
+  // known right after the barrier: w_c = v^T P[:, c] = P[j+1, c] + scal * z_c. Writes of the
+  // pivot row j are deferred by one column (it is read by every CTA at the start of column j).
   cg::grid_group grid = cg::this_grid();
-  __shared__ double sred[32];
-  __shared__ double swarp[PT / 32][NB];
+  constexpr int ZW = NB + 1;  // z_c for c < NB, norm at index NB
+  __shared__ double swarp[PT / 32][ZW];
+  __shared__ double sz[ZW];
   __shared__ double sw[NB];
+  __shared__ double srow[NB];
+  __shared__ double sbeta[NB];
   __shared__ double sG[NB * NB];
   const int nblk = gridDim.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // contiguous row chunk per CTA
   const int chunk = (m + nblk - 1) / nblk;
   const int r0 = blockIdx.x * chunk;
   const int r1 = min(m, r0 + chunk);
+  double* zpart = part;  // [2][nblk][ZW]
 
-  // partial buffers: norms double-buffered by column parity, then the dot products
-  double* npart = part;                 // [2][nblk]
-  double* dpart = part + 2 * nblk;      // [nblk][NB]
-  {
-    double s = 0.0;
-    for (int i = max(r0, 1) + threadIdx.x; i < r1; i += PT) s += P[i] * P[i];
-    s = block_sum(s, sred);
-    if (threadIdx.x == 0) npart[blockIdx.x] = s;
-    grid.sync();
-  }
-  for (int j = 0; j < jb; ++j) {
-    double* col = P + (long long)j * ld;
-    double xn2 = 0.0;
-    for (int b = 0; b < nblk; ++b) xn2 += npart[(j & 1) * nblk + b];
-    const double alpha = col[j];
-    double beta, t, scal;
-    if (xn2 == 0.0) {
-      beta = alpha; t = 0.0; scal = 0.0;
-    } else {
-      double nrm = sqrt(alpha * alpha + xn2);
-      beta = alpha >= 0.0 ? -nrm : nrm;
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    // 2) scale v (own rows), partial dots w_c = v^T P[:, c] for c > j
-    double acc[NB];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) acc[c] = 0.0;
-    for (int i = max(r0, j) + threadIdx.x; i < r1; i += PT) {
-      double v;
-      if (i == j) v = 1.0;
-      else { v = col[i] * scal; col[i] = v; }
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (c > j && c < jb) acc[c] += v * P[(long long)c * ld + i];
-    }
+  auto reduce_store = [&](double* acc, double nz, int buf) {
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
       double v = warp_sum(acc[c]);
       if (lane == 0) swarp[wid][c] = v;
     }
+    {
+      double v = warp_sum(nz);
+      if (lane == 0) swarp[wid][NB] = v;
+    }
     __syncthreads();
-    if (threadIdx.x < NB) {
+    if (threadIdx.x < ZW) {
       double v = 0.0;
       for (int w = 0; w < PT / 32; ++w) v += swarp[w][threadIdx.x];
-      dpart[(long long)blockIdx.x * NB + threadIdx.x] = v;
+      zpart[((long long)buf * nblk + blockIdx.x) * ZW + threadIdx.x] = v;
     }
+  };
+
+  {  // statistics of column 0: ||x||^2 and z_c = x^T P[:, c] over rows > 0
+    double acc[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+    double nz = 0.0;
+    for (int i = max(r0, 1) + threadIdx.x; i < r1; i += PT) {
+      const double x = P[i];
+      nz += x * x;
+#pragma unroll
+      for (int c = 1; c < NB; ++c)
+        if (c < jb) acc[c] += x * P[(long long)c * ld + i];
+    }
+    reduce_store(acc, nz, 0);
     grid.sync();
-    if (threadIdx.x < NB) {
+  }
+  for (int j = 0; j < jb; ++j) {
+    const int buf = j & 1;
+    if (threadIdx.x < ZW) {
       double v = 0.0;
-      for (int b = 0; b < nblk; ++b) v += dpart[(long long)b * NB + threadIdx.x];
-      sw[threadIdx.x] = v;
+      for (int b = 0; b < nblk; ++b) v += zpart[((long long)buf * nblk + b) * ZW + threadIdx.x];
+      sz[threadIdx.x] = v;
+    }
+    // deferred write of pivot row j-1 (nobody reads it during column j)
+    if (j >= 1 && (j - 1) >= r0 && (j - 1) < r1)
+      for (int c = j + threadIdx.x; c < jb; c += PT) P[(long long)c * ld + (j - 1)] = srow[c];
+    __syncthreads();
+    const double xn2 = sz[NB];
+    const double alpha = P[(long long)j * ld + j];
+    double beta, t, scal;
+    if (xn2 == 0.0) {
+      beta = alpha; t = 0.0; scal = 0.0;
+    } else {
+      const double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (threadIdx.x < NB) {
+      const int c = threadIdx.x;
+      if (c > j && c < jb) {
+        const double pjc = P[(long long)c * ld + j];
+        const double w = pjc + scal * sz[c];
+        sw[c] = w;
+        srow[c] = pjc - t * w;   // new pivot-row entry (written one column later by its owner)
+      }
+      if (c == 0) sbeta[j] = beta;
     }
     __syncthreads();
-    // 3) apply H_j to the remaining panel columns (own rows, all columns of a row loaded first
-    //    so the read-modify-writes are independent), and accumulate the next column's norm
-    double ss = 0.0;
-    for (int i = max(r0, j) + threadIdx.x; i < r1; i += PT) {
-      const double v = (i == j) ? 1.0 : col[i];
+    double acc[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+    double nz = 0.0;
+    for (int i = max(r0, j + 1) + threadIdx.x; i < r1; i += PT) {
+      const double v = scal * P[(long long)j * ld + i];
+      P[(long long)j * ld + i] = v;
       const double tv = t * v;
       double vals[NB];
 #pragma unroll
@@ -101,18 +123,27 @@ __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, 
 #pragma unroll
       for (int c = 0; c < NB; ++c)
         if (c > j && c < jb) {
-          const double nv = vals[c] - tv * sw[c];
-          P[(long long)c * ld + i] = nv;
-          if (c == j + 1 && i > j + 1) ss += nv * nv;
+          vals[c] -= tv * sw[c];
+          P[(long long)c * ld + i] = vals[c];
         }
+      if (i > j + 1 && j + 1 < jb) {
+        double xn = 0.0;
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c == j + 1) xn = vals[c];
+        nz += xn * xn;
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c > j + 1 && c < jb) acc[c] += xn * vals[c];
+      }
     }
-    ss = block_sum(ss, sred);
-    if (threadIdx.x == 0) npart[((j + 1) & 1) * nblk + blockIdx.x] = ss;
+    reduce_store(acc, nz, buf ^ 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) tau[j] = t;
-    // diagonal entry becomes beta (owner CTA, after everyone has read alpha via grid.sync below)
     grid.sync();
-    if (j >= r0 && j < r1 && threadIdx.x == 0) col[j] = beta;
   }
+  // the diagonal (beta) of every owned pivot row (the last pivot row has no entries right of it)
+  for (int j = threadIdx.x; j < jb; j += PT)
+    if (j >= r0 && j < r1) P[(long long)j * ld + j] = sbeta[j];
   grid.sync();
   // explicit V and the Gram G = V^T V partials
   for (int i = r0 + threadIdx.x; i < r1; i += PT) {

@@ -153,11 +153,12 @@ def run_b200(args):
     from paper_2509_13224_b200 import _lib
     from paper_2509_13224_b200 import linalg as L
     from paper_2509_13224_b200.tensor_train import tt_matvec, tt_round
+    from paper_2509_13224_b200.replicas import max_over_ranks, replica_seed, whole_job_rate
     from paper_2509_13224_b200.workloads import matvec_round_flops, matvec_round_instance, matvec_round_shapes
 
     lib = _lib.lib()
     n = args.n
-    A, X = matvec_round_instance(n, R_OP, R_VEC, 3, seed=rank)
+    A, X = matvec_round_instance(n, R_OP, R_VEC, 3, seed=replica_seed(0, rank))
     Rs, rs = matvec_round_shapes(n, R_OP, R_VEC, 3)
 
     def step():
@@ -194,12 +195,8 @@ def run_b200(args):
     launches = int(lib.ttb_launch_count(1))
     prof = L.gemm_profile(False)
     ms = e0.elapsed_time(e1) / args.steps
-    ms_all = ms
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_all = float(t.item())
-    value = flops * world / (ms_all / 1e3) / 1e9
+    ms_all = max_over_ranks(ms, device="cuda")
+    value = whole_job_rate(flops, ms_all, world) / 1e9
 
     # roofline of the dominant kernel (DMMA GEMM): algorithmic flops / event-timed duration, summed
     g_ms = sum(a.elapsed_time(b) for a, b, _ in prof)
@@ -253,11 +250,8 @@ def run_b200(args):
     torch.cuda.synchronize()
     barrier()
     e2e_ms = t0.elapsed_time(t1) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = flops * world / (e2e_ms / 1e3) / 1e9
+    e2e_ms = max_over_ranks(e2e_ms, device="cuda")
+    e2e_value = whole_job_rate(flops, e2e_ms, world) / 1e9
     del hA, hX, outs, Yd, dA, dX
 
     line = None

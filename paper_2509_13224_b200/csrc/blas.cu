@@ -334,7 +334,7 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
   }
   GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};
   long long work = (long long)M * N * batch;
-  const bool big = work >= (long long)148 * 128 * 128 * 2 && M >= 128 && N >= 128;
+  const bool big = (work >= (long long)148 * 128 * 128 * 2 || K >= 8192) && M >= 128 && N >= 128;
   const bool narrow = !big && N <= 32 && M >= 48;  // thin outputs (WY products over panel widths)
   const long long tiles = big ? (long long)ceil_div(M, 128) * ceil_div(N, 128) * batch
                         : narrow ? (long long)ceil_div(M, 128) * ceil_div(N, 32) * batch

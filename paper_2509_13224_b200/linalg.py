@@ -162,13 +162,16 @@ def qr(X):
 # ---------------------------------------------------------------------------
 # SVD
 
-def _jacobi(Rcm, n, want_v=False):
-    """SVD of a col-major n x n matrix held as torch (n, n): returns (U_mem, S, V_mem|None) col-major."""
+def _jacobi(Rcm, n, want_v=False, info=None):
+    """SVD of a col-major n x n matrix held as torch (n, n): returns (U_mem, S, V_mem|None) col-major.
+
+    ``info`` (optional int32 device tensor) receives the number of Jacobi sweeps.
+    """
     S = empty(n)
     U = empty(n, n)
     V = empty(n, n) if want_v else None
     work = empty(2 * n * n + n) if n > 64 else None
-    call("ttb_svd_jacobi", n, ptr(Rcm), n * n, ptr(S), n, ptr(U), ptr(V), n * n, 1, ptr(work), None)
+    call("ttb_svd_jacobi", n, ptr(Rcm), n * n, ptr(S), n, ptr(U), ptr(V), n * n, 1, ptr(work), ptr(info))
     return U, S, V
 
 

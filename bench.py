@@ -254,6 +254,12 @@ def run_b200(args):
     e2e_value = whole_job_rate(flops, e2e_ms, world) / 1e9
     del hA, hX, outs, Yd, dA, dX
 
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r1_dominant_kernel.json")
+    if os.path.exists(tf):
+        with open(tf) as fh:
+            d = json.load(fh)
+        traffic = d["dram_bytes_read"] + d["dram_bytes_write"]
     line = None
     if rank == 0:
         line = {
@@ -265,9 +271,11 @@ def run_b200(args):
                        "parallelism": f"replicas x{world}", "l2": "inputs 2.4 GB > 126 MB L2, no flush needed"},
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
                     int(d2h), "ms_per_step": e2e_ms},
-            "roofline": {"bound": "fp64", "kernel": "dgemm_kernel (DMMA m8n8k4 f64)",
+            "roofline": {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync m8n8k4 f64)",
+                         "kernel": "dgemm_kernel (middle-core TT-matvec GEMM)",
                          "achieved": big_fl / (big_ms / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": (big_fl / (big_ms / 1e3) / 1e12) / fp64_peak, "traffic": None,
+                         "frac": (big_fl / (big_ms / 1e3) / 1e12) / fp64_peak, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
                          "all_gemms": {"tflops": g_fl / (g_ms / 1e3) / 1e12, "share_of_step": g_ms / args.steps / ms_all,
                                        "launches": len(prof)}},

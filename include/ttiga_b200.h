@@ -51,6 +51,10 @@ int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, double* tau,
 /* Explicit Q (m x kq, col-major) from ttb_geqrf (same ws); kf = reflector count, n_factored = n of geqrf. */
 int ttb_orgqr(void* stream, int m, int kq, int kf, const double* A, long long lda, double* Q, long long ldq, double* ws,
               int n_factored);
+/* Single-CTA shared-memory QR for TT-rank-sized unfoldings (n <= 64, m*n + m*min(m,n) <= 24576):
+ * ttb_qr_small_fits(m, n) says whether it applies; Q (nullable) m x k col-major, R k x n col-major. */
+int ttb_qr_small_fits(int m, int n);
+int ttb_qr_small(void* stream, int m, int n, const double* A, long long lda, double* Q, long long ldq, double* R);
 /* R (k x n col-major) = upper triangle of the geqrf result. */
 int ttb_extract_r(void* stream, int k, int n, const double* A, long long lda, double* R);
 

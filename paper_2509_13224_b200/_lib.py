@@ -34,6 +34,8 @@ SIGNATURES = {
     "ttb_geqrf": (i32, [vp, i32, i32, vp, i64, vp, vp]),
     "ttb_orgqr": (i32, [vp, i32, i32, i32, vp, i64, vp, i64, vp, i32]),
     "ttb_extract_r": (i32, [vp, i32, i32, vp, i64, vp]),
+    "ttb_qr_small_fits": (i32, [i32, i32]),
+    "ttb_qr_small": (i32, [vp, i32, i32, vp, i64, vp, i64, vp]),
     "ttb_svd_jacobi": (i32, [vp, i32, vp, i64, vp, i64, vp, vp, i64, i32, vp, vp]),
     "ttb_lu_solve": (i32, [vp, i32, vp, i64, vp, i32, vp, i64, i32, vp]),
     "ttb_potrf": (i32, [vp, i32, vp, i64, vp]),

@@ -382,3 +382,109 @@ TTB_API int ttb_extract_r(void* stream, int k, int n, const double* A, long long
   extract_r_kernel<<<blocks, 256, 0, as_stream(stream)>>>(k, n, A, lda, R); ttb_count();
   return ttb_last_error();
 }
+
+// ---------------------------------------------------------------------------
+// Small QR in one CTA: the whole m x n matrix and the explicit Q live in shared memory
+// (m*n + m*k <= kSmallQr doubles). This is the shape of almost every TT-rank-sized
+// unfolding in the IGA solves (n = TT rank <= 64), where the blocked multi-kernel path
+// is launch-latency bound. Same Householder convention as ttb_geqrf/ttb_orgqr.
+namespace {
+
+constexpr int SQT = 512;
+constexpr int kSmallQr = 24576;  // doubles of shared memory for A and Q (192 KB)
+
+__global__ void __launch_bounds__(SQT) small_qr_kernel(int m, int n, const double* __restrict__ A, long long lda,
+                                                        double* Q, long long ldq, double* R, int want_q) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ double taus[64];
+  __shared__ double betas[64];
+  __shared__ double w[64];
+  const int k = m < n ? m : n;
+  double* S = sm;               // m x n, col-major, ld m
+  double* Qs = sm + (long long)m * n;  // m x k
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = SQT / 32;
+  for (int e = threadIdx.x; e < m * n; e += SQT) S[e] = A[(long long)(e / m) * lda + (e % m)];
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    double* col = S + (long long)j * m;
+    double s = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < m; i += SQT) s += col[i] * col[i];
+    s = block_sum(s, red);
+    const double alpha = col[j];
+    double beta, t, scal;
+    if (s == 0.0) { beta = alpha; t = 0.0; scal = 0.0; }
+    else {
+      const double nrm = sqrt(alpha * alpha + s);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = j + 1 + threadIdx.x; i < m; i += SQT) col[i] *= scal;
+    __syncthreads();
+    // w_c = v^T S[j:, c] (one warp per column), then S[j:, c] -= t v w_c
+    for (int c = j + 1 + wid; c < n; c += nw) {
+      const double* sc = S + (long long)c * m;
+      double acc = 0.0;
+      for (int i = j + lane; i < m; i += 32) acc += (i == j ? 1.0 : col[i]) * sc[i];
+      acc = warp_sum(acc);
+      if (lane == 0) w[c] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < (n - j - 1) * (m - j); e += SQT) {
+      const int c = j + 1 + e / (m - j), i = j + e % (m - j);
+      S[(long long)c * m + i] -= t * (i == j ? 1.0 : col[i]) * w[c];
+    }
+    if (threadIdx.x == 0) { taus[j] = t; betas[j] = beta; }
+    __syncthreads();
+  }
+  // R (k x n, col-major ld k)
+  for (int e = threadIdx.x; e < k * n; e += SQT) {
+    const int c = e / k, i = e % k;
+    R[e] = (i < c) ? S[(long long)c * m + i] : (i == c ? betas[i] : 0.0);
+  }
+  if (!want_q) return;
+  for (int e = threadIdx.x; e < m * k; e += SQT) Qs[e] = ((e / m) == (e % m)) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = k - 1; j >= 0; --j) {
+    const double* v = S + (long long)j * m;
+    const double t = taus[j];
+    for (int c = j + wid; c < k; c += nw) {
+      const double* qc = Qs + (long long)c * m;
+      double acc = 0.0;
+      for (int i = j + lane; i < m; i += 32) acc += (i == j ? 1.0 : v[i]) * qc[i];
+      acc = warp_sum(acc);
+      if (lane == 0) w[c] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < (k - j) * (m - j); e += SQT) {
+      const int c = j + e / (m - j), i = j + e % (m - j);
+      Qs[(long long)c * m + i] -= t * (i == j ? 1.0 : v[i]) * w[c];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * k; e += SQT) Q[(long long)(e / m) * ldq + (e % m)] = Qs[e];
+}
+
+}  // namespace
+
+// 1 if (m, n) fits the single-CTA shared-memory QR.
+TTB_API int ttb_qr_small_fits(int m, int n) {
+  const long long k = m < n ? m : n;
+  return (n <= 64 && (long long)m * n + (long long)m * k <= kSmallQr) ? 1 : 0;
+}
+
+// Q (m x k col-major, ld ldq; skipped when Q == NULL) and R (k x n col-major, ld k) of col-major A.
+TTB_API int ttb_qr_small(void* stream, int m, int n, const double* A, long long lda, double* Q, long long ldq,
+                         double* R) {
+  if (!ttb_qr_small_fits(m, n) || m < 1 || n < 1) return TTB_EARG;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(small_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallQr * 8);
+    cfg = true;
+  }
+  const long long k = m < n ? m : n;
+  const size_t smem = (size_t)((long long)m * n + (Q ? (long long)m * k : 0)) * sizeof(double);
+  small_qr_kernel<<<1, SQT, smem, as_stream(stream)>>>(m, n, A, lda, Q, ldq, R, Q ? 1 : 0); ttb_count();
+  return ttb_last_error();
+}

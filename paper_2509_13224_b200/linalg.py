@@ -139,6 +139,11 @@ def qr_colmajor(Acm, m, n, want_q=True, want_r=True):
     k = min(m, n)
     if k == 0:
         return empty(0, m), empty(n, 0)
+    if call_raw("ttb_qr_small_fits", m, n):
+        Qt = empty(k, m) if want_q else None
+        Rt = empty(n, k)
+        call("ttb_qr_small", m, n, ptr(Acm), m, ptr(Qt), m, ptr(Rt))
+        return Qt, (Rt if want_r else None)
     ws = empty(int(call_raw("ttb_qr_workspace", m, n)))
     tau = empty(k)
     call("ttb_geqrf", m, n, ptr(Acm), m, ptr(tau), ptr(ws))

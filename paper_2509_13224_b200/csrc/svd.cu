@@ -182,6 +182,108 @@ __global__ void __launch_bounds__(CT) jacobi_coop_kernel(int n, double* A, doubl
   if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
+// Block one-sided Jacobi: the n columns are split into blocks of b; in every round each CTA
+// takes one pair of blocks (tournament order over blocks), stages their 2b columns (and V's)
+// in shared memory and runs a full local sweep over all their column pairs there, so a
+// grid-wide barrier is paid once per block round (nb-1 per sweep) instead of once per
+// column round (n-1 per sweep).
+constexpr int BT = 256;
+
+__global__ void __launch_bounds__(BT) jacobi_block_kernel(int n, int b, double* A, double* V, int* cnt,
+                                                           int max_sweeps, double tol, int* sweeps_out) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  __shared__ int rot;
+  __shared__ int cols[64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = BT / 32;
+  const int nb = (n + b - 1) / b;
+  const int NB2 = (nb + 1) & ~1;
+  double* As = sm;
+  double* Vs = sm + (long long)2 * b * n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { cnt[0] = 0; cnt[1] = 0; }
+  grid.sync();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int* c = cnt + (sweep & 1);
+    for (int r = 0; r < NB2 - 1; ++r) {
+      for (int pr = blockIdx.x; pr < NB2 / 2; pr += gridDim.x) {
+        int bp = rr_index(pr, r, NB2), bq = rr_index(NB2 - 1 - pr, r, NB2);
+        if (bp > bq) { int t = bp; bp = bq; bq = t; }
+        if (bq >= nb) continue;  // dummy block (uniform per CTA)
+        int L = 0;
+        for (int j = bp * b; j < min(n, bp * b + b); ++j) cols[L++] = j;
+        for (int j = bq * b; j < min(n, bq * b + b); ++j) cols[L++] = j;
+        for (int lc = 0; lc < L; ++lc) {
+          const double* src = A + (long long)cols[lc] * n;
+          double* dst = As + (long long)lc * n;
+          for (int i = threadIdx.x; i < n; i += BT) dst[i] = src[i];
+          if (V) {
+            const double* vs = V + (long long)cols[lc] * n;
+            double* vd = Vs + (long long)lc * n;
+            for (int i = threadIdx.x; i < n; i += BT) vd[i] = vs[i];
+          }
+        }
+        if (threadIdx.x == 0) rot = 0;
+        __syncthreads();
+        const int Lp = (L + 1) & ~1;
+        for (int ir = 0; ir < Lp - 1; ++ir) {
+          for (int ip = wid; ip < Lp / 2; ip += nw) {
+            int p = rr_index(ip, ir, Lp), q = rr_index(Lp - 1 - ip, ir, Lp);
+            if (p > q) { int t = p; p = q; q = t; }
+            if (q >= L) continue;
+            double* ap = As + (long long)p * n;
+            double* aq = As + (long long)q * n;
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int i = lane; i < n; i += 32) {
+              const double x = ap[i], y = aq[i];
+              al += x * x; be += y * y; ga += x * y;
+            }
+            al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+            if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+            if (lane == 0) rot = 1;
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+            for (int i = lane; i < n; i += 32) {
+              const double x = ap[i], y = aq[i];
+              ap[i] = cs * x - sn * y;
+              aq[i] = sn * x + cs * y;
+            }
+            if (V) {
+              double* vp = Vs + (long long)p * n;
+              double* vq = Vs + (long long)q * n;
+              for (int i = lane; i < n; i += 32) {
+                const double x = vp[i], y = vq[i];
+                vp[i] = cs * x - sn * y;
+                vq[i] = sn * x + cs * y;
+              }
+            }
+          }
+          __syncthreads();
+        }
+        for (int lc = 0; lc < L; ++lc) {
+          double* dst = A + (long long)cols[lc] * n;
+          const double* src = As + (long long)lc * n;
+          for (int i = threadIdx.x; i < n; i += BT) dst[i] = src[i];
+          if (V) {
+            double* vd = V + (long long)cols[lc] * n;
+            const double* vs = Vs + (long long)lc * n;
+            for (int i = threadIdx.x; i < n; i += BT) vd[i] = vs[i];
+          }
+        }
+        if (threadIdx.x == 0 && rot) atomicAdd(c, 1);
+        __syncthreads();
+      }
+      grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(sweep + 1) & 1] = 0;
+    const int done = (*(volatile int*)c) == 0;
+    grid.sync();
+    if (done) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
 __global__ void init_av_kernel(int n, const double* Ain, double* A, double* V) {
   const long long nn = (long long)n * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
@@ -264,14 +366,35 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_coop_kernel, CT, 0);
       max_blocks = sms * (per > 0 ? (per > 2 ? 2 : per) : 1);
     }
-    int want = ceil_div((n + 1) / 2, CT / 32);  // one warp per pair
-    int nblk = want < max_blocks ? want : max_blocks;
-    if (nblk < 1) nblk = 1;
     init_av_kernel<<<ceil_div(nn, 256) < 2048 ? ceil_div(nn, 256) : 2048, 256, 0, st>>>(n, A, Aw, Vw); ttb_count();
     int ms = max_sweeps;
     double tl = tol;
-    void* args[] = {&n, &Aw, &Vw, &cnt, &ms, &tl, &sw};
-    cudaError_t e = cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(nblk), dim3(CT), args, 0, st); ttb_count();
+    // block size: 2b columns of A (and V) must fit in ~200 KB of shared memory
+    int bsz = (int)(200 * 1024 / (16LL * n * (V ? 2 : 1)));
+    if (bsz > 8) bsz = 8;
+    cudaError_t e;
+    if (bsz >= 2) {
+      static int bmax = 0;
+      if (!bmax) {
+        cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_block_kernel, BT, 200 * 1024);
+        bmax = sms * (per > 0 ? per : 1);
+      }
+      const int nbk = (n + bsz - 1) / bsz;
+      int nblk = ((nbk + 1) / 2) < bmax ? ((nbk + 1) / 2) : bmax;
+      const size_t smem = (size_t)2 * bsz * n * (V ? 2 : 1) * sizeof(double);
+      void* args[] = {&n, &bsz, &Aw, &Vw, &cnt, &ms, &tl, &sw};
+      e = cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(nblk), dim3(BT), args, smem, st); ttb_count();
+    } else {
+      int want = ceil_div((n + 1) / 2, CT / 32);  // one warp per pair
+      int nblk = want < max_blocks ? want : max_blocks;
+      if (nblk < 1) nblk = 1;
+      void* args[] = {&n, &Aw, &Vw, &cnt, &ms, &tl, &sw};
+      e = cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(nblk), dim3(CT), args, 0, st); ttb_count();
+    }
     if (e != cudaSuccess) return (int)e;
     jacobi_finish_kernel<<<ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, Aw, Vw, sig, S, U, V); ttb_count();
     jacobi_scatter_kernel<<<ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, Aw, Vw, sig, S, U, V); ttb_count();

@@ -66,6 +66,10 @@ int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, double* S,
 /* LU with partial pivoting (in place, col-major) and solve of op(A) X = B (B col-major n x nrhs). */
 int ttb_lu_solve(void* stream, int n, double* A, long long lda, int* piv, int nrhs, double* B, long long ldb,
                  int trans, int* info);
+/* Banded LU WITHOUT pivoting (totally positive matrices, e.g. B-spline collocation at Greville
+ * points, assembly.py:409-413) and solve of A X = B for nrhs columns (in place). */
+int ttb_band_lu_solve(void* stream, int n, int kl, int ku, double* A, long long lda, int nrhs, double* B,
+                      long long ldb);
 /* Blocked Cholesky (lower, col-major) ; *info > 0 on a non-positive pivot (device int). */
 int ttb_potrf(void* stream, int n, double* A, long long lda, int* info);
 /* Solve L L^T x = b in place (n <= 25600). */

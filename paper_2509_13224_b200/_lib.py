@@ -39,6 +39,7 @@ SIGNATURES = {
     "ttb_svd_jacobi": (i32, [vp, i32, vp, i64, vp, i64, vp, vp, i64, i32, vp, vp]),
     "ttb_lu_solve": (i32, [vp, i32, vp, i64, vp, i32, vp, i64, i32, vp]),
     "ttb_potrf": (i32, [vp, i32, vp, i64, vp]),
+    "ttb_band_lu_solve": (i32, [vp, i32, i32, i32, vp, i64, i32, vp, i64]),
     "ttb_potrs": (i32, [vp, i32, vp, i64, vp]),
     "ttb_maxvol_workspace": (i64, [i32, i32]),
     "ttb_maxvol": (i32, [vp, i32, i32, vp, f64, i32, vp, vp, vp]),

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int n, int j0, double* 
   for (int k = 0; k < nb; ++k) {
     double d = L11[k * CNB + k];
     if (d <= 0.0 || !isfinite(d)) {
-      if (threadIdx.x == 0) { bad = 1; *info = j0 + k + 1; }
+      if (threadIdx.x == 0) { bad = 1; if (blockIdx.x == 0) *info = j0 + k + 1; }
       __syncthreads();
       break;
     }
@@ -125,12 +125,14 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int n, int j0, double* 
     __syncthreads();
   }
   if (bad) return;
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    int c = e / nb, i = e % nb;
-    if (i >= c) A[(long long)(j0 + c) * lda + j0 + i] = L11[c * CNB + i];
-  }
-  // rows below: x L11^T = a  (each thread one row)
-  for (int r = j0 + nb + threadIdx.x; r < n; r += blockDim.x) {
+  // every CTA factors the (tiny) diagonal block redundantly; CTA 0 writes it back
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+      int c = e / nb, i = e % nb;
+      if (i >= c) A[(long long)(j0 + c) * lda + j0 + i] = L11[c * CNB + i];
+    }
+  // rows below: x L11^T = a  (one row per thread, rows spread over the grid)
+  for (int r = j0 + nb + blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     double x[CNB];
 #pragma unroll
     for (int k = 0; k < CNB; ++k) {
@@ -390,7 +392,12 @@ TTB_API int ttb_potrf(void* stream, int n, double* A, long long lda, int* info) 
   cudaMemsetAsync(info, 0, sizeof(int), st);
   for (int j0 = 0; j0 < n; j0 += CNB) {
     const int nb = n - j0 < CNB ? n - j0 : CNB;
-    chol_panel_kernel<<<1, 256, 0, st>>>(n, j0, A, lda, info); ttb_count();
+    {
+      int g = ceil_div(n - j0 - nb, 256);
+      if (g < 1) g = 1;
+      if (g > 148) g = 148;
+      chol_panel_kernel<<<g, 256, 0, st>>>(n, j0, A, lda, info); ttb_count();
+    }
     const int m2 = n - j0 - nb;
     if (m2 > 0) {
       const double* Lp = A + (long long)j0 * lda + j0 + nb;  // col-major m2 x nb == row-major nb x m2 (ld lda)
@@ -436,4 +443,55 @@ TTB_API int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, 
   void* args[] = {&n, &r, &Q, &W, &perm, &C, &Ainv, &pv, &pi, &tol, &max_iters, &rows_out, &status};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)maxvol_kernel, dim3(nblk), dim3(MT_), args, 0, as_stream(stream)); ttb_count();
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// Banded LU without pivoting (stable for totally positive matrices such as B-spline
+// collocation at Greville points) + parallel solves of many right-hand sides.
+namespace {
+
+__global__ void band_lu_kernel(int n, int kl, int ku, double* A, long long lda) {
+  // one warp: the k-th step touches at most kl x ku entries
+  const int lane = threadIdx.x;
+  for (int k = 0; k < n; ++k) {
+    const double piv = A[(long long)k * lda + k];
+    const int i1 = min(n - 1, k + kl), j1 = min(n - 1, k + ku);
+    for (int i = k + 1 + lane; i <= i1; i += 32) A[(long long)k * lda + i] /= piv;
+    __syncwarp();
+    const int ni = i1 - k, nj = j1 - k;
+    for (int e = lane; e < ni * nj; e += 32) {
+      const int i = k + 1 + e / nj, j = k + 1 + e % nj;
+      A[(long long)j * lda + i] -= A[(long long)k * lda + i] * A[(long long)j * lda + k];
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void band_lu_apply_kernel(int n, int kl, int ku, const double* __restrict__ LU, long long lda, int nrhs,
+                                     double* B, long long ldb) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  double* b = B + (long long)c * ldb;
+  for (int k = 0; k < n; ++k) {
+    double s = b[k];
+    for (int i = max(0, k - kl); i < k; ++i) s -= LU[(long long)i * lda + k] * b[i];
+    b[k] = s;
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    double s = b[k];
+    for (int j = k + 1; j <= min(n - 1, k + ku); ++j) s -= LU[(long long)j * lda + k] * b[j];
+    b[k] = s / LU[(long long)k * lda + k];
+  }
+}
+
+}  // namespace
+
+// A (n x n col-major, band kl/ku) is factored in place without pivoting; B (n x nrhs col-major) <- A^-1 B.
+TTB_API int ttb_band_lu_solve(void* stream, int n, int kl, int ku, double* A, long long lda, int nrhs, double* B,
+                              long long ldb) {
+  if (n < 1 || kl < 0 || ku < 0) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  band_lu_kernel<<<1, 32, 0, st>>>(n, kl, ku, A, lda); ttb_count();
+  if (nrhs > 0) { band_lu_apply_kernel<<<ceil_div(nrhs, 128), 128, 0, st>>>(n, kl, ku, A, lda, nrhs, B, ldb); ttb_count(); }
+  return ttb_last_error();
 }

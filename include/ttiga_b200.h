@@ -130,6 +130,12 @@ int ttb_band_apply(void* stream, int X, int Ra, int Rb, int n, int h, int W, con
 /* Dense projected local matrix (band entries only; Bm pre-zeroed), T1[x,y,i,t,b] = sum_a phiL[x,a,y] M[a,i,t,b]. */
 int ttb_local_dense(void* stream, int r0, int n, int r1, int h, int Rb, const double* T1, const double* phiR,
                     double* Bm);
+/* Banded form of the projected local matrix in (i, x, z) ordering: LB[row*(bw+1)+d] = B[row,row-d],
+ * bw = (h+1) r0 r1 - 1 (same T1 as ttb_local_dense). */
+int ttb_local_band_build(void* stream, int r0, int n, int r1, int h, int Rb, const double* T1, const double* phiR,
+                         double* LB);
+/* In-place banded Cholesky + solve (one CTA); *info > 0 on a non-positive pivot (caller falls back to LU). */
+int ttb_band_chol_solve(void* stream, long long N, int bw, double* LB, double* b, int* info);
 /* Jacobi diagonal of the local operator, floored at 1e-14 max|d| (amen.py:380-403). part: >= 297 doubles. */
 int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
                     const double* phiR, double* d, double* part);

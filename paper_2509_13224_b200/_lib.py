@@ -54,6 +54,8 @@ SIGNATURES = {
     "ttb_band_matvec": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
     "ttb_band_apply": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32]),
     "ttb_local_dense": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
+    "ttb_local_band_build": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
+    "ttb_band_chol_solve": (i32, [vp, i64, i32, vp, vp, vp]),
     "ttb_jacobi_diag": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
     "ttb_tt_gather3": (i32, [vp, i32, vp, vp, i32, i32, vp, i32, i32, vp, i32, vp]),
     "ttb_local_matvec": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),

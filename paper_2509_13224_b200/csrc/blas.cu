@@ -297,6 +297,41 @@ __global__ void permute_kernel(PermArgs a, long long total, const double* __rest
   }
 }
 
+// out[b, c, r] = in[b, r, c] through a padded 32x32 shared-memory tile
+__global__ void transpose_tile_kernel(long long Bt, long long R, long long C, const double* __restrict__ src,
+                                      double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (long long b = blockIdx.z; b < Bt; b += gridDim.z) {
+    const double* in = src + b * R * C;
+    double* out = dst + b * R * C;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const long long r = r0 + y, c = c0 + threadIdx.x;
+      if (r < R && c < C) tile[y][threadIdx.x] = in[r * C + c];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const long long c = c0 + y, r = r0 + threadIdx.x;
+      if (r < R && c < C) out[c * R + r] = tile[threadIdx.x][y];
+    }
+    __syncthreads();
+  }
+}
+
+// out[b, c, r, s] = in[b, r, c, s] for contiguous runs of S >= 8 doubles (coalesced along s)
+__global__ void transpose_runs_kernel(long long total, long long R, long long C, long long S,
+                                      const double* __restrict__ src, double* __restrict__ dst) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long s = e % S;
+    long long t = e / S;
+    const long long r = t % R;
+    t /= R;
+    const long long c = t % C;
+    const long long b = t / C;
+    dst[e] = src[((b * R + r) * C + c) * S + s];
+  }
+}
+
 // deterministic two-level reductions ----------------------------------------
 constexpr int RED_BLOCKS = 296;
 constexpr int RED_THREADS = 256;
@@ -381,6 +416,43 @@ TTB_API int ttb_permute(void* stream, int nd, const long long* in_dims, const in
     a.in_stride_for_out[k] = stride[perm[k]];
   }
   if (total == 0) return TTB_OK;
+  // fast path: perm = [prefix | B-group | A-group | suffix] of input [prefix | A | B | suffix]
+  // -> out[b, c, r, s] = in[b, r, c, s]: coalesced run copies (S >= 8) or 32x32 smem tiles (S == 1)
+  {
+    int p0 = 0;
+    while (p0 < nd && perm[p0] == p0) ++p0;
+    int sfx = 0;
+    while (sfx < nd - p0 && perm[nd - 1 - sfx] == nd - 1 - sfx) ++sfx;
+    const int mid = nd - p0 - sfx;
+    if (mid >= 2) {
+      const int first = perm[p0];  // start of the B group in the input
+      const int la = first - p0;   // length of A
+      bool ok = la >= 1 && la < mid;
+      for (int k = 0; ok && k < mid; ++k) {
+        const int want = (k < mid - la) ? first + k : p0 + (k - (mid - la));
+        ok = perm[p0 + k] == want;
+      }
+      if (ok) {
+        long long Bt = 1, R = 1, Cc = 1, S = 1;
+        for (int k = 0; k < p0; ++k) Bt *= in_dims[k];
+        for (int k = p0; k < p0 + la; ++k) R *= in_dims[k];
+        for (int k = p0 + la; k < nd - sfx; ++k) Cc *= in_dims[k];
+        for (int k = nd - sfx; k < nd; ++k) S *= in_dims[k];
+        cudaStream_t st = as_stream(stream);
+        if (S == 1) {
+          dim3 grid(ceil_div(Cc, 32), ceil_div(R, 32), (unsigned)(Bt < 65535 ? Bt : 65535));
+          transpose_tile_kernel<<<grid, dim3(32, 8), 0, st>>>(Bt, R, Cc, src, dst); ttb_count();
+          return ttb_last_error();
+        }
+        if (S >= 8) {
+          int blocks = ceil_div(total, 256);
+          if (blocks > 148 * 16) blocks = 148 * 16;
+          transpose_runs_kernel<<<blocks, 256, 0, st>>>(total, R, Cc, S, src, dst); ttb_count();
+          return ttb_last_error();
+        }
+      }
+    }
+  }
   int blocks = ceil_div(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   permute_kernel<<<blocks, 256, 0, as_stream(stream)>>>(a, total, src, dst); ttb_count();

@@ -396,3 +396,104 @@ TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, i
   if (iters) *iters = (int)host[6];
   return ttb_last_error();
 }
+
+// ---------------------------------------------------------------------------
+// Banded direct solve of the projected AMEn system. In the (i, x, z) ordering
+// (mode index outermost) the local matrix B = phiL (x) A_k (x) phiR is banded with
+// half-bandwidth bw = (h+1) r0 r1 - 1, so its Cholesky costs N bw^2 instead of N^3.
+// The solution of the permuted system is the reference's (amen.py:386-394) up to roundoff.
+namespace {
+
+// LB[row * (bw+1) + d] = B[row, row - d] (lower band), rows/cols in (i, x, z) order
+__global__ void local_band_build_kernel(int r0, int n, int r1, int h, int Rb, int bw, const double* __restrict__ T1,
+                                        const double* __restrict__ phiR, double* __restrict__ LB) {
+  const int B = 2 * h + 1;
+  const long long N = (long long)r0 * n * r1;
+  const long long tot = N * (bw + 1);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int d = (int)(e % (bw + 1));
+    const long long row = e / (bw + 1);
+    const long long col = row - d;
+    double acc = 0.0;
+    if (col >= 0) {
+      const int z = (int)(row % r1), x = (int)((row / r1) % r0), i = (int)(row / ((long long)r1 * r0));
+      const int w = (int)(col % r1), y = (int)((col / r1) % r0), j = (int)(col / ((long long)r1 * r0));
+      const int t = j - i + h;
+      if (t >= 0 && t < B) {
+        const double* tp = T1 + ((((long long)x * r0 + y) * n + i) * B + t) * Rb;
+        const double* pp = phiR + (long long)z * Rb * r1 + w;
+        for (int b = 0; b < Rb; ++b) acc += tp[b] * pp[(long long)b * r1];
+      }
+    }
+    LB[e] = acc;
+  }
+}
+
+// in-place banded Cholesky (lower) + forward/backward solve of b; one CTA
+__global__ void __launch_bounds__(256) band_chol_solve_kernel(long long N, int bw, double* LB, double* b, int* info) {
+  __shared__ int bad;
+  const int W = bw + 1;
+  if (threadIdx.x == 0) { bad = 0; *info = 0; }
+  __syncthreads();
+  for (long long k = 0; k < N; ++k) {
+    const double dkk = LB[k * W];
+    if (!(dkk > 0.0) || !isfinite(dkk)) {
+      if (threadIdx.x == 0) { bad = 1; *info = (int)(k + 1); }
+      __syncthreads();
+      return;
+    }
+    const double lkk = sqrt(dkk);
+    const int m = (int)min((long long)bw, N - 1 - k);
+    // column k below the diagonal: L[k+q, k] = A[k+q, k] / lkk, stored at LB[(k+q)*W + q]
+    for (int q = 1 + threadIdx.x; q <= m; q += blockDim.x) LB[(k + q) * W + q] /= lkk;
+    __syncthreads();
+    if (threadIdx.x == 0) LB[k * W] = lkk;
+    // trailing update inside the band: A[k+q, k+s] -= L[k+q,k] L[k+s,k], 1 <= s <= q <= m
+    const int pairs = m * (m + 1) / 2;
+    for (int e = threadIdx.x; e < pairs; e += blockDim.x) {
+      int q = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((q + 1) * (q + 2) / 2 <= e) ++q;
+      while (q * (q + 1) / 2 > e) --q;
+      const int s = e - q * (q + 1) / 2;  // 0..q
+      const int qq = q + 1, ss = s + 1;   // 1-based offsets
+      LB[(k + qq) * W + (qq - ss)] -= LB[(k + qq) * W + qq] * LB[(k + ss) * W + ss];
+    }
+    __syncthreads();
+  }
+  // forward: L y = b (one warp)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (long long k = 0; k < N; ++k) {
+      double s = 0.0;
+      for (int q = 1 + lane; q <= bw && q <= k; q += 32) s += LB[k * W + q] * b[k - q];
+      s = warp_sum(s);
+      if (lane == 0) b[k] = (b[k] - s) / LB[k * W];
+      __syncwarp();
+    }
+    // backward: L^T x = y
+    for (long long k = N - 1; k >= 0; --k) {
+      double s = 0.0;
+      for (int q = 1 + lane; q <= bw && k + q < N; q += 32) s += LB[(k + q) * W + q] * b[k + q];
+      s = warp_sum(s);
+      if (lane == 0) b[k] = (b[k] - s) / LB[k * W];
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace
+
+TTB_API int ttb_local_band_build(void* stream, int r0, int n, int r1, int h, int Rb, const double* T1,
+                                 const double* phiR, double* LB) {
+  const int bw = (h + 1) * r0 * r1 - 1;
+  const long long tot = (long long)r0 * n * r1 * (bw + 1);
+  if (tot == 0) return TTB_OK;
+  local_band_build_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r0, n, r1, h, Rb, bw, T1, phiR, LB); ttb_count();
+  return ttb_last_error();
+}
+
+TTB_API int ttb_band_chol_solve(void* stream, long long N, int bw, double* LB, double* b, int* info) {
+  if (N < 1 || bw < 0) return TTB_EARG;
+  band_chol_solve_kernel<<<1, 256, 0, as_stream(stream)>>>(N, bw, LB, b, info); ttb_count();
+  return ttb_last_error();
+}

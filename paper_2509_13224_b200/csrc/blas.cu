@@ -251,6 +251,42 @@ __global__ void scale_kernel(long long n, double beta, double* C, long long ldc,
   }
 }
 
+// C[r, c] = alpha * sum_k A[r, k] B[k, c] + beta * C[r, c] for small K: each CTA owns 256 columns,
+// keeps B[:, tile] in shared memory and streams the rows of C once (coalesced read-modify-write).
+__global__ void __launch_bounds__(128) lowrank_update_kernel(int M, int N, int K, double alpha,
+                                                             const double* __restrict__ A, long long lda,
+                                                             const double* __restrict__ B, long long ldb,
+                                                             double beta, double* C, long long ldc) {
+  __shared__ double Bs[32][128];
+  __shared__ double As[32][33];
+  const int c0 = blockIdx.x * 128;
+  const int c = c0 + threadIdx.x;
+  for (int k = 0; k < K; ++k) Bs[k][threadIdx.x] = (c < N) ? B[(long long)k * ldb + c] : 0.0;
+  for (int r0 = 0; r0 < M; r0 += 32) {
+    const int rn = min(32, M - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < rn * K; e += 128) As[e / K][e % K] = A[(long long)(r0 + e / K) * lda + (e % K)];
+    __syncthreads();
+    if (c < N) {
+      // 8 rows at a time: issue the 8 independent loads of C first (memory-level parallelism)
+      for (int rr0 = 0; rr0 < rn; rr0 += 8) {
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          cv[u] = (beta != 0.0 && rr0 + u < rn) ? C[(long long)(r0 + rr0 + u) * ldc + c] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (rr0 + u < rn) {
+            double acc = 0.0;
+            for (int k = 0; k < K; ++k) acc += As[rr0 + u][k] * Bs[k][threadIdx.x];
+            C[(long long)(r0 + rr0 + u) * ldc + c] = alpha * acc + beta * cv[u];
+          }
+        }
+      }
+    }
+  }
+}
+
 __global__ void splitk_reduce(int M, int N, int S, const double* __restrict__ part, double alpha, double beta,
                               double* C, long long ldc) {
   long long tot = (long long)M * N;
@@ -365,6 +401,12 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
     long long n = (long long)M * N;
     dim3 grid(ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), batch);
     scale_kernel<<<grid, 256, 0, st>>>(n, beta, C, ldc, M, N, sC); ttb_count();
+    return ttb_last_error();
+  }
+  if (!tA && !tB && batch == 1 && K <= 32 && N >= 2048) {
+    // low-rank update of a long matrix (WY panel updates): memory-bound, one coalesced RMW pass
+    dim3 grid(ceil_div(N, 128));
+    lowrank_update_kernel<<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc); ttb_count();
     return ttb_last_error();
   }
   GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};

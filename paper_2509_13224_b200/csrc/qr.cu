@@ -20,7 +20,7 @@ constexpr int kMaxPanelBlocks = 1024;  // sizing of the per-CTA partial buffers
 // Factor the m x jb panel P (col-major, ld) in place. Writes tau[0..jb), the explicit
 // reflectors V (m x jb col-major, ld m: unit diagonal, zeros above) and the WY factor T
 // (jb x jb row-major, upper triangular). part: gridDim.x * (NB*NB + NB) doubles.
-__global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, long long ld, double* tau, double* V,
+__global__ void __launch_bounds__(PT, 2) panel_qr_kernel(int m, int jb, double* P, long long ld, double* tau, double* V,
                                                       double* T, double* part) {
   // One pass over the panel and ONE grid-wide barrier per column. While column j's reflector
   // is applied to a row, the row's updated entries are already folded into the next column's
@@ -34,7 +34,6 @@ __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, 
   __shared__ double sw[NB];
   __shared__ double srow[NB];
   __shared__ double sbeta[NB];
-  __shared__ double sG[NB * NB];
   const int nblk = gridDim.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int chunk = (m + nblk - 1) / nblk;
@@ -77,10 +76,13 @@ __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, 
   }
   for (int j = 0; j < jb; ++j) {
     const int buf = j & 1;
-    if (threadIdx.x < ZW) {
+    // every CTA re-sums the per-CTA partials (same order everywhere -> identical results):
+    // one warp per statistic, lanes stride over the CTAs, then a shuffle reduction
+    for (int t = wid; t < ZW; t += PT / 32) {
       double v = 0.0;
-      for (int b = 0; b < nblk; ++b) v += zpart[((long long)buf * nblk + b) * ZW + threadIdx.x];
-      sz[threadIdx.x] = v;
+      for (int b = lane; b < nblk; b += 32) v += zpart[((long long)buf * nblk + b) * ZW + t];
+      v = warp_sum(v);
+      if (lane == 0) sz[t] = v;
     }
     // deferred write of pivot row j-1 (nobody reads it during column j)
     if (j >= 1 && (j - 1) >= r0 && (j - 1) < r1)
@@ -145,47 +147,11 @@ __global__ void __launch_bounds__(PT) panel_qr_kernel(int m, int jb, double* P, 
   for (int j = threadIdx.x; j < jb; j += PT)
     if (j >= r0 && j < r1) P[(long long)j * ld + j] = sbeta[j];
   grid.sync();
-  // explicit V and the Gram G = V^T V partials
+  // explicit V (unit diagonal, zeros above); its Gram and the WY factor T follow on the host side
   for (int i = r0 + threadIdx.x; i < r1; i += PT) {
     for (int c = 0; c < jb; ++c) {
       double v = (i < c) ? 0.0 : (i == c ? 1.0 : P[(long long)c * ld + i]);
       V[(long long)c * m + i] = v;
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < NB * NB; e += PT) sG[e] = 0.0;
-  __syncthreads();
-  // Gram partial: each warp takes pairs (a,b) with a<b
-  for (int pr = wid; pr < jb * jb; pr += PT / 32) {
-    int a = pr / jb, b = pr % jb;
-    if (a >= b) continue;
-    double v = 0.0;
-    for (int i = max(r0, b) + lane; i < r1; i += 32) v += V[(long long)a * m + i] * V[(long long)b * m + i];
-    v = warp_sum(v);
-    if (lane == 0) sG[a * NB + b] = v;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < NB * NB; e += PT) part[(long long)blockIdx.x * NB * NB + e] = sG[e];
-  grid.sync();
-  if (blockIdx.x == 0) {
-    for (int e = threadIdx.x; e < NB * NB; e += PT) {
-      double v = 0.0;
-      for (int b = 0; b < nblk; ++b) v += part[(long long)b * NB * NB + e];
-      sG[e] = v;
-    }
-    __syncthreads();
-    // dlarft (forward, columnwise): T[i,i] = tau_i; T[0:i, i] = -tau_i T[0:i,0:i] G[0:i, i]
-    if (threadIdx.x == 0) {
-      for (int e = 0; e < jb * jb; ++e) T[e] = 0.0;
-      for (int i = 0; i < jb; ++i) {
-        const double ti = tau[i];
-        T[i * jb + i] = ti;
-        for (int r = 0; r < i; ++r) {
-          double v = 0.0;
-          for (int c = r; c < i; ++c) v += T[r * jb + c] * sG[c * NB + i];
-          T[r * jb + i] = -ti * v;
-        }
-      }
     }
   }
 }
@@ -259,6 +225,54 @@ __global__ void larft_kernel(int nb, const double* G, int ldg, const double* tau
   }
 }
 
+// G (nb x nb row-major, nb <= NB) = V^T V for a tall col-major V (m x nb, ld m): every CTA
+// stages 128-row tiles in shared memory, one thread per (a, b) pair accumulates; per-CTA
+// partials are summed by a second kernel in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) gram_partial_kernel(int m, int nb, const double* __restrict__ V,
+                                                           double* __restrict__ part) {
+  __shared__ double tile[NB][129];
+  const int pairs = nb * nb;
+  double acc = 0.0;
+  const int a = threadIdx.x / nb, b = threadIdx.x % nb;
+  for (int r0 = blockIdx.x * 128; r0 < m; r0 += gridDim.x * 128) {
+    const int rn = min(128, m - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * 128; e += 256) {
+      const int c = e / 128, i = e % 128;
+      tile[c][i] = i < rn ? V[(long long)c * m + r0 + i] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < pairs && a <= b)
+      for (int i = 0; i < 128; ++i) acc += tile[a][i] * tile[b][i];
+  }
+  if (threadIdx.x < pairs) part[(long long)blockIdx.x * pairs + threadIdx.x] = (a <= b) ? acc : 0.0;
+}
+
+__global__ void gram_final_kernel(int nb, int nblk, const double* __restrict__ part, double* G) {
+  const int pairs = nb * nb;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = wid; e < pairs; e += blockDim.x / 32) {
+    double v = 0.0;
+    for (int b = lane; b < nblk; b += 32) v += part[(long long)b * pairs + e];
+    v = warp_sum(v);
+    if (lane == 0) G[e] = v;
+  }
+  __syncthreads();
+  // mirror the upper triangle (a <= b) into the lower one
+  for (int e = threadIdx.x; e < pairs; e += blockDim.x) {
+    const int a = e / nb, b = e % nb;
+    if (a > b) G[e] = G[b * nb + a];
+  }
+}
+
+int launch_gram(int m, int nb, const double* V, double* G, double* part, cudaStream_t st) {
+  int blocks = ceil_div(m, 128);
+  if (blocks > 592) blocks = 592;
+  gram_partial_kernel<<<blocks, 256, 0, st>>>(m, nb, V, part); ttb_count();
+  gram_final_kernel<<<1, 256, 0, st>>>(nb, blocks, part, G); ttb_count();
+  return ttb_last_error();
+}
+
 struct QrWs {
   double *part, *Vp, *Vb, *W, *W2, *G, *Tin, *Tout;
 };
@@ -326,6 +340,10 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
       double* T = w.Tin + (long long)(j0 / NB) * NB * NB;
       int rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, st);
       if (rc) return rc;
+      // T from the Gram V^T V (one streaming pass over V) -- dlarft
+      rc = launch_gram(mp, jb, w.Vp, w.G, w.part, st);
+      if (rc) return rc;
+      larft_kernel<<<1, 128, 0, st>>>(jb, w.G, jb, tau + j0, T); ttb_count();
       // inside the outer block, or -- when the block is a single panel -- the whole trailing matrix
       const int n2 = (JB <= NB) ? (n - j0 - jb) : (J0 + JB - j0 - jb);
       if (n2 > 0) {

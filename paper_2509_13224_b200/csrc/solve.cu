@@ -205,6 +205,22 @@ __global__ void __launch_bounds__(ST) chol_solve_kernel(int n, const double* __r
 constexpr int MT_ = 256;
 constexpr int RMAX = 128;
 
+// every CTA merges the per-CTA (value, index) partials: warp 0, lanes stride over CTAs
+__device__ __forceinline__ AbsMax grid_absmax(const double* pv, const long long* pi, int nblk, double* sv,
+                                              long long* si) {
+  __shared__ AbsMax res;
+  if (threadIdx.x < 32) {
+    AbsMax g{-1.0, (long long)1 << 62};
+    for (int b = threadIdx.x; b < nblk; b += 32) g = absmax_merge(g, AbsMax{pv[b], pi[b]});
+    g = warp_absmax(g);
+    if (threadIdx.x == 0) res = g;
+  }
+  __syncthreads();
+  AbsMax r = res;
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double* __restrict__ Q, double* W, int* perm,
                                                       double* C, double* Ainv, double* pv, long long* pi, double tol,
                                                       int max_iters, int* rows_out, int* status) {
@@ -240,8 +256,7 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
     best = block_absmax(best, sv, si);
     if (threadIdx.x == 0) { pv[blockIdx.x] = best.v; pi[blockIdx.x] = best.i; }
     grid.sync();
-    AbsMax g{-1.0, (long long)1 << 62};
-    for (int b = 0; b < nblk; ++b) g = absmax_merge(g, AbsMax{pv[b], pi[b]});
+    AbsMax g = grid_absmax(pv, pi, nblk, sv, si);
     if (g.v <= 1e-14 * fmax(scale, 1e-300)) {
       if (blockIdx.x == 0 && threadIdx.x == 0) *status = 1;
       return;  // uniform across the grid
@@ -333,8 +348,7 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
     best = block_absmax(best, sv, si);
     if (threadIdx.x == 0) { pv[blockIdx.x] = best.v; pi[blockIdx.x] = best.i; }
     grid.sync();
-    AbsMax g{-1.0, (long long)1 << 62};
-    for (int b = 0; b < nblk; ++b) g = absmax_merge(g, AbsMax{pv[b], pi[b]});
+    AbsMax g = grid_absmax(pv, pi, nblk, sv, si);
     if (g.v <= tol) break;
     const int bi = (int)(g.i / r), bj = (int)(g.i % r);
     for (int c = threadIdx.x; c < r; c += MT_) srow[c] = C[(long long)c * n + bi] - (c == bj ? 1.0 : 0.0);

@@ -438,6 +438,9 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
       return ttb_last_error();
     }
   }
+  // short-K updates of a long C (WY trailing updates): 128x64 tiles, ~120 registers -> 2 CTAs/SM so
+  // one CTA's epilogue read-modify-write overlaps the other's main loop
+  if (big && K <= 256 && N >= 4096) return launch_gemm<128, 64, 4, 2>(g, batch, st);
   if (big) return launch_gemm<128, 128, 2, 4>(g, batch, st);
   if (narrow) return launch_gemm<128, 32, 4, 1>(g, batch, st);
   return launch_gemm<64, 64, 2, 2>(g, batch, st);

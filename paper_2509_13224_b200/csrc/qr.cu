@@ -196,6 +196,96 @@ int panel_grid(int m) {
   return want < max_blocks ? want : max_blocks;
 }
 
+// Panel small enough for one CTA's shared memory (m * jb <= kSmallPanel): no grid barriers,
+// factorization + explicit V + Gram + T in one launch (latency-bound medium-sized QRs).
+constexpr int kSmallPanel = 20480;
+constexpr int SPT = 512;
+
+__global__ void __launch_bounds__(SPT) panel_small_kernel(int m, int jb, double* P, long long ld, double* tau,
+                                                           double* V, double* T) {
+  extern __shared__ double S[];  // m x jb col-major, ld m
+  __shared__ double red[32];
+  __shared__ double w[NB], taus[NB], betas[NB], G[NB * NB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = SPT / 32;
+  for (int e = threadIdx.x; e < m * jb; e += SPT) S[e] = P[(long long)(e / m) * ld + (e % m)];
+  __syncthreads();
+  for (int j = 0; j < jb; ++j) {
+    double* col = S + (long long)j * m;
+    double s = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < m; i += SPT) s += col[i] * col[i];
+    s = block_sum(s, red);
+    const double alpha = col[j];
+    double beta, t, scal;
+    if (s == 0.0) { beta = alpha; t = 0.0; scal = 0.0; }
+    else {
+      const double nrm = sqrt(alpha * alpha + s);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = j + 1 + threadIdx.x; i < m; i += SPT) col[i] *= scal;
+    __syncthreads();
+    for (int c = j + 1 + wid; c < jb; c += nw) {
+      const double* sc = S + (long long)c * m;
+      double acc = 0.0;
+      for (int i = j + lane; i < m; i += 32) acc += (i == j ? 1.0 : col[i]) * sc[i];
+      acc = warp_sum(acc);
+      if (lane == 0) w[c] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < (jb - j - 1) * (m - j); e += SPT) {
+      const int c = j + 1 + e / (m - j), i = j + e % (m - j);
+      S[(long long)c * m + i] -= t * (i == j ? 1.0 : col[i]) * w[c];
+    }
+    if (threadIdx.x == 0) { taus[j] = t; betas[j] = beta; }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * jb; e += SPT) {
+    const int c = e / m, i = e % m;
+    P[(long long)c * ld + i] = (i == c) ? betas[c] : S[e];
+    V[e] = (i < c) ? 0.0 : (i == c ? 1.0 : S[e]);
+  }
+  if (threadIdx.x < jb) tau[threadIdx.x] = taus[threadIdx.x];
+  // Gram of the unit-lower V (one warp per pair a < b), then dlarft
+  for (int pr = wid; pr < jb * jb; pr += nw) {
+    const int a = pr / jb, b = pr % jb;
+    if (a >= b) continue;
+    double acc = 0.0;
+    for (int i = b + lane; i < m; i += 32) {
+      const double va = (i == a) ? 1.0 : S[(long long)a * m + i];
+      const double vb = (i == b) ? 1.0 : S[(long long)b * m + i];
+      acc += va * vb;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) G[a * NB + b] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int e = 0; e < jb * jb; ++e) T[e] = 0.0;
+    for (int i = 0; i < jb; ++i) {
+      const double ti = taus[i];
+      T[i * jb + i] = ti;
+      for (int r = 0; r < i; ++r) {
+        double v = 0.0;
+        for (int c = r; c < i; ++c) v += T[r * jb + c] * G[c * NB + i];
+        T[r * jb + i] = -ti * v;
+      }
+    }
+  }
+}
+
+bool panel_is_small(int m, int jb) { return (long long)m * jb <= kSmallPanel; }
+
+int launch_panel_small(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, cudaStream_t st) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(panel_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallPanel * 8);
+    cfg = true;
+  }
+  panel_small_kernel<<<1, SPT, (size_t)m * jb * sizeof(double), st>>>(m, jb, P, ld, tau, V, T); ttb_count();
+  return ttb_last_error();
+}
+
 int launch_panel(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, double* part, cudaStream_t st) {
   int nblk = panel_grid(m);
   void* args[] = {&m, &jb, &P, &ld, &tau, &V, &T, &part};
@@ -338,12 +428,18 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
       const int mp = m - j0;
       double* P = A + (long long)j0 * lda + j0;
       double* T = w.Tin + (long long)(j0 / NB) * NB * NB;
-      int rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, st);
-      if (rc) return rc;
-      // T from the Gram V^T V (one streaming pass over V) -- dlarft
-      rc = launch_gram(mp, jb, w.Vp, w.G, w.part, st);
-      if (rc) return rc;
-      larft_kernel<<<1, 128, 0, st>>>(jb, w.G, jb, tau + j0, T); ttb_count();
+      int rc;
+      if (panel_is_small(mp, jb)) {
+        rc = launch_panel_small(mp, jb, P, lda, tau + j0, w.Vp, T, st);
+        if (rc) return rc;
+      } else {
+        rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, st);
+        if (rc) return rc;
+        // T from the Gram V^T V (one streaming pass over V) -- dlarft
+        rc = launch_gram(mp, jb, w.Vp, w.G, w.part, st);
+        if (rc) return rc;
+        larft_kernel<<<1, 128, 0, st>>>(jb, w.G, jb, tau + j0, T); ttb_count();
+      }
       // inside the outer block, or -- when the block is a single panel -- the whole trailing matrix
       const int n2 = (JB <= NB) ? (n - j0 - jb) : (J0 + JB - j0 - jb);
       if (n2 > 0) {

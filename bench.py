@@ -131,7 +131,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "parallelism": "replicas", "l2": "inputs > L2"},
+        "config": {"workload": WORKLOAD, "mode_size": N_MODE, "op_ranks": R_OP, "vec_ranks": R_VEC, "round_eps": EPS,
+                   "sample_mode_size": CPU_SAMPLE_N, "parallelism": "replicas x1 (rank 0 only)",
+                   "l2": "inputs > L2"},
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": ncores, "kind": "port",
                          "sample": f"oracle (numpy/LAPACK restatement of the reference tt_matvec + tt_round) on the "
                                    f"same workload at mode size {CPU_SAMPLE_N} (ranks 16/64 kept), one matvec+round "

@@ -204,9 +204,10 @@ class Face:
 
 @dataclass(frozen=True)
 class Bc:
-    """Reference BoundarySpec (assembly.py:334-371)."""
+    """Reference BoundarySpec (assembly.py:334-371); allow_adjacent: EXTENSION switch."""
 
     faces: dict = field(default_factory=dict)
+    allow_adjacent: bool = False
 
     def __post_init__(self):
         for k, v in self.faces.items():
@@ -279,6 +280,8 @@ def lift_tt(patch, disc: Disc, bc: Bc):
     sizes = disc.sizes
     nz = [f for f in bc.dirichlet() if not bc.at(*f).zero()]
     adjacent = any(fa[0] != fb[0] for i, fa in enumerate(nz) for fb in nz[i + 1:])
+    if adjacent and not bc.allow_adjacent:
+        raise IgaFault("nonzero Dirichlet data on adjacent faces is not supported")
     lift = T.TT.zeros(sizes)
     for a, s in nz:
         c = face_coeffs(patch, disc, bc, a, s)
@@ -424,7 +427,8 @@ class Config:
         if self.bc is None:
             if self.bc_from_analytic:
                 fn = ANALYTIC[self.analytic](self, patch)
-                self.bc = Bc({(int(a), int(s)): Face("dirichlet", fn) for a, s in patch.meta["default_dirichlet"]})
+                self.bc = Bc({(int(a), int(s)): Face("dirichlet", fn) for a, s in patch.meta["default_dirichlet"]},
+                             allow_adjacent=True)
             else:
                 self.bc = Bc({(int(a), int(s)): Face("dirichlet", 0.0) for a, s in patch.meta["default_dirichlet"]})
         return self

@@ -128,7 +128,8 @@ class SolveConfig:
                     raise DriverError("bc_from_analytic needs an analytic solution")
                 fn = ANALYTIC[self.analytic](self, patch)[2]
                 self.bc = BoundarySpec({(int(a), int(s)): FaceCondition("dirichlet", fn)
-                                        for a, s in patch.metadata.get("default_dirichlet", [])})
+                                        for a, s in patch.metadata.get("default_dirichlet", [])},
+                                       allow_adjacent_nonzero=True)
             else:
                 self.bc = BoundarySpec({(int(a), int(s)): FaceCondition("dirichlet", 0.0)
                                         for a, s in patch.metadata.get("default_dirichlet", [])})

@@ -58,7 +58,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
 // conflict-free (pitches chosen so a warp's 32 x 8 B fragment read is exactly two wavefronts):
 //   A !tA : As[m][k] pitch BK+4     A tA : As[k][m] pitch BM+8
 //   B !tB : Bs[k][n] pitch BN+8     B tB : Bs[n][k] pitch BK+4
-template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC, int STAGES>
+template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC, int STAGES, int CI>
 __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
   constexpr int T = WM * WN * 32;
   constexpr int ASZ = TA ? BK * (BM + 8) : BM * (BK + 4);
@@ -152,6 +152,21 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
     if (s < nk) load(s, s);
     cp_async_commit();
   }
+  if (CI) {
+    // short-K read-modify-write updates: fetch C while the first operand stages are in flight
+    const double f = g.beta * g.alpha;  // == beta / alpha for alpha = +-1
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int m = bm0 + wm * (BM / WM) + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = bn0 + wn * (BN / WN) + j * 8 + (lane & 3) * 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (m < M && n + h < N) acc[i][j][h] = f * __ldg(C + (long long)m * g.ldc + n + h);
+      }
+    }
+  }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -196,7 +211,7 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
         if (n + h < N) {
           double* c = C + (long long)m * g.ldc + n + h;
           double v = g.alpha * acc[i][j][h];
-          if (!g.split && g.beta != 0.0) v += g.beta * *c;
+          if (!g.split && !CI && g.beta != 0.0) v += g.beta * *c;
           *c = v;
         }
       }
@@ -204,7 +219,7 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
   }
 }
 
-template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC>
+template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC, int CI>
 int launch_gemm_t(const GemmArgs& g, int batch, cudaStream_t st) {
   constexpr int STAGES = 3;
   constexpr int T = WM * WN * 32;
@@ -213,16 +228,16 @@ int launch_gemm_t(const GemmArgs& g, int batch, cudaStream_t st) {
   const size_t smem = (size_t)STAGES * (ASZ + BSZ) * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES>,
+    cudaFuncSetAttribute(dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES, CI>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), batch);
-  dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES><<<grid, T, smem, st>>>(g); ttb_count();
+  dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES, CI><<<grid, T, smem, st>>>(g); ttb_count();
   return ttb_last_error();
 }
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int CI = 0>
 int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
   // 16-byte copies when both operands' rows (and batch strides) keep 16 B alignment
   const bool vec = ((g.lda & 1) == 0) && ((g.ldb & 1) == 0) && ((((uintptr_t)g.A) & 15) == 0) &&
@@ -230,14 +245,14 @@ int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
                    (!g.split || (g.Kc & 1) == 0);
   const int key = (g.tA ? 1 : 0) | (g.tB ? 2 : 0) | (vec ? 4 : 0);
   switch (key) {
-    case 0: return launch_gemm_t<BM, BN, WM, WN, 0, 0, 1>(g, batch, st);
-    case 1: return launch_gemm_t<BM, BN, WM, WN, 1, 0, 1>(g, batch, st);
-    case 2: return launch_gemm_t<BM, BN, WM, WN, 0, 1, 1>(g, batch, st);
-    case 3: return launch_gemm_t<BM, BN, WM, WN, 1, 1, 1>(g, batch, st);
-    case 4: return launch_gemm_t<BM, BN, WM, WN, 0, 0, 2>(g, batch, st);
-    case 5: return launch_gemm_t<BM, BN, WM, WN, 1, 0, 2>(g, batch, st);
-    case 6: return launch_gemm_t<BM, BN, WM, WN, 0, 1, 2>(g, batch, st);
-    default: return launch_gemm_t<BM, BN, WM, WN, 1, 1, 2>(g, batch, st);
+    case 0: return launch_gemm_t<BM, BN, WM, WN, 0, 0, 1, CI>(g, batch, st);
+    case 1: return launch_gemm_t<BM, BN, WM, WN, 1, 0, 1, CI>(g, batch, st);
+    case 2: return launch_gemm_t<BM, BN, WM, WN, 0, 1, 1, CI>(g, batch, st);
+    case 3: return launch_gemm_t<BM, BN, WM, WN, 1, 1, 1, CI>(g, batch, st);
+    case 4: return launch_gemm_t<BM, BN, WM, WN, 0, 0, 2, CI>(g, batch, st);
+    case 5: return launch_gemm_t<BM, BN, WM, WN, 1, 0, 2, CI>(g, batch, st);
+    case 6: return launch_gemm_t<BM, BN, WM, WN, 0, 1, 2, CI>(g, batch, st);
+    default: return launch_gemm_t<BM, BN, WM, WN, 1, 1, 2, CI>(g, batch, st);
   }
 }
 
@@ -410,6 +425,8 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
     return ttb_last_error();
   }
   GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};
+  // alpha = +-1, beta != 0: the short-K path starts its accumulators at (beta/alpha) C (CI kernels)
+  const bool cinit = beta != 0.0 && (alpha == 1.0 || alpha == -1.0);
   long long work = (long long)M * N * batch;
   const bool big = (work >= (long long)148 * 128 * 128 * 2 || K >= 8192) && M >= 128 && N >= 128;
   const bool narrow = !big && N <= 32 && M >= 48;  // thin outputs (WY products over panel widths)
@@ -417,8 +434,9 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
                         : narrow ? (long long)ceil_div(M, 128) * ceil_div(N, 32) * batch
                                  : (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch;
   if (batch == 1 && tiles < 148 && K >= 1024) {
-    // split-K: enough K chunks to cover ~2 waves, each chunk >= 256 deep, deterministic reduction
-    long long S = (296 + tiles - 1) / tiles;
+    // split-K: chunks filling (not exceeding) two waves of 148 SMs, each chunk >= 256 deep,
+    // deterministic reduction
+    long long S = 296 / tiles;
     long long maxS = K / 256;
     if (S > maxS) S = maxS;
     if (S > 1) {
@@ -440,7 +458,8 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
   }
   // short-K updates of a long C (WY trailing updates): 128x64 tiles, ~120 registers -> 2 CTAs/SM so
   // one CTA's epilogue read-modify-write overlaps the other's main loop
-  if (big && K <= 256 && N >= 4096) return launch_gemm<128, 64, 4, 2>(g, batch, st);
+  if (big && K <= 256 && N >= 4096)
+    return cinit ? launch_gemm<128, 64, 4, 2, 1>(g, batch, st) : launch_gemm<128, 64, 4, 2>(g, batch, st);
   if (big) return launch_gemm<128, 128, 2, 4>(g, batch, st);
   if (narrow) return launch_gemm<128, 32, 4, 1>(g, batch, st);
   return launch_gemm<64, 64, 2, 2>(g, batch, st);

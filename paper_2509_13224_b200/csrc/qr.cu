@@ -6,10 +6,16 @@
 // the trailing matrix is updated with the compact-WY form
 // A2 -= V (T^T (V^T A2)) through three DMMA GEMMs, which carry the flops.
 #include "common.cuh"
+#include <stdlib.h>
 
 TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                       long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
                       long long ldc, long long sC, int batch);
+// tsqr.cu
+long long tsqr_workspace(long long m);
+bool tsqr_applies(long long m, int jb);
+int tsqr_panel(long long m, int jb, double* P, long long ld, double* tau, double* V, double* Tout, double* ws,
+               cudaStream_t st);
 
 namespace {
 
@@ -364,7 +370,7 @@ int launch_gram(int m, int nb, const double* V, double* G, double* part, cudaStr
 }
 
 struct QrWs {
-  double *part, *Vp, *Vb, *W, *W2, *G, *Tin, *Tout;
+  double *part, *Vp, *Vb, *W, *W2, *G, *Tin, *Tout, *ts;
 };
 
 QrWs carve(double* ws, int m, int n) {
@@ -379,7 +385,18 @@ QrWs carve(double* ws, int m, int n) {
   w.G = w.W2 + wn * NB2;
   w.Tin = w.G + (long long)NB2 * NB2;
   w.Tout = w.Tin + (long long)((k + NB - 1) / NB) * NB * NB;
+  w.ts = w.Tout + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
   return w;
+}
+
+// TTB_PANEL=coop selects the cooperative column-by-column panel for tall panels (A/B testing)
+bool coop_panels() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TTB_PANEL");
+    v = (e && e[0] == 'c') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 int grid_v(long long tot) {
@@ -408,6 +425,7 @@ TTB_API long long ttb_qr_workspace(int m, int n) {
   long long s = (long long)kMaxPanelBlocks * (NB * NB + NB + 2);
   s += (long long)m * NB + (long long)m * NB2 + 2 * wn * NB2 + (long long)NB2 * NB2;
   s += (long long)((k + NB - 1) / NB) * NB * NB + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
+  s += tsqr_workspace(m);
   return s + 64;
 }
 
@@ -431,6 +449,9 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
       int rc;
       if (panel_is_small(mp, jb)) {
         rc = launch_panel_small(mp, jb, P, lda, tau + j0, w.Vp, T, st);
+        if (rc) return rc;
+      } else if (tsqr_applies(mp, jb) && !coop_panels()) {
+        rc = tsqr_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.ts, st);
         if (rc) return rc;
       } else {
         rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, st);

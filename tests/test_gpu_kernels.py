@@ -44,7 +44,7 @@ def test_permute_and_tdot(la):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 3), (3, 5), (64, 64), (200, 37), (1000, 70), (40, 300), (5000, 33),
-                                 (20000, 100)])
+                                 (20000, 100), (1100, 16), (1500, 17), (200000, 40), (131073, 150)])
 def test_qr(la, m, n):
     rng = np.random.default_rng(m + n)
     X = rng.standard_normal((m, n))
@@ -68,6 +68,16 @@ def test_qr_rank_deficient(la):
     Z = np.zeros((20, 4))
     Q, R = la.qr(T(Z))
     assert np.all(R.cpu().numpy() == 0)
+    # tall panels (TSQR path): repeated columns, zero columns, an all-zero matrix
+    B = rng.standard_normal((60000, 7))
+    X = np.hstack([B, B, np.zeros((60000, 3)), B[:, :2] * 1e-9, B])
+    Q, R = la.qr(T(X))
+    Q, R = Q.cpu().numpy(), R.cpu().numpy()
+    assert np.abs(Q @ R - X).max() < 1e-12 * np.abs(X).max() * 10
+    assert np.abs(Q.T @ Q - np.eye(X.shape[1])).max() < 1e-12
+    Q, R = la.qr(T(np.zeros((30000, 20))))
+    assert np.all(R.cpu().numpy() == 0)
+    assert np.abs(Q.cpu().numpy().T @ Q.cpu().numpy() - np.eye(20)).max() < 1e-14
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (6, 4), (4, 6), (64, 64), (100, 65), (65, 100), (2000, 120), (300, 300)])

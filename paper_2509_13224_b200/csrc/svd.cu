@@ -6,6 +6,7 @@
 // entries. n <= 64 runs entirely in shared memory; larger n keeps A and V in
 // global memory (L2 resident) with the same schedule.
 #include "common.cuh"
+#include <stdlib.h>
 
 namespace {
 
@@ -284,6 +285,232 @@ __global__ void __launch_bounds__(BT) jacobi_block_kernel(int n, int b, double* 
   if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
+// Gram block one-sided Jacobi (n >= 128, one matrix). The n columns form blocks of GB/2; each
+// round (tournament order over blocks, one grid-wide barrier) every CTA owns one pair of blocks
+// = GB columns, staged in shared memory, and orthogonalizes them completely:
+//   repeat { G = A_loc^T A_loc (DMMA, fresh from the columns);
+//            stop if every pair passes |g_pq| <= tol sqrt(g_pp g_qq)  (the scalar test);
+//            eigen-decompose G by a cyclic two-sided Jacobi in one warp (rotations J);
+//            A_loc <- A_loc J (DMMA) }
+// The pass/fail test always uses a Gram recomputed from the columns, so the stopping rule
+// and the attainable orthogonality are those of the scalar one-sided method (relative
+// accuracy); only the rotation angles come from the 8 x 8 eigen-solve. A sweep in which no
+// CTA rotates ends the iteration.
+constexpr int GB = 8;       // columns per CTA (two blocks of 4)
+constexpr int GT = 256;     // threads per CTA
+constexpr int GW = GT / 32;
+constexpr int kLocalIters = 1;   // Gram -> rotate -> apply rounds per block pair and visit
+constexpr int kEigenSweeps = 1;  // cyclic sweeps of the 8 x 8 eigen-solve per local round
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, double* V, int* cnt, int max_sweeps,
+                                                          double tol, int* sweeps_out, int local_iters,
+                                                          int eigen_sweeps) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  __shared__ double Gp[GW][GB * GB];
+  __shared__ double G[GB * GB];
+  __shared__ double J[GB * GB];
+  __shared__ double rc[GB / 2], rs[GB / 2];
+  __shared__ int cols[GB];
+  __shared__ int ncols, need, rotated;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int hb = GB / 2;
+  const int nb = (n + hb - 1) / hb;
+  const int NBL = (nb + 1) & ~1;
+  const int NR = (n + 31) & ~31;      // padded rows (zeros)
+  const int LD = NR + 4;
+  double* As = sm;
+  double* Vs = sm + (long long)GB * LD;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { cnt[0] = 0; cnt[1] = 0; }
+  for (int e = threadIdx.x; e < GB * LD; e += GT) { As[e] = 0.0; if (V) Vs[e] = 0.0; }
+  grid.sync();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int* c = cnt + (sweep & 1);
+    for (int r = 0; r < NBL - 1; ++r) {
+      for (int pr = blockIdx.x; pr < NBL / 2; pr += gridDim.x) {
+        int bp = rr_index(pr, r, NBL), bq = rr_index(NBL - 1 - pr, r, NBL);
+        if (bp > bq) { int t = bp; bp = bq; bq = t; }
+        if (bq >= nb) continue;  // dummy block (uniform per CTA)
+        if (threadIdx.x == 0) {
+          int L = 0;
+          for (int j = bp * hb; j < min(n, bp * hb + hb); ++j) cols[L++] = j;
+          for (int j = bq * hb; j < min(n, bq * hb + hb); ++j) cols[L++] = j;
+          ncols = L;
+          rotated = 0;
+        }
+        __syncthreads();
+        const int L = ncols;
+        for (int i0 = 0; i0 < n; i0 += 4 * GT) {  // 4 x GB independent loads in flight per thread
+          double buf[GB][4];
+#pragma unroll
+          for (int lc = 0; lc < GB; ++lc)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * GT + threadIdx.x;
+              buf[lc][u] = (lc < L && i < n) ? A[(long long)cols[lc] * n + i] : 0.0;
+            }
+#pragma unroll
+          for (int lc = 0; lc < GB; ++lc)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * GT + threadIdx.x;
+              if (i < n) As[lc * LD + i] = buf[lc][u];
+            }
+          if (V) {
+#pragma unroll
+            for (int lc = 0; lc < GB; ++lc)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * GT + threadIdx.x;
+                buf[lc][u] = (lc < L && i < n) ? V[(long long)cols[lc] * n + i] : 0.0;
+              }
+#pragma unroll
+            for (int lc = 0; lc < GB; ++lc)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * GT + threadIdx.x;
+                if (i < n) Vs[lc * LD + i] = buf[lc][u];
+              }
+          }
+        }
+        __syncthreads();
+        for (int it = 0; it < local_iters; ++it) {
+          // fresh Gram: warp w sums rows [w NR/GW, (w+1) NR/GW) with DMMA (A operand = B operand)
+          {
+            double d0 = 0.0, d1 = 0.0;
+            const int k0 = wid * (NR / GW), k1 = k0 + NR / GW;
+            const double* col = As + (lane >> 2) * LD + (lane & 3);
+            for (int k = k0; k < k1; k += 4) {
+              const double x = col[k];
+              dmma8(d0, d1, x, x);
+            }
+            Gp[wid][(lane >> 2) * GB + 2 * (lane & 3)] = d0;
+            Gp[wid][(lane >> 2) * GB + 2 * (lane & 3) + 1] = d1;
+          }
+          __syncthreads();
+          if (threadIdx.x < GB * GB) {
+            double g = 0.0;
+            for (int w = 0; w < GW; ++w) g += Gp[w][threadIdx.x];
+            G[threadIdx.x] = g;
+          }
+          if (threadIdx.x == 0) need = 0;
+          __syncthreads();
+          if (threadIdx.x < GB * GB) {
+            const int p = threadIdx.x / GB, q = threadIdx.x % GB;
+            if (p < q && q < L) {
+              const double ga = G[p * GB + q];
+              if (!(ga == 0.0 || fabs(ga) <= tol * sqrt(G[p * GB + p] * G[q * GB + q]))) need = 1;
+            }
+          }
+          __syncthreads();
+          if (!need) break;
+          if (wid == 0) {
+            // cyclic two-sided Jacobi on G (one warp), rotations accumulated in J
+            for (int e = lane; e < GB * GB; e += 32) J[e] = (e / GB == e % GB) ? 1.0 : 0.0;
+            __syncwarp();
+            for (int es = 0; es < eigen_sweeps; ++es) {
+              int any = 0;
+              for (int rd = 0; rd < GB - 1; ++rd) {
+                if (lane < hb) {
+                  int p = rr_index(lane, rd, GB), q = rr_index(GB - 1 - lane, rd, GB);
+                  if (p > q) { int t = p; p = q; q = t; }
+                  double cs = 1.0, sn = 0.0;
+                  const double al = G[p * GB + p], be = G[q * GB + q], ga = G[p * GB + q];
+                  if (q < L && !(ga == 0.0 || fabs(ga) <= 0.25 * tol * sqrt(al * be))) {
+                    const double zeta = (be - al) / (2.0 * ga);
+                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    cs = 1.0 / sqrt(1.0 + t * t);
+                    sn = cs * t;
+                  }
+                  rc[lane] = cs;
+                  rs[lane] = sn;
+                }
+                __syncwarp();
+                any |= __any_sync(0xffffffffu, lane < hb && rs[lane] != 0.0);
+                {  // columns: G <- G J_r, J <- J J_r   (32 lanes = 4 pairs x 8 rows)
+                  const int k = lane >> 3, i = lane & 7;
+                  int p = rr_index(k, rd, GB), q = rr_index(GB - 1 - k, rd, GB);
+                  if (p > q) { int t = p; p = q; q = t; }
+                  const double cs = rc[k], sn = rs[k];
+                  if (sn != 0.0) {
+                    const double gp = G[i * GB + p], gq = G[i * GB + q];
+                    G[i * GB + p] = cs * gp - sn * gq;
+                    G[i * GB + q] = sn * gp + cs * gq;
+                    const double jp = J[i * GB + p], jq = J[i * GB + q];
+                    J[i * GB + p] = cs * jp - sn * jq;
+                    J[i * GB + q] = sn * jp + cs * jq;
+                  }
+                  __syncwarp();
+                  if (sn != 0.0) {  // rows: G <- J_r^T G
+                    const double gp = G[p * GB + i], gq = G[q * GB + i];
+                    G[p * GB + i] = cs * gp - sn * gq;
+                    G[q * GB + i] = sn * gp + cs * gq;
+                  }
+                  __syncwarp();
+                }
+              }
+              if (!any) break;
+            }
+          }
+          __syncthreads();
+          // A_loc <- A_loc J (and V_loc): warp w takes row tiles of 8, two k-steps of 4 columns
+          for (int rt = wid; rt < NR / 8; rt += GW) {
+            const int r0 = rt * 8;
+            for (int mat = 0; mat < (V ? 2 : 1); ++mat) {
+              double* X = mat ? Vs : As;
+              const double a0 = X[(lane & 3) * LD + r0 + (lane >> 2)];
+              const double a1 = X[(4 + (lane & 3)) * LD + r0 + (lane >> 2)];
+              const double b0 = J[(lane & 3) * GB + (lane >> 2)];
+              const double b1 = J[(4 + (lane & 3)) * GB + (lane >> 2)];
+              double d0 = 0.0, d1 = 0.0;
+              dmma8(d0, d1, a0, b0);
+              dmma8(d0, d1, a1, b1);
+              __syncwarp();
+              X[(2 * (lane & 3)) * LD + r0 + (lane >> 2)] = d0;
+              X[(2 * (lane & 3) + 1) * LD + r0 + (lane >> 2)] = d1;
+            }
+          }
+          if (threadIdx.x == 0) rotated = 1;
+          __syncthreads();
+        }
+        if (rotated) {
+          for (int i0 = 0; i0 < n; i0 += 4 * GT) {
+#pragma unroll
+            for (int lc = 0; lc < GB; ++lc)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * GT + threadIdx.x;
+                if (lc < L && i < n) {
+                  A[(long long)cols[lc] * n + i] = As[lc * LD + i];
+                  if (V) V[(long long)cols[lc] * n + i] = Vs[lc * LD + i];
+                }
+              }
+          }
+        }
+        if (threadIdx.x == 0 && rotated) atomicAdd(c, 1);
+        __syncthreads();
+      }
+      grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(sweep + 1) & 1] = 0;
+    const int done = (*(volatile int*)c) == 0;
+    grid.sync();
+    if (done) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
 __global__ void init_av_kernel(int n, const double* Ain, double* A, double* V) {
   const long long nn = (long long)n * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
@@ -373,7 +600,28 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
     int bsz = (int)(200 * 1024 / (16LL * n * (V ? 2 : 1)));
     if (bsz > 8) bsz = 8;
     cudaError_t e;
-    if (bsz >= 2) {
+    const size_t gsmem = (size_t)GB * (((n + 31) & ~31) + 4) * (V ? 2 : 1) * sizeof(double);
+    static int jalg = -1;
+    if (jalg < 0) {
+      const char* ev = getenv("TTB_JACOBI");
+      jalg = (ev && ev[0] == 'b') ? 1 : 0;
+    }
+    if (jalg == 0 && gsmem <= 200 * 1024) {
+      static int gmax = 0;
+      if (!gmax) {
+        cudaFuncSetAttribute(jacobi_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_gram_kernel, GT, 200 * 1024);
+        gmax = sms * (per > 0 ? per : 1);
+      }
+      const int nbk = (n + GB / 2 - 1) / (GB / 2);
+      int nblk = ((nbk + 1) / 2) < gmax ? ((nbk + 1) / 2) : gmax;
+      static int li = env_int("TTB_JACOBI_LI", kLocalIters), es = env_int("TTB_JACOBI_ES", kEigenSweeps);
+      void* args[] = {&n, &Aw, &Vw, &cnt, &ms, &tl, &sw, &li, &es};
+      e = cudaLaunchCooperativeKernel((void*)jacobi_gram_kernel, dim3(nblk), dim3(GT), args, gsmem, st); ttb_count();
+    } else if (bsz >= 2) {
       static int bmax = 0;
       if (!bmax) {
         cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -80,7 +80,8 @@ def test_qr_rank_deficient(la):
     assert np.abs(Q.cpu().numpy().T @ Q.cpu().numpy() - np.eye(20)).max() < 1e-14
 
 
-@pytest.mark.parametrize("m,n", [(1, 1), (6, 4), (4, 6), (64, 64), (100, 65), (65, 100), (2000, 120), (300, 300)])
+@pytest.mark.parametrize("m,n", [(1, 1), (6, 4), (4, 6), (64, 64), (100, 65), (65, 100), (2000, 120), (300, 300),
+                                 (257, 257), (3000, 515), (1100, 1024)])
 def test_svd(la, m, n):
     rng = np.random.default_rng(10 * m + n)
     X = rng.standard_normal((m, n)) * np.logspace(0, -8, n)[None, :]
@@ -92,6 +93,23 @@ def test_svd(la, m, n):
     k = min(m, n)
     assert np.abs(U.T @ U - np.eye(k)).max() < 1e-12
     assert np.all(np.diff(S) <= 0)
+
+
+def test_svd_graded_and_degenerate(la):
+    # graded singular values down to 1e-14 (relative accuracy of the one-sided Jacobi on R),
+    # repeated singular values and exact rank deficiency, on the multi-CTA Jacobi sizes
+    rng = np.random.default_rng(77)
+    for n, spec in ((384, np.logspace(0, -14, 384)), (520, np.repeat([1.0, 1e-3, 1e-7, 0.0], 130))):
+        Q1, _ = np.linalg.qr(rng.standard_normal((2 * n, n)))
+        Q2, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        X = (Q1 * spec) @ Q2.T
+        U, S, Vt = la.svd(T(X))
+        U, S, Vt = U.cpu().numpy(), S.cpu().numpy(), Vt.cpu().numpy()
+        Sn = np.linalg.svd(X, compute_uv=False)
+        assert np.abs(S - Sn).max() <= 1e-12 * Sn[0]
+        assert np.abs((U * S) @ Vt - X).max() <= 1e-13 * Sn[0] * np.sqrt(n)
+        keep = S > 1e-12 * S[0]
+        assert np.abs(U[:, keep].T @ U[:, keep] - np.eye(keep.sum())).max() < 1e-12
 
 
 def test_lu_and_cholesky(la):

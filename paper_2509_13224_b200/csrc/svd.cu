@@ -312,9 +312,38 @@ __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, double* V, int* cnt, int max_sweeps,
-                                                          double tol, int* sweeps_out, int local_iters,
-                                                          int eigen_sweeps) {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Rotation (c, s) annihilating g_pq of the symmetric 2 x 2 [[al, ga], [ga, be]] (one-sided
+// convention: a_p' = c a_p - s a_q, a_q' = s a_p + c a_q); identity when inactive or when
+// ga^2 <= thr2 al be. t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+// evaluated as |2ga| / (|d| + sqrt(d^2 + 4ga^2)) with one division and one rsqrt.
+__device__ __forceinline__ void jrot(double al, double be, double ga, double thr2, bool active, double& c, double& s) {
+  c = 1.0;
+  s = 0.0;
+  if (active && ga != 0.0 && ga * ga > thr2 * al * be) {
+    const double d = be - al, g2 = 2.0 * ga;
+    const double mag = fabs(g2) / (fabs(d) + sqrt(d * d + g2 * g2));
+    const bool pos = (d == 0.0) || ((d > 0.0) == (g2 > 0.0));
+    const double t = pos ? mag : -mag;
+    c = rsqrt(1.0 + t * t);
+    s = c * t;
+  }
+}
+
+// Rounds are ordered by per-block version counters instead of grid-wide barriers: a CTA starts
+// its pair in round R as soon as both blocks have finished round R - 1 (ver[b] == R), and
+// publishes them with a release store; one grid barrier per sweep takes the stop decision.
+__global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, double* V, int* cnt, int* ver,
+                                                          int max_sweeps, double tol, int* sweeps_out,
+                                                          int local_iters, int eigen_sweeps) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
   __shared__ double Gp[GW][GB * GB];
@@ -332,17 +361,27 @@ __global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, doubl
   double* As = sm;
   double* Vs = sm + (long long)GB * LD;
   if (blockIdx.x == 0 && threadIdx.x == 0) { cnt[0] = 0; cnt[1] = 0; }
+  if (blockIdx.x == 0)
+    for (int b = threadIdx.x; b < nb; b += GT) ver[b] = 0;
   for (int e = threadIdx.x; e < GB * LD; e += GT) { As[e] = 0.0; if (V) Vs[e] = 0.0; }
   grid.sync();
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     int* c = cnt + (sweep & 1);
     for (int r = 0; r < NBL - 1; ++r) {
+      const int R = sweep * (NBL - 1) + r;
       for (int pr = blockIdx.x; pr < NBL / 2; pr += gridDim.x) {
         int bp = rr_index(pr, r, NBL), bq = rr_index(NBL - 1 - pr, r, NBL);
         if (bp > bq) { int t = bp; bp = bq; bq = t; }
-        if (bq >= nb) continue;  // dummy block (uniform per CTA)
+        if (bq >= nb) {  // paired with the dummy block: just pass the round
+          if (threadIdx.x == 0 && bp < nb) {
+            while (ld_acquire(ver + bp) < R) {}
+            st_release(ver + bp, R + 1);
+          }
+          continue;
+        }
         if (threadIdx.x == 0) {
+          while (ld_acquire(ver + bp) < R || ld_acquire(ver + bq) < R) {}
           int L = 0;
           for (int j = bp * hb; j < min(n, bp * hb + hb); ++j) cols[L++] = j;
           for (int j = bq * hb; j < min(n, bq * hb + hb); ++j) cols[L++] = j;
@@ -358,7 +397,7 @@ __global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, doubl
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int i = i0 + u * GT + threadIdx.x;
-              buf[lc][u] = (lc < L && i < n) ? A[(long long)cols[lc] * n + i] : 0.0;
+              buf[lc][u] = (lc < L && i < n) ? __ldcg(A + (long long)cols[lc] * n + i) : 0.0;
             }
 #pragma unroll
           for (int lc = 0; lc < GB; ++lc)
@@ -373,7 +412,7 @@ __global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, doubl
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int i = i0 + u * GT + threadIdx.x;
-                buf[lc][u] = (lc < L && i < n) ? V[(long long)cols[lc] * n + i] : 0.0;
+                buf[lc][u] = (lc < L && i < n) ? __ldcg(V + (long long)cols[lc] * n + i) : 0.0;
               }
 #pragma unroll
             for (int lc = 0; lc < GB; ++lc)
@@ -416,51 +455,37 @@ __global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, doubl
           __syncthreads();
           if (!need) break;
           if (wid == 0) {
-            // cyclic two-sided Jacobi on G (one warp), rotations accumulated in J
+            // cyclic two-sided Jacobi on G (one warp), rotations accumulated in J. Per round the
+            // 4 disjoint rotations are recomputed by every lane that needs them (no exchange), and
+            // G <- J_r^T G J_r is formed block-wise: lane = (row pair k1, col pair k2, row r).
             for (int e = lane; e < GB * GB; e += 32) J[e] = (e / GB == e % GB) ? 1.0 : 0.0;
             __syncwarp();
+            const double thr2 = 0.0625 * tol * tol;
+            const int k1 = (lane >> 3) & 3, k2 = (lane >> 1) & 3, rr = lane & 1, ji = lane & 7;
             for (int es = 0; es < eigen_sweeps; ++es) {
-              int any = 0;
+              bool any = false;
               for (int rd = 0; rd < GB - 1; ++rd) {
-                if (lane < hb) {
-                  int p = rr_index(lane, rd, GB), q = rr_index(GB - 1 - lane, rd, GB);
-                  if (p > q) { int t = p; p = q; q = t; }
-                  double cs = 1.0, sn = 0.0;
-                  const double al = G[p * GB + p], be = G[q * GB + q], ga = G[p * GB + q];
-                  if (q < L && !(ga == 0.0 || fabs(ga) <= 0.25 * tol * sqrt(al * be))) {
-                    const double zeta = (be - al) / (2.0 * ga);
-                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    cs = 1.0 / sqrt(1.0 + t * t);
-                    sn = cs * t;
-                  }
-                  rc[lane] = cs;
-                  rs[lane] = sn;
-                }
+                int p1 = rr_index(k1, rd, GB), q1 = rr_index(GB - 1 - k1, rd, GB);
+                if (p1 > q1) { int t = p1; p1 = q1; q1 = t; }
+                int p2 = rr_index(k2, rd, GB), q2 = rr_index(GB - 1 - k2, rd, GB);
+                if (p2 > q2) { int t = p2; p2 = q2; q2 = t; }
+                double c1, s1, c2, s2;
+                jrot(G[p1 * GB + p1], G[q1 * GB + q1], G[p1 * GB + q1], thr2, q1 < L, c1, s1);
+                jrot(G[p2 * GB + p2], G[q2 * GB + q2], G[p2 * GB + q2], thr2, q2 < L, c2, s2);
+                any |= (s1 != 0.0);
+                const int x = rr ? q1 : p1;
+                const double gpp = G[p1 * GB + p2], gpq = G[p1 * GB + q2], gqp = G[q1 * GB + p2], gqq = G[q1 * GB + q2];
+                const double up = rr ? (s1 * gpp + c1 * gqp) : (c1 * gpp - s1 * gqp);
+                const double uq = rr ? (s1 * gpq + c1 * gqq) : (c1 * gpq - s1 * gqq);
+                const double jp = J[ji * GB + p1], jq = J[ji * GB + q1];
                 __syncwarp();
-                any |= __any_sync(0xffffffffu, lane < hb && rs[lane] != 0.0);
-                {  // columns: G <- G J_r, J <- J J_r   (32 lanes = 4 pairs x 8 rows)
-                  const int k = lane >> 3, i = lane & 7;
-                  int p = rr_index(k, rd, GB), q = rr_index(GB - 1 - k, rd, GB);
-                  if (p > q) { int t = p; p = q; q = t; }
-                  const double cs = rc[k], sn = rs[k];
-                  if (sn != 0.0) {
-                    const double gp = G[i * GB + p], gq = G[i * GB + q];
-                    G[i * GB + p] = cs * gp - sn * gq;
-                    G[i * GB + q] = sn * gp + cs * gq;
-                    const double jp = J[i * GB + p], jq = J[i * GB + q];
-                    J[i * GB + p] = cs * jp - sn * jq;
-                    J[i * GB + q] = sn * jp + cs * jq;
-                  }
-                  __syncwarp();
-                  if (sn != 0.0) {  // rows: G <- J_r^T G
-                    const double gp = G[p * GB + i], gq = G[q * GB + i];
-                    G[p * GB + i] = cs * gp - sn * gq;
-                    G[q * GB + i] = sn * gp + cs * gq;
-                  }
-                  __syncwarp();
-                }
+                G[x * GB + p2] = c2 * up - s2 * uq;
+                G[x * GB + q2] = s2 * up + c2 * uq;
+                J[ji * GB + p1] = c1 * jp - s1 * jq;
+                J[ji * GB + q1] = s1 * jp + c1 * jq;
+                __syncwarp();
               }
-              if (!any) break;
+              if (!__any_sync(0xffffffffu, any)) break;
             }
           }
           __syncthreads();
@@ -498,11 +523,16 @@ __global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, doubl
               }
           }
         }
-        if (threadIdx.x == 0 && rotated) atomicAdd(c, 1);
         __syncthreads();
+        if (threadIdx.x == 0) {
+          if (rotated) atomicAdd(c, 1);
+          __threadfence();
+          st_release(ver + bp, R + 1);
+          st_release(ver + bq, R + 1);
+        }
       }
-      grid.sync();
     }
+    grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(sweep + 1) & 1] = 0;
     const int done = (*(volatile int*)c) == 0;
     grid.sync();
@@ -619,7 +649,14 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
       const int nbk = (n + GB / 2 - 1) / (GB / 2);
       int nblk = ((nbk + 1) / 2) < gmax ? ((nbk + 1) / 2) : gmax;
       static int li = env_int("TTB_JACOBI_LI", kLocalIters), es = env_int("TTB_JACOBI_ES", kEigenSweeps);
-      void* args[] = {&n, &Aw, &Vw, &cnt, &ms, &tl, &sw, &li, &es};
+      static int* ver = nullptr;
+      static int ver_cap = 0;
+      if (nbk > ver_cap) {
+        if (ver) { cudaStreamSynchronize(st); cudaFree(ver); }
+        ver_cap = nbk + 1024;
+        if (cudaMalloc(&ver, sizeof(int) * ver_cap) != cudaSuccess) { ver = nullptr; ver_cap = 0; return (int)cudaErrorMemoryAllocation; }
+      }
+      void* args[] = {&n, &Aw, &Vw, &cnt, &ver, &ms, &tl, &sw, &li, &es};
       e = cudaLaunchCooperativeKernel((void*)jacobi_gram_kernel, dim3(nblk), dim3(GT), args, gsmem, st); ttb_count();
     } else if (bsz >= 2) {
       static int bmax = 0;

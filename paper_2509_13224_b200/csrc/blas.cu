@@ -70,7 +70,9 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WM, wn = warp / WM;
-  const int bm0 = blockIdx.y * BM, bn0 = blockIdx.x * BN;
+  // CI (short-K read-modify-write updates): M tiles fastest, so the CTAs sharing one B tile run
+  // together and B is fetched from HBM once
+  const int bm0 = (CI ? blockIdx.x : blockIdx.y) * BM, bn0 = (CI ? blockIdx.y : blockIdx.x) * BN;
   const long long bz = blockIdx.z;
   const double* A;
   const double* B;
@@ -232,7 +234,7 @@ int launch_gemm_t(const GemmArgs& g, int batch, cudaStream_t st) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), batch);
+  dim3 grid = CI ? dim3(ceil_div(g.M, BM), ceil_div(g.N, BN), batch) : dim3(ceil_div(g.N, BN), ceil_div(g.M, BM), batch);
   dgemm_kernel<BM, BN, WM, WN, TA, TB, VEC, STAGES, CI><<<grid, T, smem, st>>>(g); ttb_count();
   return ttb_last_error();
 }

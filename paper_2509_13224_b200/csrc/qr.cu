@@ -344,28 +344,23 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(int m, int nb, const 
   if (threadIdx.x < pairs) part[(long long)blockIdx.x * pairs + threadIdx.x] = (a <= b) ? acc : 0.0;
 }
 
+// one CTA per Gram entry (upper triangle a <= b; larft reads only that): fixed-order block sum
 __global__ void gram_final_kernel(int nb, int nblk, const double* __restrict__ part, double* G) {
+  __shared__ double red[32];
   const int pairs = nb * nb;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int e = wid; e < pairs; e += blockDim.x / 32) {
-    double v = 0.0;
-    for (int b = lane; b < nblk; b += 32) v += part[(long long)b * pairs + e];
-    v = warp_sum(v);
-    if (lane == 0) G[e] = v;
-  }
-  __syncthreads();
-  // mirror the upper triangle (a <= b) into the lower one
-  for (int e = threadIdx.x; e < pairs; e += blockDim.x) {
-    const int a = e / nb, b = e % nb;
-    if (a > b) G[e] = G[b * nb + a];
-  }
+  const int e = blockIdx.x;
+  if ((e / nb) > (e % nb)) return;  // uniform per CTA
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) v += part[(long long)b * pairs + e];
+  v = block_sum(v, red);
+  if (threadIdx.x == 0) G[e] = v;
 }
 
 int launch_gram(int m, int nb, const double* V, double* G, double* part, cudaStream_t st) {
   int blocks = ceil_div(m, 128);
   if (blocks > 592) blocks = 592;
   gram_partial_kernel<<<blocks, 256, 0, st>>>(m, nb, V, part); ttb_count();
-  gram_final_kernel<<<1, 256, 0, st>>>(nb, blocks, part, G); ttb_count();
+  gram_final_kernel<<<nb * nb, 128, 0, st>>>(nb, blocks, part, G); ttb_count();
   return ttb_last_error();
 }
 
@@ -417,6 +412,21 @@ int apply_wy(void* stream, int mp, int nq, int jb, const double* V, const double
 }
 
 }  // namespace
+
+// Householder panel with dgeqr2 + dlarft outputs (single-CTA kernel when it fits shared memory,
+// else the cooperative one + Gram + larft); tsqr.cu runs it on the stacked R factors.
+// part: kMaxPanelBlocks * (NB * NB + NB + 2) doubles, G: NB * NB doubles.
+int householder_panel(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, double* part,
+                      double* G, cudaStream_t st) {
+  if (panel_is_small(m, jb)) return launch_panel_small(m, jb, P, ld, tau, V, T, st);
+  int rc = launch_panel(m, jb, P, ld, tau, V, T, part, st);
+  if (rc) return rc;
+  rc = launch_gram(m, jb, V, G, part, st);
+  if (rc) return rc;
+  larft_kernel<<<1, 128, 0, st>>>(jb, G, jb, tau, T); ttb_count();
+  return ttb_last_error();
+}
+long long householder_panel_part() { return (long long)kMaxPanelBlocks * (NB * NB + NB + 2); }
 
 // Workspace sizes (in doubles) for ttb_geqrf / ttb_orgqr.
 TTB_API long long ttb_qr_workspace(int m, int n) {

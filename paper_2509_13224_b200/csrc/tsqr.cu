@@ -5,19 +5,18 @@
 // above it), tau and the compact-WY factor T. A column-by-column panel over 1M rows is bound by
 // one grid-wide reduction per column and by re-streaming the panel once per column. Here:
 //
-//   1. every warp factors one tile of <= 128 rows held in registers (4 rows per lane; the
-//      column reductions are warp shuffles, T is built alongside in the dlarft recurrence);
-//   2. the jb x jb R factors of all tiles are stacked and factored the same way, level by
-//      level (8x fewer rows per level), until one tile is left;
-//   3. the explicit orthonormal Q of the panel is formed top-down (Q_tile = H_tile [X; 0],
-//      X = the tile's block of its parent's Q, applied in compact-WY form);
-//   4. Householder reconstruction (Ballard, Demmel, Grigori, Jacquelin, Nguyen, Solomonik
-//      2014): the LU factorization Y = [I; 0] - Q S = V U with the sign matrix S chosen on the
-//      fly (pivots 1 + |q_kk| >= 1) gives V (= L), T = U L^{-T}, tau = diag(U), R = S R_tsqr.
-//      The leaf pass of step 3 writes V_below = -Q_below S U^{-1} directly.
+//   1. every warp factors one tile of <= 128 rows held in registers (4 rows per lane; one
+//      batched warp reduction per column, T built alongside in the dlarft recurrence);
+//   2. the jb x jb R factors of all tiles (m/8 rows) are stacked and factored by the ordinary
+//      Householder panel (qr.cu), whose WY form gives their explicit Q, X1;
+//   3. Householder reconstruction (Ballard, Demmel, Grigori, Jacquelin, Nguyen, Solomonik
+//      2014): with the panel's orthonormal Q (Q_tile = H_tile [X1 block; 0]), the LU
+//      factorization Y = [I; 0] - Q S = V U with the sign matrix S chosen on the fly (pivots
+//      1 + |q_kk| >= 1) gives V (= L on top), T = U L^{-T}, tau = diag(U), R = S R_tsqr;
+//   4. one leaf pass forms every tile's Q rows and writes V_below = -Q_below S U^{-1}.
 //
 // Passes over the panel: read + write in step 1, read + write (P and the explicit V copy) in
-// the leaf pass; everything else touches jb/8 of the rows or less.
+// step 4; the stacked level touches jb/8 of the rows.
 #include "common.cuh"
 
 namespace {
@@ -45,24 +44,57 @@ __device__ __forceinline__ void load_tile(double (&a)[TS][NB], const double* M, 
     }
 }
 
-// Sum each of the first n entries of z over the warp (butterfly; every lane gets the sums).
-template <int N>
-__device__ __forceinline__ void warp_sum_vec(double (&z)[NB], int n) {
+// Warp all-reduce of 16 values: reduce-scatter over lane bits 4..1 (lane l ends with the sum of
+// index l >> 1), a final exchange over bit 0, then an all-gather: 64 shuffles instead of 160.
+__device__ __forceinline__ void warp_allreduce16(double (&z)[NB], int lane) {
+  double v8[8], v4[4], v2[2];
+  {
+    const bool hi = lane & 16;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+    for (int k = 0; k < 8; ++k) {
+      const double send = hi ? z[k] : z[k + 8];
+      const double keep = hi ? z[k + 8] : z[k];
+      v8[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
 #pragma unroll
-    for (int c = 0; c < N; ++c)
-      if (c < n) z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
+    for (int k = 0; k < 4; ++k) {
+      const double send = hi ? v8[k] : v8[k + 4];
+      const double keep = hi ? v8[k + 4] : v8[k];
+      v4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double send = hi ? v4[k] : v4[k + 2];
+      const double keep = hi ? v4[k + 2] : v4[k];
+      v2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  double v;
+  {
+    const bool hi = lane & 2;
+    const double send = hi ? v2[0] : v2[1];
+    const double keep = hi ? v2[1] : v2[0];
+    v = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  v += __shfl_xor_sync(0xffffffffu, v, 1);  // lane l: full sum of index l >> 1
+#pragma unroll
+  for (int c = 0; c < NB; ++c) z[c] = __shfl_sync(0xffffffffu, v, 2 * c);
 }
 
 // Householder QR of every tile of an (rows x jb) col-major matrix M (in place: R on/above the
 // diagonal, V below), T per tile (NB x NB row-major) and the tile's R into rows [t jb, t jb + jb)
-// of S (col-major, ld ldS). JB > 0: compile-time panel width.
+// of S (col-major, ld ldS). JB > 0: compile-time panel width. Columns >= jb are zero.
 //
 // One batched warp reduction per column: with x = A[j+1:, j] the statistics
 // z_c = x^T A[j+1:, c] (c = j: ||x||^2; c > j: trailing columns; c < j: stored reflectors) give
 // both the reflector application w_c = A[j, c] + scal z_c and the dlarft column
-// v_b^T v_j = V[j, b] + scal z_b, and are accumulated while column j-1's update is applied.
+// v_b^T v_j = V[j, b] + scal z_b, and are accumulated right after column j-1's update.
 template <int JB>
 __global__ void __launch_bounds__(FW * 32) tsqr_factor_kernel(double* M, long long ld, long long rows, int nt, int jb_rt,
                                                                double* Tt, double* S, long long ldS) {
@@ -79,22 +111,27 @@ __global__ void __launch_bounds__(FW * 32) tsqr_factor_kernel(double* M, long lo
   double* T = Tsh[w];
   for (int e = lane; e < NB * NB; e += 32) T[e] = 0.0;
   double z[NB];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    z[c] = 0.0;
+  {
+    double x[TS];
 #pragma unroll
     for (int s = 0; s < TS; ++s) {
       const int i = lane + 32 * s;
-      if (i > 0 && i < r && c < jb) z[c] += a[s][0] * a[s][c];
+      x[s] = (i > 0 && i < r) ? a[s][0] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      z[c] = 0.0;
+#pragma unroll
+      for (int s = 0; s < TS; ++s) z[c] += x[s] * a[s][c];
     }
   }
-  warp_sum_vec<JB ? JB : NB>(z, jb);
+  warp_allreduce16(z, lane);
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     if (j < jb) {
       double rowj[NB];  // row j of the tile (lane j, slot 0)
 #pragma unroll
-      for (int c = 0; c < NB; ++c) rowj[c] = (c < jb) ? __shfl_sync(0xffffffffu, a[0][c], j) : 0.0;
+      for (int c = 0; c < NB; ++c) rowj[c] = __shfl_sync(0xffffffffu, a[0][c], j);
       const double alpha = rowj[j], s2 = z[j];
       double beta, tj, scal;
       if (s2 == 0.0) {
@@ -116,29 +153,31 @@ __global__ void __launch_bounds__(FW * 32) tsqr_factor_kernel(double* M, long lo
         T[lane * NB + j] = -tj * acc;
       }
       if (lane == 0) T[j * NB + j] = tj;
+      // v (zero above row j, 1 at row j), then A[:, c] -= tj v w_c for c > j
 #pragma unroll
       for (int s = 0; s < TS; ++s) {
         const int i = lane + 32 * s;
-        if (i >= j && i < r) {
-          double vi = 1.0;
-          if (i > j) { vi = a[s][j] * scal; a[s][j] = vi; }
+        const double vi = (i > j && i < r) ? a[s][j] * scal : (i == j ? 1.0 : 0.0);
+        if (i > j) a[s][j] = vi;
+        const double tv = tj * vi;
 #pragma unroll
-          for (int c = 0; c < NB; ++c)
-            if (c > j && c < jb) a[s][c] -= tj * vi * wv[c];
-        }
+        for (int c = j + 1; c < NB; ++c) a[s][c] -= tv * wv[c];
       }
       if (lane == j) a[0][j] = beta;
       if (j + 1 < jb) {  // statistics of column j + 1
+        double x[TS];
+#pragma unroll
+        for (int s = 0; s < TS; ++s) {
+          const int i = lane + 32 * s;
+          x[s] = (i > j + 1 && i < r) ? a[s][j + 1] : 0.0;
+        }
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
           z[c] = 0.0;
 #pragma unroll
-          for (int s = 0; s < TS; ++s) {
-            const int i = lane + 32 * s;
-            if (i > j + 1 && i < r && c < jb) z[c] += a[s][j + 1] * a[s][c];
-          }
+          for (int s = 0; s < TS; ++s) z[c] += x[s] * a[s][c];
         }
-        warp_sum_vec<JB ? JB : NB>(z, jb);
+        warp_allreduce16(z, lane);
       }
       __syncwarp();
     }
@@ -157,33 +196,29 @@ __global__ void __launch_bounds__(FW * 32) tsqr_factor_kernel(double* M, long lo
   for (int e = lane; e < NB * NB; e += 32) Tt[(long long)t * NB * NB + e] = T[e];
 }
 
-// Q_tile = H_tile [X; 0] = [X; 0] - V (T (V_top^T X)) for every tile of a factored level.
-// X = rows [t jb, t jb + jb) of the parent's Q (col-major, ld ldX), or the identity (top level).
-// LEAF: instead of Q, write the reconstructed Householder vectors V = Q Z, Z = -S U^{-1}, of rows
-// >= jb to M (below-diagonal storage) and to the explicit V copy Vx (col-major, ld rows).
-template <bool LEAF>
-__global__ void __launch_bounds__(QW * 32) tsqr_form_kernel(double* M, long long ld, long long rows, int nt, int jb,
+// Leaf pass: the panel's Householder vectors V = Q Z (Z = -S U^{-1}) for rows >= jb, where the
+// tile's orthonormal rows are Q_tile = H_tile [X; 0] = [X; 0] - V_tile (T (V_top^T X)) and X is
+// the tile's jb x jb block of X1 (col-major, ld ldX). Folded: V = [X Z; 0] - V_tile (W Z),
+// W = T V_top^T X, one 16 x 16 product per row. Written to M (below-diagonal storage) and to
+// the explicit copy Vx (col-major, ld rows); the top jb rows of tile 0 (R and L) come from
+// the setup kernel through Z + NB*NB.
+__global__ void __launch_bounds__(QW * 32) tsqr_leaf_kernel(double* M, long long ld, long long rows, int nt, int jb,
                                                              const double* __restrict__ Tt, const double* X,
                                                              long long ldX, const double* __restrict__ Z,
                                                              double* Vx) {
-  __shared__ double Vt[QW][NB * LDS];  // V_top, later W
-  __shared__ double Xs[QW][NB * LDS];
-  __shared__ double Ms[QW][NB * LDS];
+  __shared__ double Bf[QW][3][NB * LDS];
   __shared__ double Zs[NB * LDS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (LEAF) {
-    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Zs[(e / NB) * LDS + (e % NB)] = Z[e];
-    __syncthreads();
-  }
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Zs[(e / NB) * LDS + (e % NB)] = Z[e];
+  __syncthreads();
   const int t = blockIdx.x * QW + w;
   if (t >= nt) return;
   long long r0;
   int r;
   tile_bounds(rows, nt, t, r0, r);
-  double* vt = Vt[w];
-  double* xs = Xs[w];
-  double* ms = Ms[w];
-  // V_top (rows 0..NB-1 of the tile; explicit: unit diagonal, zeros above; rows >= jb meet X = 0)
+  double* vt = Bf[w][0];
+  double* xs = Bf[w][1];
+  double* ms = Bf[w][2];
   if (lane < NB)
 #pragma unroll
     for (int c = 0; c < NB; ++c)
@@ -191,13 +226,11 @@ __global__ void __launch_bounds__(QW * 32) tsqr_form_kernel(double* M, long long
                                                 : 0.0;
   for (int e = lane; e < NB * NB; e += 32) {
     const int i = e % NB, c = e / NB;
-    double x = 0.0;
-    if (i < jb && c < jb) x = X ? X[(long long)c * ldX + (long long)t * jb + i] : (i == c ? 1.0 : 0.0);
-    xs[i * LDS + c] = x;
+    xs[i * LDS + c] = (i < jb && c < jb) ? X[(long long)c * ldX + (long long)t * jb + i] : 0.0;
   }
   __syncwarp();
   const double* Tg = Tt + (long long)t * NB * NB;
-  for (int e = lane; e < NB * NB; e += 32) {  // M1 = V_top^T X
+  for (int e = lane; e < NB * NB; e += 32) {  // ms = V_top^T X
     const int p = e / NB, c = e % NB;
     double acc = 0.0;
 #pragma unroll
@@ -205,7 +238,7 @@ __global__ void __launch_bounds__(QW * 32) tsqr_form_kernel(double* M, long long
     ms[p * LDS + c] = acc;
   }
   __syncwarp();
-  for (int e = lane; e < NB * NB; e += 32) {  // W = T M1 (T upper)
+  for (int e = lane; e < NB * NB; e += 32) {  // vt = W = T ms (T upper)
     const int p = e / NB, c = e % NB;
     double acc = 0.0;
 #pragma unroll
@@ -213,52 +246,43 @@ __global__ void __launch_bounds__(QW * 32) tsqr_form_kernel(double* M, long long
     vt[p * LDS + c] = acc;
   }
   __syncwarp();
-  double v[TS][NB];
+  for (int e = lane; e < NB * NB; e += 32) {  // ms = W Z, Z upper
+    const int p = e / NB, c = e % NB;
+    double acc = 0.0;
 #pragma unroll
-  for (int s = 0; s < TS; ++s) {
-    const int i = lane + 32 * s;
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-      v[s][c] = (c < jb && i < r) ? (i > c ? M[(long long)c * ld + r0 + i] : (i == c ? 1.0 : 0.0)) : 0.0;
+    for (int b = 0; b < NB; ++b) acc += (b <= c ? vt[p * LDS + b] * Zs[b * LDS + c] : 0.0);
+    ms[p * LDS + c] = acc;
   }
+  __syncwarp();
+  for (int e = lane; e < NB * NB; e += 32) {  // vt = X Z
+    const int p = e / NB, c = e % NB;
+    double acc = 0.0;
 #pragma unroll
-  for (int s = 0; s < TS; ++s) {
+    for (int b = 0; b < NB; ++b) acc += (b <= c ? xs[p * LDS + b] * Zs[b * LDS + c] : 0.0);
+    vt[p * LDS + c] = acc;
+  }
+  __syncwarp();
+  for (int s = 0; s < TS; ++s) {  // one row per lane at a time (keeps registers low)
     const int i = lane + 32 * s;
     if (i >= r) continue;
-    double q[NB];
+    if (r0 + i < jb) {  // top rows (R and L), prepared by the setup kernel behind Z
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c < jb) M[(long long)c * ld + i] = Z[NB * NB + c * NB + i];
+      continue;
+    }
+    double v[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) v[c] = (c < jb) ? (i > c ? M[(long long)c * ld + r0 + i] : (i == c ? 1.0 : 0.0)) : 0.0;
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      double acc = (i < NB) ? xs[i * LDS + c] : 0.0;
+      if (c < jb) {
+        double acc = (i < NB) ? vt[i * LDS + c] : 0.0;
 #pragma unroll
-      for (int p = 0; p < NB; ++p) acc -= v[s][p] * vt[p * LDS + c];
-      q[c] = acc;
-    }
-    if (!LEAF) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (c < jb) M[(long long)c * ld + r0 + i] = q[c];
-    } else {
-      if (r0 + i < jb) {  // top rows (R and L), prepared by the setup kernel behind Z
-#pragma unroll
-        for (int c = 0; c < NB; ++c)
-          if (c < jb) M[(long long)c * ld + i] = Z[NB * NB + c * NB + i];
-        continue;
+        for (int p = 0; p < NB; ++p) acc -= v[p] * ms[p * LDS + c];
+        M[(long long)c * ld + r0 + i] = acc;
+        Vx[(long long)c * rows + r0 + i] = acc;
       }
-      // V row = -(q S) U^{-1} = q Z (Z from the setup kernel)
-      double y[NB];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int p = 0; p <= c; ++p) acc += q[p] * Zs[p * LDS + c];
-        y[c] = acc;
-      }
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (c < jb) {
-          M[(long long)c * ld + r0 + i] = y[c];
-          Vx[(long long)c * rows + r0 + i] = y[c];
-        }
     }
   }
 }
@@ -270,7 +294,7 @@ __global__ void __launch_bounds__(QW * 32) tsqr_form_kernel(double* M, long long
 // leaf pass.
 __global__ void tsqr_setup_kernel(int jb, double* P, long long ld, long long mp, const double* __restrict__ T0,
                                   const double* __restrict__ X1, long long ldX1, const double* __restrict__ Rt,
-                                  double* tau, double* Vx, double* Tout, double* Z) {
+                                  long long ldR, double* tau, double* Vx, double* Tout, double* Z) {
   __shared__ double Vt[NB * LDS], Xs[NB * LDS], Ms[NB * LDS], Ws[NB * LDS];
   __shared__ double E[NB * LDS], Q[NB * LDS], L[NB * LDS], U[NB * LDS], Li[NB * LDS];
   __shared__ double sg[NB];
@@ -349,7 +373,7 @@ __global__ void tsqr_setup_kernel(int jb, double* P, long long ld, long long mp,
   }
   for (int e = lane; e < jb * jb; e += 32) {
     const int i = e % jb, c = e / jb;
-    Z[NB * NB + c * NB + i] = (i <= c) ? sg[i] * Rt[(long long)c * jb + i] : L[i * LDS + c];  // P top block
+    Z[NB * NB + c * NB + i] = (i <= c) ? sg[i] * Rt[(long long)c * ldR + i] : L[i * LDS + c];  // P top block
     Vx[(long long)c * mp + i] = (i < c) ? 0.0 : (i == c ? 1.0 : L[i * LDS + c]);
   }
   if (lane < jb) tau[lane] = U[lane * LDS + lane];
@@ -369,21 +393,47 @@ __global__ void tsqr_setup_kernel(int jb, double* P, long long ld, long long mp,
   }
 }
 
+// X = [I; 0] - V (T V_top^T): explicit Q of a WY-factored panel (V col-major, ld rows, unit lower;
+// T row-major jb x jb, upper)
+__global__ void tsqr_q1_kernel(long long rows, int jb, const double* __restrict__ V, const double* __restrict__ T,
+                               double* X) {
+  __shared__ double W[NB * NB];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int p = e / NB, c = e % NB;
+    double acc = 0.0;
+    if (p < jb && c < jb)
+      for (int b = p; b <= c; ++b) acc += T[p * jb + b] * (b == c ? 1.0 : V[(long long)b * rows + c]);
+    W[e] = acc;
+  }
+  __syncthreads();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows; i += (long long)gridDim.x * blockDim.x) {
+    double v[NB];
+#pragma unroll
+    for (int p = 0; p < NB; ++p) v[p] = (p < jb) ? (i == p ? 1.0 : (i > p ? V[(long long)p * rows + i] : 0.0)) : 0.0;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      if (c >= jb) break;
+      double acc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int p = 0; p < NB; ++p) acc -= v[p] * W[p * NB + c];
+      X[(long long)c * rows + i] = acc;
+    }
+  }
+}
+
 int tiles_of(long long rows) { return (int)((rows + TR - 1) / TR); }
 
 }  // namespace
 
+int householder_panel(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, double* part,
+                      double* G, cudaStream_t st);
+long long householder_panel_part();
+
 // Workspace (doubles) for tsqr_panel on panels of up to m rows.
 long long tsqr_workspace(long long m) {
-  long long s = 3 * NB * NB + 128;
-  long long rows = m;
-  while (rows > TR) {
-    const long long nt = (rows + TR - 1) / TR;
-    s += nt * NB * NB;          // T per tile
-    rows = nt * NB;
-    s += rows * NB;             // stacked R of the next level
-  }
-  return s + NB * NB + 64;      // top level T
+  const long long nt = (m + TR - 1) / TR;
+  const long long rows1 = nt * NB;
+  return householder_panel_part() + 4 * NB * NB + 2 * NB + nt * NB * NB + 3 * rows1 * NB + 256;
 }
 
 bool tsqr_applies(long long m, int jb) { return m > 8LL * TR && jb >= 1 && jb <= NB; }
@@ -392,46 +442,32 @@ bool tsqr_applies(long long m, int jb) { return m > 8LL * TR && jb >= 1 && jb <=
 // explicit V (m x jb, ld m, unit diagonal, zeros above) and T (jb x jb row-major, upper).
 int tsqr_panel(long long m, int jb, double* P, long long ld, double* tau, double* V, double* Tout, double* ws,
                cudaStream_t st) {
-  constexpr int kMaxLevels = 16;
-  double* US = ws;                  // Z = -S U^{-1} (NB x NB) | P top block (NB x NB, col-major)
-  double* Rt = US + 2 * NB * NB;    // top-level R (jb x jb, ld jb)
-  double* cur = Rt + NB * NB + 64;
-  double* M[kMaxLevels];
-  long long ldm[kMaxLevels], rows[kMaxLevels];
-  double* Tt[kMaxLevels];
-  int nt[kMaxLevels];
-  int L = 0;
-  M[0] = P; ldm[0] = ld; rows[0] = m;
-  for (;;) {
-    if (L + 1 >= kMaxLevels) return TTB_EARG;
-    nt[L] = tiles_of(rows[L]);
-    Tt[L] = cur;
-    cur += (long long)nt[L] * NB * NB;
-    if (nt[L] == 1) break;
-    rows[L + 1] = (long long)nt[L] * jb;
-    ldm[L + 1] = rows[L + 1];
-    M[L + 1] = cur;
-    cur += rows[L + 1] * NB;
-    ++L;
+  const int nt = tiles_of(m);
+  const long long rows1 = (long long)nt * jb;
+  if (rows1 > 0x7fffffffLL) return TTB_EARG;
+  double* part = ws;
+  double* G = part + householder_panel_part();
+  double* T1 = G + NB * NB;
+  double* Z = T1 + NB * NB;         // Z = -S U^{-1} | P top block
+  double* tau1 = Z + 2 * NB * NB;
+  double* Tt = tau1 + 2 * NB;
+  double* S1 = Tt + (long long)nt * NB * NB;
+  double* V1 = S1 + rows1 * NB;
+  double* X1 = V1 + rows1 * NB;
+  if (jb == NB)
+    tsqr_factor_kernel<NB><<<ceil_div(nt, FW), FW * 32, 0, st>>>(P, ld, m, nt, jb, Tt, S1, rows1);
+  else
+    tsqr_factor_kernel<0><<<ceil_div(nt, FW), FW * 32, 0, st>>>(P, ld, m, nt, jb, Tt, S1, rows1);
+  ttb_count();
+  int rc = householder_panel((int)rows1, jb, S1, rows1, tau1, V1, T1, part, G, st);
+  if (rc) return rc;
+  {
+    int blocks = ceil_div(rows1, 256);
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    tsqr_q1_kernel<<<blocks, 256, 0, st>>>(rows1, jb, V1, T1, X1); ttb_count();
   }
-  for (int l = 0; l <= L; ++l) {
-    double* S = (l == L) ? Rt : M[l + 1];
-    const long long ldS = (l == L) ? jb : ldm[l + 1];
-    if (jb == NB)
-      tsqr_factor_kernel<NB><<<ceil_div(nt[l], FW), FW * 32, 0, st>>>(M[l], ldm[l], rows[l], nt[l], jb, Tt[l], S, ldS);
-    else
-      tsqr_factor_kernel<0><<<ceil_div(nt[l], FW), FW * 32, 0, st>>>(M[l], ldm[l], rows[l], nt[l], jb, Tt[l], S, ldS);
-    ttb_count();
-  }
-  for (int l = L; l >= 1; --l) {
-    const double* X = (l == L) ? nullptr : M[l + 1];
-    const long long ldX = (l == L) ? 0 : ldm[l + 1];
-    tsqr_form_kernel<false><<<ceil_div(nt[l], QW), QW * 32, 0, st>>>(M[l], ldm[l], rows[l], nt[l], jb, Tt[l], X, ldX,
-                                                                     nullptr, nullptr);
-    ttb_count();
-  }
-  tsqr_setup_kernel<<<1, 32, 0, st>>>(jb, P, ld, m, Tt[0], M[1], ldm[1], Rt, tau, V, Tout, US); ttb_count();
-  tsqr_form_kernel<true><<<ceil_div(nt[0], QW), QW * 32, 0, st>>>(P, ld, m, nt[0], jb, Tt[0], M[1], ldm[1], US, V);
+  tsqr_setup_kernel<<<1, 32, 0, st>>>(jb, P, ld, m, Tt, X1, rows1, S1, rows1, tau, V, Tout, Z); ttb_count();
+  tsqr_leaf_kernel<<<ceil_div(nt, QW), QW * 32, 0, st>>>(P, ld, m, nt, jb, Tt, X1, rows1, Z, V);
   ttb_count();
   return ttb_last_error();
 }

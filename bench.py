@@ -223,38 +223,30 @@ def run_b200(args):
     fp64_peak = 2 * 8192 ** 3 / (best / 1e3) / 1e12
     del a, b
 
-    # ---------------- end-to-end: pinned host cores -> device -> matvec+round -> host cores
+    # ---------------- end-to-end: pinned host cores in, rounded host cores out, through the host
+    # entry point (uploads overlapped with the core contractions, downloads with the last core)
+    from paper_2509_13224_b200.tensor_train import tt_matvec_round_host
     hA = [G.cpu().pin_memory() for G in A.cores]
     hX = [G.cpu().pin_memory() for G in X.cores]
     hY = [torch.empty(s, dtype=torch.float64).pin_memory() for s in out_shapes]
     h2d = sum(t.numel() * 8 for t in hA + hX)
-    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor
     e2e_steps = max(1, min(args.steps, 3))
-    d2h = 0
+    hY = tt_matvec_round_host(hA, hX, EPS, out=hY)  # warm (allocator pools, pinned buffers)
+    d2h = sum(t.numel() * 8 for t in hY)
     barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(st)
     for _ in range(e2e_steps):
-        dA = TtMatrix([t.to("cuda", non_blocking=True) for t in hA])
-        dX = TtTensor([t.to("cuda", non_blocking=True) for t in hX])
-        Yd = tt_round(tt_matvec(dA, dX), EPS)
-        outs = []
-        for G, H in zip(Yd.cores, hY):
-            if tuple(G.shape) == tuple(H.shape):
-                H.copy_(G, non_blocking=True)
-                outs.append(H)
-            else:  # ranks changed (never for this seeded workload): unpinned fallback copy
-                outs.append(G.to("cpu"))
-        d2h = sum(G.numel() * 8 for G in Yd.cores)
+        hY = tt_matvec_round_host(hA, hX, EPS, out=hY)
     t1.record(st)
     torch.cuda.synchronize()
     barrier()
     e2e_ms = t0.elapsed_time(t1) / e2e_steps
     e2e_ms = max_over_ranks(e2e_ms, device="cuda")
     e2e_value = whole_job_rate(flops, e2e_ms, world) / 1e9
-    del hA, hX, outs, Yd, dA, dX
+    del hA, hX, hY
 
     traffic = None
     tf = os.path.join(ROOT, "profiles", "r1_dominant_kernel.json")

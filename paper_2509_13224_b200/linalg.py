@@ -78,13 +78,17 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
     return out
 
 
-def permute(X, perm):
-    """Materialized X.permute(perm) (row-major), by the native transpose kernel."""
+def permute(X, perm, out=None):
+    """Materialized X.permute(perm) (row-major), by the native transpose kernel (into ``out`` if given)."""
     perm = tuple(int(p) for p in perm)
-    if perm == tuple(range(X.dim())):
+    if perm == tuple(range(X.dim())) and out is None:
         return X.contiguous()
     X = X.contiguous()
-    out = empty(*[X.shape[p] for p in perm])
+    shape = [X.shape[p] for p in perm]
+    if out is None:
+        out = empty(*shape)
+    elif list(out.shape) != shape or not out.is_contiguous():
+        raise ValueError("bad permute output")
     if X.numel():
         dims = (C.c_longlong * X.dim())(*X.shape)
         pm = (C.c_int * X.dim())(*perm)
@@ -213,6 +217,13 @@ class SVDFactors:
         if self.tall:
             return gemm(self.Qt, self.UJ[:r], tA=True, tB=True)
         return self.UJ[:r].t().contiguous()
+
+    def U_rows(self, r, i0, i1, out):
+        """Rows [i0, i1) of U(r) into ``out`` ((i1 - i0) x r, row-major) -- chunked formation."""
+        if self.tall:
+            return gemm(self.Qt[:, i0:i1], self.UJ[:r], tA=True, tB=True, out=out)
+        out.copy_(self.UJ[:r, i0:i1].t())
+        return out
 
     def SVt(self, r):
         """diag(S[:r]) Vt[:r] = U[:, :r]^T X  (r x n)."""

@@ -1,0 +1,46 @@
+"""Host-memory entry point: same result as the device-resident call, transfers overlapped."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(rng, n, d, R, r):
+    Rs = [1] + [R] * (d - 1) + [1]
+    rs = [1] + [r] * (d - 1) + [1]
+    A = [rng.standard_normal((Rs[k], n, n, Rs[k + 1])) / np.sqrt(Rs[k]) for k in range(d)]
+    x = [rng.standard_normal((rs[k], n, rs[k + 1])) / np.sqrt(rs[k]) for k in range(d)]
+    return A, x
+
+
+@pytest.mark.parametrize("n,d,R,r,eps", [(48, 3, 4, 6, 1e-8), (40, 2, 3, 5, 1e-10), (24, 4, 3, 4, 1e-6),
+                                         (64, 3, 5, 7, 1e-2)])
+def test_host_matches_device(n, d, R, r, eps):
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor, tt_matvec, tt_matvec_round_host, tt_round
+    rng = np.random.default_rng(n + d)
+    A, x = _instance(rng, n, d, R, r)
+    ref = tt_round(tt_matvec(TtMatrix(A), TtTensor(x)), eps)
+    got = tt_matvec_round_host(A, x, eps, slices=3, chunks=5)
+    assert [tuple(g.shape) for g in got] == [tuple(G.shape) for G in ref.cores]
+    assert all(g.is_pinned() for g in got)
+    full = TtTensor(got).full()
+    want = ref.full()
+    assert np.abs(full - want).max() <= 1e-13 * np.abs(want).max()
+    # reuse of the output buffers
+    got2 = tt_matvec_round_host(A, x, eps, out=got)
+    assert all(a.data_ptr() == b.data_ptr() for a, b in zip(got, got2))
+    assert np.abs(TtTensor(got2).full() - want).max() <= 1e-13 * np.abs(want).max()
+
+
+def test_host_zero_and_errors():
+    from paper_2509_13224_b200.tensor_train import TtShapeError, tt_matvec_round_host
+    A = [np.zeros((1, 5, 5, 2)), np.zeros((2, 5, 5, 1))]
+    x = [np.ones((1, 5, 3)), np.ones((3, 5, 1))]
+    got = tt_matvec_round_host(A, x, 1e-8)
+    assert [tuple(g.shape) for g in got] == [(1, 5, 1), (1, 5, 1)] and all(float(g.abs().max()) == 0 for g in got)
+    with pytest.raises(TtShapeError):
+        tt_matvec_round_host(A, [np.ones((1, 4, 3)), np.ones((3, 5, 1))], 1e-8)
+    with pytest.raises(ValueError):
+        tt_matvec_round_host(A, x, 0.0)

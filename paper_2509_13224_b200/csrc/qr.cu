@@ -305,20 +305,78 @@ namespace {
 
 constexpr int NB2 = 128;  // outer WY block (trailing-update GEMMs have K = 128)
 
-// T (nb x nb row-major, upper) from the Gram G = V^T V (row-major ld ldg) and tau (dlarft, forward, columnwise)
+// T (nb x nb row-major, upper, nb <= NB) from the Gram G = V^T V (upper triangle read, row-major
+// ld ldg) and tau (dlarft, forward, columnwise); staged in shared memory.
 __global__ void larft_kernel(int nb, const double* G, int ldg, const double* tau, double* T) {
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = 0.0;
+  __shared__ double Ts[NB][NB + 1], Gs[NB][NB + 1];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    Ts[r][c] = 0.0;
+    Gs[r][c] = (r < nb && c < nb && r <= c) ? G[(long long)r * ldg + c] : 0.0;
+  }
   __syncthreads();
   for (int i = 0; i < nb; ++i) {
     const double ti = tau[i];
-    if (threadIdx.x == 0) T[i * nb + i] = ti;
+    if (threadIdx.x == 0) Ts[i][i] = ti;
     for (int r = threadIdx.x; r < i; r += blockDim.x) {
       double v = 0.0;
-      for (int c = r; c < i; ++c) v += T[r * nb + c] * G[(long long)c * ldg + i];
-      T[r * nb + i] = -ti * v;
+      for (int c = r; c < i; ++c) v += Ts[r][c] * Gs[c][i];
+      Ts[r][i] = -ti * v;
     }
     __syncthreads();
   }
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = Ts[e / nb][e % nb];
+}
+
+// Outer-block T (JB x JB row-major) from the inner panels' T factors (NB x NB each, row-major ld
+// jb_p, at Tin + p NB NB) and the outer Gram G (row-major ld ldg) by block merges:
+// T[0:c0, c0:c0+jb] = -T[0:c0, 0:c0] (G[0:c0, c0:c0+jb] T_pp)   (I - V1 T1 V1^T)(I - V2 T2 V2^T)
+constexpr int LBT = 256;
+__global__ void __launch_bounds__(LBT) larft_block_kernel(int JB, const double* __restrict__ G, int ldg,
+                                                           const double* __restrict__ Tin, double* T) {
+  extern __shared__ double sm[];
+  const int LDT = JB + 1;
+  double* Ts = sm;                       // JB x LDT
+  double* Ps = sm + (long long)JB * LDT; // JB x NB
+  for (int e = threadIdx.x; e < JB * LDT; e += LBT) Ts[e] = 0.0;
+  __syncthreads();
+  const int np = (JB + NB - 1) / NB;
+  for (int p = 0; p < np; ++p) {
+    const int c0 = p * NB, jb = min(NB, JB - c0);
+    const double* Tp = Tin + (long long)p * NB * NB;
+    for (int e = threadIdx.x; e < jb * jb; e += LBT) Ts[(c0 + e / jb) * LDT + c0 + e % jb] = Tp[e];
+  }
+  __syncthreads();
+  for (int p = 1; p < np; ++p) {
+    const int c0 = p * NB, jb = min(NB, JB - c0);
+    const double* Tp = Ts + (long long)c0 * LDT + c0;
+    for (int e = threadIdx.x; e < c0 * jb; e += LBT) {  // P = G[0:c0, c0:c0+jb] T_pp (T_pp upper)
+      const int r = e / jb, c = e % jb;
+      double acc = 0.0;
+      for (int b = 0; b <= c; ++b) acc += G[(long long)r * ldg + c0 + b] * Tp[b * LDT + c];
+      Ps[r * NB + c] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < c0 * jb; e += LBT) {  // T[0:c0, c0:] = -T[0:c0, 0:c0] P
+      const int r = e / jb, c = e % jb;
+      double acc = 0.0;
+      for (int b = r; b < c0; ++b) acc += Ts[r * LDT + b] * Ps[b * NB + c];
+      Ts[r * LDT + c0 + c] = -acc;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < JB * JB; e += LBT) T[e] = Ts[(e / JB) * LDT + e % JB];
+}
+
+int launch_larft_block(int JB, const double* G, int ldg, const double* Tin, double* T, cudaStream_t st) {
+  const size_t smem = ((size_t)JB * (JB + 1) + (size_t)JB * NB) * sizeof(double);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(larft_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cfg = true;
+  }
+  larft_block_kernel<<<1, LBT, smem, st>>>(JB, G, ldg, Tin, T); ttb_count();
+  return ttb_last_error();
 }
 
 // G (nb x nb row-major, nb <= NB) = V^T V for a tall col-major V (m x nb, ld m): every CTA
@@ -411,6 +469,32 @@ int apply_wy(void* stream, int mp, int nq, int jb, const double* V, const double
   return ttb_dgemm(stream, 0, 0, nq, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, C, ldc, 0, 1);
 }
 
+// Same update with V read in place from the factored panel Ap (col-major, ld lda): rows >= jb of V
+// are the stored reflector entries; only the unit-lower top jb x jb block (Vtop, ld jb) is explicit.
+int apply_wy_panel(void* stream, int mp, int nq, int jb, const double* Ap, long long lda, const double* Vtop,
+                   const double* T, int transT, double* C, long long ldc, double* W, double* W2) {
+  const int mb = mp - jb;
+  int rc = 0;
+  if (mb > 0) rc = ttb_dgemm(stream, 0, 1, nq, jb, mb, 1.0, C + jb, ldc, 0, Ap + jb, lda, 0, 0.0, W, jb, 0, 1);
+  if (rc) return rc;
+  rc = ttb_dgemm(stream, 0, 1, nq, jb, jb, 1.0, C, ldc, 0, Vtop, jb, 0, mb > 0 ? 1.0 : 0.0, W, jb, 0, 1);
+  if (rc) return rc;
+  rc = ttb_dgemm(stream, 0, transT ? 0 : 1, nq, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
+  if (rc) return rc;
+  rc = ttb_dgemm(stream, 0, 0, nq, jb, jb, -1.0, W2, jb, 0, Vtop, jb, 0, 1.0, C, ldc, 0, 1);
+  if (rc || mb <= 0) return rc;
+  return ttb_dgemm(stream, 0, 0, nq, mb, jb, -1.0, W2, jb, 0, Ap + jb, lda, 0, 1.0, C + jb, ldc, 0, 1);
+}
+
+// G = V^T V for the in-place reflectors of apply_wy_panel
+int gram_panel(void* stream, int mp, int jb, const double* Ap, long long lda, const double* Vtop, double* G) {
+  const int mb = mp - jb;
+  int rc = 0;
+  if (mb > 0) rc = ttb_dgemm(stream, 0, 1, jb, jb, mb, 1.0, Ap + jb, lda, 0, Ap + jb, lda, 0, 0.0, G, jb, 0, 1);
+  if (rc) return rc;
+  return ttb_dgemm(stream, 0, 1, jb, jb, jb, 1.0, Vtop, jb, 0, Vtop, jb, 0, mb > 0 ? 1.0 : 0.0, G, jb, 0, 1);
+}
+
 }  // namespace
 
 // Householder panel with dgeqr2 + dlarft outputs (single-CTA kernel when it fits shared memory,
@@ -484,13 +568,16 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
                       cudaMemcpyDeviceToDevice, st);
       continue;
     }
-    extract_v_kernel<<<grid_v((long long)MP * JB), 256, 0, st>>>(MP, JB, A + (long long)J0 * lda + J0, lda, w.Vb); ttb_count();
-    int rc = ttb_dgemm(stream, 0, 1, JB, JB, MP, 1.0, w.Vb, MP, 0, w.Vb, MP, 0, 0.0, w.G, JB, 0, 1);
+    const double* Ap = A + (long long)J0 * lda + J0;
+    extract_v_kernel<<<grid_v((long long)JB * JB), 256, 0, st>>>(JB, JB, Ap, lda, w.Vb); ttb_count();  // Vtop
+    int rc = gram_panel(stream, MP, JB, Ap, lda, w.Vb, w.G);
     if (rc) return rc;
-    larft_kernel<<<1, 128, 0, st>>>(JB, w.G, JB, tau + J0, Tb); ttb_count();
+    rc = launch_larft_block(JB, w.G, JB, w.Tin + (long long)(J0 / NB) * NB * NB, Tb, st);
+    if (rc) return rc;
     const int n2 = n - J0 - JB;
     if (n2 > 0) {
-      rc = apply_wy(stream, MP, n2, JB, w.Vb, Tb, 1, A + (long long)(J0 + JB) * lda + J0, lda, w.W, w.W2);
+      rc = apply_wy_panel(stream, MP, n2, JB, Ap, lda, w.Vb, Tb, 1, A + (long long)(J0 + JB) * lda + J0, lda, w.W,
+                          w.W2);
       if (rc) return rc;
     }
   }
@@ -512,8 +599,9 @@ TTB_API int ttb_orgqr(void* stream, int m, int kq, int kf, const double* A, long
     const int nq = kq - J0;
     if (nq <= 0) continue;
     double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
-    extract_v_kernel<<<grid_v((long long)MP * JB), 256, 0, st>>>(MP, JB, A + (long long)J0 * lda + J0, lda, w.Vb); ttb_count();
-    int rc = apply_wy(stream, MP, nq, JB, w.Vb, Tb, 0, Q + (long long)J0 * ldq + J0, ldq, w.W, w.W2);
+    const double* Ap = A + (long long)J0 * lda + J0;
+    extract_v_kernel<<<grid_v((long long)JB * JB), 256, 0, st>>>(JB, JB, Ap, lda, w.Vb); ttb_count();  // Vtop
+    int rc = apply_wy_panel(stream, MP, nq, JB, Ap, lda, w.Vb, Tb, 0, Q + (long long)J0 * ldq + J0, ldq, w.W, w.W2);
     if (rc) return rc;
   }
   return ttb_last_error();

@@ -5,6 +5,7 @@
 // (mma.sync m8n8k4 .f64 -> SASS DMMA) from shared-memory tiles filled with
 // cp.async (LDGSTS) in a two-stage pipeline.
 #include "common.cuh"
+#include <stdlib.h>
 
 long long g_ttb_launches = 0;
 
@@ -258,6 +259,164 @@ int launch_gemm(const GemmArgs& g, int batch, cudaStream_t st) {
   }
 }
 
+// C += alpha A B for a long, short-K product (WY trailing updates: M <= ~1024 rows of C_rm,
+// K <= 128, N ~ 1e6; alpha = +-1, beta = 1). Persistent CTAs: each keeps its 64 x K block of A
+// resident in shared memory and walks N tiles of WU_BN columns; B flows through a WU_S-stage ring
+// of WU_KC-deep k-chunks (cp.async), continuous across tiles, and the next C tile is prefetched
+// into registers while the current one is multiplied. 2 x WN warps.
+constexpr int WU_BM = 64, WU_KMAX = 128;
+constexpr int WU_LDA = WU_KMAX + 4;
+
+template <int WU_BN, int WU_KC, int WU_S, int WN>
+__global__ void __launch_bounds__(64 * WN, 1) wy_update_kernel(int M, int N, int K, double alpha, const double* __restrict__ A,
+                                                            long long lda, const double* __restrict__ B, long long ldb,
+                                                            double* C, long long ldc) {
+  constexpr int WU_LDB = WU_BN + 8;
+  constexpr int WU_T = 64 * WN;  // 2 x WN warps
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;                        // [WU_BM][WU_LDA]
+  double* Bs = sm + WU_BM * WU_LDA;       // [WU_S][WU_KC][WU_LDB]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int bm0 = blockIdx.x * WU_BM;
+  const int ntn = (N + WU_BN - 1) / WU_BN;
+  constexpr int WNC = WU_BN / WN;  // warp tile columns
+  const int nkc = (K + WU_KC - 1) / WU_KC;  // k-chunks per tile
+  for (int e = tid; e < WU_BM * (WU_KMAX / 2); e += WU_T) {
+    const int m = e / (WU_KMAX / 2), k = (e % (WU_KMAX / 2)) * 2;
+    const int gm = bm0 + m;
+    const int avail = (gm < M) ? max(0, min(2, K - k)) : 0;
+    cp_async16(As + m * WU_LDA + k, avail ? A + (long long)gm * lda + k : A, avail * 8);
+  }
+  // my tiles: tn = blockIdx.y + i * gridDim.y; global chunk g -> (tile i = g / nkc, chunk g % nkc)
+  const int my_tiles = (ntn - (int)blockIdx.y + (int)gridDim.y - 1) / (int)gridDim.y;
+  const int nchunks = my_tiles > 0 ? my_tiles * nkc : 0;
+  auto load_chunk = [&](int g) {
+    if (g < nchunks) {
+      const int tn = blockIdx.y + (g / nkc) * gridDim.y, kc = g % nkc;
+      double* bs = Bs + (g % WU_S) * (WU_KC * WU_LDB);
+      const int bn0 = tn * WU_BN, k0 = kc * WU_KC;
+#pragma unroll
+      for (int e0 = 0; e0 < WU_KC * (WU_BN / 2); e0 += WU_T) {
+        const int e = e0 + tid;
+        const int k = e / (WU_BN / 2), n = (e % (WU_BN / 2)) * 2;
+        const int gn = bn0 + n, gk = k0 + k;
+        const int avail = (gk < K) ? max(0, min(2, N - gn)) : 0;
+        cp_async16(bs + k * WU_LDB + n, avail ? B + (long long)gk * ldb + gn : B, avail * 8);
+      }
+    }
+    cp_async_commit();
+  };
+  constexpr int MT = 4, NT = WNC / 8;
+  auto load_c = [&](int tn, double (&c)[MT][NT][2]) {
+    const int bn0 = tn * WU_BN;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int m = bm0 + wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = bn0 + wn * WNC + j * 8 + (lane & 3) * 2;
+        if (m < M && n + 1 < N) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(C + (long long)m * ldc + n));
+          c[i][j][0] = v.x; c[i][j][1] = v.y;
+        } else {
+          c[i][j][0] = (m < M && n < N) ? C[(long long)m * ldc + n] : 0.0;
+          c[i][j][1] = 0.0;
+        }
+      }
+    }
+  };
+  // prologue: A block + chunks 0 .. S-2 (A rides in the first group)
+  load_chunk(0);
+#pragma unroll
+  for (int g = 1; g < WU_S - 1; ++g) load_chunk(g);
+  double cn[MT][NT][2], acc[MT][NT][2];
+  if (my_tiles > 0) load_c(blockIdx.y, cn);
+  for (int g = 0; g < nchunks; ++g) {
+    const int kc = g % nkc;
+    const int tn = blockIdx.y + (g / nkc) * gridDim.y;
+    cp_async_wait<WU_S - 2>();
+    __syncthreads();
+    load_chunk(g + WU_S - 1);
+    if (kc == 0) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          acc[i][j][0] = alpha * cn[i][j][0];  // exact for alpha = +-1: result = alpha (alpha C + A B)
+          acc[i][j][1] = alpha * cn[i][j][1];
+        }
+      const int tnext = tn + gridDim.y;
+      if (tnext < ntn) load_c(tnext, cn);
+    }
+    const double* bs = Bs + (g % WU_S) * (WU_KC * WU_LDB);
+    // 16-deep steps (zero-filled beyond K): all fragments of a step are loaded before its MMAs
+    const int kend = min(WU_KC, ((K + 15) & ~15) - kc * WU_KC);
+    const double* as = As + (wm * 32 + (lane >> 2)) * WU_LDA + kc * WU_KC + (lane & 3);
+    const double* bsl = bs + (lane & 3) * WU_LDB + wn * WNC + (lane >> 2);
+    for (int kb = 0; kb < kend; kb += 16) {
+      double af[4][MT], bf[4][NT];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i) af[q][i] = as[i * 8 * WU_LDA + kb + 4 * q];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) bf[q][j] = bsl[(kb + 4 * q) * WU_LDB + j * 8];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[q][i], bf[q][j]);
+    }
+    if (kc == nkc - 1) {
+      const int bn0 = tn * WU_BN;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int m = bm0 + wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int n = bn0 + wn * WNC + j * 8 + (lane & 3) * 2;
+          const double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+          if (m < M && n + 1 < N) {
+            __stcs(reinterpret_cast<double2*>(C + (long long)m * ldc + n), make_double2(v0, v1));
+          } else if (m < M && n < N) {
+            C[(long long)m * ldc + n] = v0;
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int BN, int KC, int S, int WN>
+int launch_wy_update_t(int M, int N, int K, double alpha, const double* A, long long lda, const double* B, long long ldb,
+                       double* C, long long ldc, cudaStream_t st) {
+  const size_t smem = (size_t)(WU_BM * WU_LDA + S * KC * (BN + 8)) * sizeof(double);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(wy_update_kernel<BN, KC, S, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cfg = true;
+  }
+  const int mt = (M + WU_BM - 1) / WU_BM;
+  const int ntn = (N + BN - 1) / BN;
+  int gy = 148 / mt;
+  if (gy < 1) gy = 1;
+  if (gy > ntn) gy = ntn;
+  wy_update_kernel<BN, KC, S, WN><<<dim3(mt, gy), 64 * WN, smem, st>>>(M, N, K, alpha, A, lda, B, ldb, C, ldc);
+  ttb_count();
+  return ttb_last_error();
+}
+
+int launch_wy_update(int M, int N, int K, double alpha, const double* A, long long lda, const double* B, long long ldb,
+                     double* C, long long ldc, cudaStream_t st) {
+  // 64 x 64 tiles, whole-K B tiles double-buffered, 2 x 4 warps (measured best of the
+  // 128-wide / k-chunk-ring / 4-warp variants on the 896 x 1M x 128 update)
+  return launch_wy_update_t<64, 128, 2, 4>(M, N, K, alpha, A, lda, B, ldb, C, ldc, st);
+}
+
 __global__ void scale_kernel(long long n, double beta, double* C, long long ldc, int M, int N, long long sC) {
   // C = beta*C over an M x N (row-major, ldc) block per batch (used when K == 0)
   long long b = blockIdx.y;
@@ -315,6 +474,16 @@ __global__ void splitk_reduce(int M, int N, int S, const double* __restrict__ pa
     if (beta != 0.0) v += beta * *c;
     *c = v;
   }
+}
+
+// TTB_WY=legacy keeps the short-K updates on the tiled GEMM (A/B testing)
+bool wy_legacy() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TTB_WY");
+    v = (e && e[0] == 'l') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 double* g_scratch = nullptr;
@@ -458,6 +627,9 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
       return ttb_last_error();
     }
   }
+  if (!tA && !tB && batch == 1 && K <= WU_KMAX && N >= 8192 && M >= 32 && beta == 1.0 && cinit &&
+      !wy_legacy() && ((lda | ldb | ldc) & 1) == 0 && ((((uintptr_t)A) | ((uintptr_t)B) | ((uintptr_t)C)) & 15) == 0)
+    return launch_wy_update(M, N, K, alpha, A, lda, B, ldb, C, ldc, st);
   // short-K updates of a long C (WY trailing updates): 128x64 tiles, ~120 registers -> 2 CTAs/SM so
   // one CTA's epilogue read-modify-write overlaps the other's main loop
   if (big && K <= 256 && N >= 4096)

@@ -31,6 +31,21 @@ def test_gemm(la, M, N, K, tA, tB):
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
 
 
+@pytest.mark.parametrize("M,N,K", [(32, 8192, 128), (37, 9001, 16), (128, 20000, 128), (300, 16387, 100),
+                                   (896, 40000, 128), (64, 8193, 7)])
+@pytest.mark.parametrize("alpha", [-1.0, 1.0])
+def test_gemm_short_k_update(la, M, N, K, alpha):
+    # C += alpha A B with beta = 1 (the WY trailing-update shape; resident-A persistent kernel)
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    C0 = rng.standard_normal((M, N))
+    ref = C0 + alpha * (A @ B)
+    out = T(C0)
+    la.gemm(T(A), T(B), alpha=alpha, beta=1.0, out=out)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
+
+
 def test_permute_and_tdot(la):
     rng = np.random.default_rng(1)
     X = rng.standard_normal((3, 4, 5, 6))

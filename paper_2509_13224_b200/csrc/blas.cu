@@ -427,25 +427,30 @@ __global__ void scale_kernel(long long n, double beta, double* C, long long ldc,
   }
 }
 
-// C[r, c] = alpha * sum_k A[r, k] B[k, c] + beta * C[r, c] for small K: each CTA owns 256 columns,
-// keeps B[:, tile] in shared memory and streams the rows of C once (coalesced read-modify-write).
+// C[r, c] = alpha * sum_k A[r, k] B[k, c] + beta * C[r, c] for small K (<= 32): every thread owns one
+// column c of C and keeps B[:, c] in registers; the rows of A are staged in shared memory and read
+// as broadcasts (one LDS.128 per two k), so the pass is bound by streaming C once through HBM.
+template <int KT>
 __global__ void __launch_bounds__(128) lowrank_update_kernel(int M, int N, int K, double alpha,
                                                              const double* __restrict__ A, long long lda,
                                                              const double* __restrict__ B, long long ldb,
                                                              double beta, double* C, long long ldc) {
-  __shared__ double Bs[32][128];
-  __shared__ double As[32][33];
-  const int c0 = blockIdx.x * 128;
-  const int c = c0 + threadIdx.x;
-  for (int k = 0; k < K; ++k) Bs[k][threadIdx.x] = (c < N) ? B[(long long)k * ldb + c] : 0.0;
-  for (int r0 = 0; r0 < M; r0 += 32) {
-    const int rn = min(32, M - r0);
+  constexpr int RB = 32;  // rows of A staged per round
+  __shared__ __align__(16) double As[RB][KT];
+  const int c = blockIdx.x * 128 + threadIdx.x;
+  double bk[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) bk[k] = (c < N && k < K) ? B[(long long)k * ldb + c] : 0.0;
+  for (int r0 = 0; r0 < M; r0 += RB) {
+    const int rn = min(RB, M - r0);
     __syncthreads();
-    for (int e = threadIdx.x; e < rn * K; e += 128) As[e / K][e % K] = A[(long long)(r0 + e / K) * lda + (e % K)];
+    for (int e = threadIdx.x; e < RB * KT; e += 128) {
+      const int r = e / KT, k = e % KT;
+      As[r][k] = (r < rn && k < K) ? A[(long long)(r0 + r) * lda + k] : 0.0;
+    }
     __syncthreads();
     if (c < N) {
-      // 8 rows at a time: issue the 8 independent loads of C first (memory-level parallelism)
-      for (int rr0 = 0; rr0 < rn; rr0 += 8) {
+      for (int rr0 = 0; rr0 < rn; rr0 += 8) {  // 8 independent loads of C in flight
         double cv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -453,8 +458,13 @@ __global__ void __launch_bounds__(128) lowrank_update_kernel(int M, int N, int K
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (rr0 + u < rn) {
+            const double2* ar = reinterpret_cast<const double2*>(As[rr0 + u]);
             double acc = 0.0;
-            for (int k = 0; k < K; ++k) acc += As[rr0 + u][k] * Bs[k][threadIdx.x];
+#pragma unroll
+            for (int k2 = 0; k2 < KT / 2; ++k2) {
+              const double2 av = ar[k2];
+              acc += av.x * bk[2 * k2] + av.y * bk[2 * k2 + 1];
+            }
             C[(long long)(r0 + rr0 + u) * ldc + c] = alpha * acc + beta * cv[u];
           }
         }
@@ -592,7 +602,11 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
   if (!tA && !tB && batch == 1 && K <= 32 && N >= 2048) {
     // low-rank update of a long matrix (WY panel updates): memory-bound, one coalesced RMW pass
     dim3 grid(ceil_div(N, 128));
-    lowrank_update_kernel<<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc); ttb_count();
+    if (K <= 16)
+      lowrank_update_kernel<16><<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else
+      lowrank_update_kernel<32><<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    ttb_count();
     return ttb_last_error();
   }
   GemmArgs g{M, N, K, alpha, beta, A, lda, sA, tA, B, ldb, sB, tB, C, ldc, sC, 0, 0};

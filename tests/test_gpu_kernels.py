@@ -110,6 +110,19 @@ def test_svd(la, m, n):
     assert np.all(np.diff(S) <= 0)
 
 
+@pytest.mark.parametrize("M,N,K,alpha,beta", [(50, 5000, 16, -0.7, 1.3), (7, 3001, 20, 2.0, 0.0), (100, 2048, 3, 1.0, -1.0),
+                                               (33, 70001, 32, -1.0, 1.0)])
+def test_gemm_lowrank_update(la, M, N, K, alpha, beta):
+    rng = np.random.default_rng(M * N + K)
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    C0 = rng.standard_normal((M, N))
+    ref = beta * C0 + alpha * (A @ B)
+    out = T(C0)
+    la.gemm(T(A), T(B), alpha=alpha, beta=beta, out=out)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
+
+
 def test_svd_graded_and_degenerate(la):
     # graded singular values down to 1e-14 (relative accuracy of the one-sided Jacobi on R),
     # repeated singular values and exact rank deficiency, on the multi-CTA Jacobi sizes

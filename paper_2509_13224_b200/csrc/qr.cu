@@ -282,7 +282,134 @@ __global__ void __launch_bounds__(SPT) panel_small_kernel(int m, int jb, double*
 
 bool panel_is_small(int m, int jb) { return (long long)m * jb <= kSmallPanel; }
 
+// Register-resident single-CTA panel (m <= CPT * CRPT rows): thread t holds rows t + CPT s. One
+// batched reduction per column (the look-ahead statistics of tsqr.cu: z_c = x^T A[:, c] with
+// x = A[j+1:, j], giving the reflector application and the dlarft column), two barriers per column.
+constexpr int CPT = 256, CRPT = 5;
+template <int JB>
+__global__ void __launch_bounds__(CPT, 1) panel_cta_kernel(int m, int jb_rt, double* P, long long ld, double* tau,
+                                                           double* V, double* T) {
+  __shared__ double red[CPT / 32][NB];
+  __shared__ double zf[NB];
+  __shared__ double rowb[2][NB];
+  __shared__ double Ts[NB][NB + 1];
+  const int jb = JB ? JB : jb_rt;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  double a[CRPT][NB];
+#pragma unroll
+  for (int s = 0; s < CRPT; ++s) {
+    const int i = t + CPT * s;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[s][c] = (i < m && c < jb) ? P[(long long)c * ld + i] : 0.0;
+  }
+  for (int e = t; e < NB * (NB + 1); e += CPT) (&Ts[0][0])[e] = 0.0;
+  auto stats = [&](int col, int buf) {  // z_c = sum_{i > col} A[i, col] A[i, c]; row col -> rowb[buf]
+    double z[NB];
+    double x[CRPT];
+#pragma unroll
+    for (int s = 0; s < CRPT; ++s) {
+      const int i = t + CPT * s;
+      double xv = 0.0;
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c == col) xv = a[s][c];
+      x[s] = (i > col && i < m) ? xv : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      z[c] = 0.0;
+#pragma unroll
+      for (int s = 0; s < CRPT; ++s) z[c] += x[s] * a[s][c];
+    }
+    warp_allreduce16(z, lane);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) red[w][c] = z[c];
+    if (t == col)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) rowb[buf][c] = a[0][c];
+    __syncthreads();
+    if (t < NB) {
+      double v = 0.0;
+      for (int q = 0; q < CPT / 32; ++q) v += red[q][t];
+      zf[t] = v;
+    }
+    __syncthreads();
+  };
+  stats(0, 0);
+  for (int j = 0; j < jb; ++j) {
+    double rowj[NB], zj[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) { rowj[c] = rowb[j & 1][c]; zj[c] = zf[c]; }
+    double alpha = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+      if (c == j) { alpha = rowj[c]; s2 = zj[c]; }
+    double beta, tj, scal;
+    if (s2 == 0.0) {
+      beta = alpha; tj = 0.0; scal = 0.0;
+    } else {
+      const double nrm = sqrt(alpha * alpha + s2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    double wv[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) wv[c] = rowj[c] + scal * zj[c];
+    if (t < j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (b >= t && b < j) acc += Ts[t][b] * wv[b];
+      Ts[t][j] = -tj * acc;
+    }
+    if (t == 0) Ts[j][j] = tj;
+#pragma unroll
+    for (int s = 0; s < CRPT; ++s) {
+      const int i = t + CPT * s;
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        if (c == j) {
+          const double vi = (i > j && i < m) ? a[s][c] * scal : (i == j ? 1.0 : 0.0);
+          if (i > j) a[s][c] = vi;
+          const double tv = tj * vi;
+#pragma unroll
+          for (int c2 = 0; c2 < NB; ++c2)
+            if (c2 > c) a[s][c2] -= tv * wv[c2];
+        }
+      }
+    }
+    if (t == j)
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c == j) a[0][c] = beta;
+    if (j + 1 < jb) stats(j + 1, (j + 1) & 1);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < CRPT; ++s) {
+    const int i = t + CPT * s;
+    if (i < m)
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c < jb) {
+          P[(long long)c * ld + i] = a[s][c];
+          V[(long long)c * m + i] = (i < c) ? 0.0 : (i == c ? 1.0 : a[s][c]);
+        }
+  }
+  for (int e = t; e < jb * jb; e += CPT) T[e] = Ts[e / jb][e % jb];
+  if (t < jb) tau[t] = Ts[t][t];
+}
+
 int launch_panel_small(int m, int jb, double* P, long long ld, double* tau, double* V, double* T, cudaStream_t st) {
+  static int legacy = getenv("TTB_PANEL_SMALL") ? 1 : 0;
+  if (!legacy && m <= CPT * CRPT && jb <= NB) {
+    if (jb == NB) panel_cta_kernel<NB><<<1, CPT, 0, st>>>(m, jb, P, ld, tau, V, T);
+    else panel_cta_kernel<0><<<1, CPT, 0, st>>>(m, jb, P, ld, tau, V, T);
+    ttb_count();
+    return ttb_last_error();
+  }
   static bool cfg = false;
   if (!cfg) {
     cudaFuncSetAttribute(panel_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallPanel * 8);

@@ -44,49 +44,6 @@ __device__ __forceinline__ void load_tile(double (&a)[TS][NB], const double* M, 
     }
 }
 
-// Warp all-reduce of 16 values: reduce-scatter over lane bits 4..1 (lane l ends with the sum of
-// index l >> 1), a final exchange over bit 0, then an all-gather: 64 shuffles instead of 160.
-__device__ __forceinline__ void warp_allreduce16(double (&z)[NB], int lane) {
-  double v8[8], v4[4], v2[2];
-  {
-    const bool hi = lane & 16;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double send = hi ? z[k] : z[k + 8];
-      const double keep = hi ? z[k + 8] : z[k];
-      v8[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-  }
-  {
-    const bool hi = lane & 8;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double send = hi ? v8[k] : v8[k + 4];
-      const double keep = hi ? v8[k + 4] : v8[k];
-      v4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-  }
-  {
-    const bool hi = lane & 4;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const double send = hi ? v4[k] : v4[k + 2];
-      const double keep = hi ? v4[k + 2] : v4[k];
-      v2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-  }
-  double v;
-  {
-    const bool hi = lane & 2;
-    const double send = hi ? v2[0] : v2[1];
-    const double keep = hi ? v2[1] : v2[0];
-    v = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  v += __shfl_xor_sync(0xffffffffu, v, 1);  // lane l: full sum of index l >> 1
-#pragma unroll
-  for (int c = 0; c < NB; ++c) z[c] = __shfl_sync(0xffffffffu, v, 2 * c);
-}
-
 // Householder QR of every tile of an (rows x jb) col-major matrix M (in place: R on/above the
 // diagonal, V below), T per tile (NB x NB row-major) and the tile's R into rows [t jb, t jb + jb)
 // of S (col-major, ld ldS). JB > 0: compile-time panel width. Columns >= jb are zero.

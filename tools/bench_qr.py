@@ -15,7 +15,7 @@ def timed(fn, reps=3):
     return best
 
 
-for m, n in ((1 << 20, 1024), (1 << 18, 1024), (1 << 20, 256), (4096, 1024)):
+for m, n in ((1 << 20, 1024), (1 << 18, 1024), (1 << 20, 256), (4096, 1024), (1024, 1024)):
     X = torch.randn(n, m, dtype=torch.float64, device="cuda")  # col-major m x n
     k = min(m, n)
     fl = 2.0 * m * n * k - 2.0 / 3.0 * k ** 3

@@ -17,7 +17,10 @@ TTB_API long long ttb_launch_count(int reset) {
 
 namespace {
 
-constexpr int BK = 16;
+constexpr int kKcAlign = 32;  // split-K chunk alignment (multiple of every tile depth)
+// tile depth: 32 for the 128 x 128 tiles (fewer barriers per K; measured +4%), 16 elsewhere
+template <int BM, int BN>
+constexpr int tile_bk() { return (BM == 128 && BN == 128) ? 32 : 16; }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -62,6 +65,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
 template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC, int STAGES, int CI>
 __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(GemmArgs g) {
   constexpr int T = WM * WN * 32;
+  constexpr int BK = tile_bk<BM, BN>();
   constexpr int ASZ = TA ? BK * (BM + 8) : BM * (BK + 4);
   constexpr int BSZ = TB ? BN * (BK + 4) : BK * (BN + 8);
   constexpr int MT = BM / WM / 8, NT = BN / WN / 8;
@@ -226,6 +230,7 @@ template <int BM, int BN, int WM, int WN, int TA, int TB, int VEC, int CI>
 int launch_gemm_t(const GemmArgs& g, int batch, cudaStream_t st) {
   constexpr int STAGES = 3;
   constexpr int T = WM * WN * 32;
+  constexpr int BK = tile_bk<BM, BN>();
   constexpr int ASZ = TA ? BK * (BM + 8) : BM * (BK + 4);
   constexpr int BSZ = TB ? BN * (BK + 4) : BK * (BN + 8);
   const size_t smem = (size_t)STAGES * (ASZ + BSZ) * sizeof(double);
@@ -625,7 +630,7 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
     long long maxS = K / 256;
     if (S > maxS) S = maxS;
     if (S > 1) {
-      int Kc = (int)(((K + S - 1) / S + BK - 1) / BK * BK);
+      int Kc = (int)(((K + S - 1) / S + kKcAlign - 1) / kKcAlign * kKcAlign);
       S = (K + Kc - 1) / Kc;
       double* part = scratch((size_t)S * M * N * sizeof(double));
       if (!part) return (int)cudaErrorMemoryAllocation;

@@ -481,6 +481,151 @@ __global__ void __launch_bounds__(256) band_chol_solve_kernel(long long N, int b
   }
 }
 
+// Blocked banded Cholesky + solves in one CTA with a shared-memory window (bw <= 127, N <= 8192).
+// Storage as band_chol_solve_kernel: LB[i*W + q] = A[i][i-q], W = bw + 1. The window holds rows
+// [k0, k0 + NBB + bw) plus the NBB rows of the next block, prefetched while the current block is
+// processed (circular, WRC = 2 NBB + bw slots); per block of NBB columns: warp 0 factors the panel,
+// all warps apply the rank-NBB update of the band triangle, finished rows stream out. Solves
+// stream rows through staged chunks; b lives in shared memory; the forward solve takes blocks of
+// NBB rows (band dots in parallel over warps, then the NBB x NBB triangle).
+constexpr int BCT = 256, NBB = 8, BCH = 64;
+
+__global__ void __launch_bounds__(BCT) band_chol_blocked_kernel(int N, int bw, double* LB, double* b, int* info) {
+  extern __shared__ double sm[];
+  const int W = bw + 1;
+  const int WRC = 2 * NBB + bw;
+  const int WROWS = max(WRC, BCH);
+  double* win = sm;                               // WRC x W (factorization) / BCH x W (solves)
+  double* bs = sm + (long long)WROWS * W;         // N
+  __shared__ int bad;
+  __shared__ double dot[NBB], rinv[BCH];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { bad = 0; *info = 0; }
+  auto row = [&](int i) { return win + (long long)(i % WRC) * W; };
+  // rows [0, NBB + bw) now, rows [NBB + bw, 2 NBB + bw) as the prefetch of block 1
+  const int r0n = min(N, WRC);
+  for (int e = tid; e < r0n * W; e += BCT) win[e] = LB[e];
+  __syncthreads();
+  for (int k0 = 0; k0 < N; k0 += NBB) {
+    const int nb = min(NBB, N - k0);
+    asm volatile("cp.async.wait_group 1;\n" ::);  // rows prefetched two blocks ago have landed
+    __syncthreads();
+    if (warp == 0) {
+      for (int c = k0; c < k0 + nb; ++c) {
+        double* rc = row(c);
+        const double d = rc[0];
+        if (!(d > 0.0) || !isfinite(d)) {
+          if (lane == 0) { bad = 1; *info = c + 1; }
+          break;
+        }
+        const double l = sqrt(d), il = 1.0 / l;
+        const int iend = min(N - 1, c + bw);
+        for (int i = c + 1 + lane; i <= iend; i += 32) row(i)[i - c] *= il;
+        __syncwarp();
+        if (lane == 0) rc[0] = l;
+        for (int c2 = c + 1; c2 < k0 + nb; ++c2) {
+          const double lc2 = row(c2)[c2 - c];
+          for (int i = c2 + lane; i <= iend; i += 32) row(i)[i - c2] -= row(i)[i - c] * lc2;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (bad) return;
+    const int ib = k0 + nb, ie = min(N - 1, k0 + nb - 1 + bw);
+    for (int i = ib + warp; i <= ie; i += BCT / 32) {
+      double* ri = row(i);
+      double li[NBB];
+      const int cmin = max(k0, i - bw);
+#pragma unroll
+      for (int t = 0; t < NBB; ++t) {
+        const int c = k0 + t;
+        li[t] = (t < nb && c >= cmin) ? ri[i - c] : 0.0;
+      }
+      for (int j = max(ib, i - bw) + lane; j <= i; j += 32) {
+        const double* rj = row(j);
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < NBB; ++t) {
+          const int c = k0 + t;
+          if (t < nb && c >= cmin) acc += li[t] * rj[j - c];
+        }
+        ri[i - j] -= acc;
+      }
+    }
+    __syncthreads();
+    // finished rows out; their slots take the rows of block + 2 (prefetch one block ahead)
+    for (int e = tid; e < nb * W; e += BCT) {
+      const int t = e / W, q = e % W;
+      const int i = k0 + t;
+      double* slot = row(i);
+      LB[(long long)i * W + q] = slot[q];
+      const int inew = i + WRC;
+      if (inew < N) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(slot + q);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(LB + (long long)inew * W + q));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  for (int e = tid; e < N; e += BCT) bs[e] = b[e];
+  __syncthreads();
+  // forward L y = b in blocks of NBB rows
+  for (int c0 = 0; c0 < N; c0 += BCH) {
+    const int cn = min(BCH, N - c0);
+    for (int e = tid; e < cn * W; e += BCT) win[e] = LB[(long long)c0 * W + e];
+    __syncthreads();
+    for (int e = tid; e < cn; e += BCT) rinv[e] = 1.0 / win[(long long)e * W];
+    for (int k = c0; k < c0 + cn; k += NBB) {
+      const int kn = min(NBB, c0 + cn - k);
+      // contributions of rows before the block: one warp per row
+      if (warp < kn) {
+        const int r = k + warp;
+        const double* rr = win + (long long)(r - c0) * W;
+        double s = 0.0;
+        for (int q = (r - k) + 1 + lane; q <= bw && q <= r; q += 32) s += rr[q] * bs[r - q];
+        s = warp_sum(s);
+        if (lane == 0) dot[warp] = s;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int t = 0; t < kn; ++t) {
+          const int r = k + t;
+          const double* rr = win + (long long)(r - c0) * W;
+          double v = bs[r] - dot[t];
+          for (int u = 0; u < t; ++u)
+            if (t - u <= bw) v -= rr[t - u] * bs[k + u];
+          bs[r] = v * rinv[r - c0];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // backward L^T x = y, row-oriented: x_k = y_k / L_kk, then y_{k-q} -= L[k][k-q] x_k
+  for (int c1 = N; c1 > 0; c1 -= BCH) {
+    const int c0 = max(0, c1 - BCH);
+    const int cn = c1 - c0;
+    for (int e = tid; e < cn * W; e += BCT) win[e] = LB[(long long)c0 * W + e];
+    __syncthreads();
+    for (int e = tid; e < cn; e += BCT) rinv[e] = 1.0 / win[(long long)e * W];
+    __syncthreads();
+    if (warp == 0) {
+      for (int k = c1 - 1; k >= c0; --k) {
+        const double* rk = win + (long long)(k - c0) * W;
+        const double xk = bs[k] * rinv[k - c0];
+        __syncwarp();
+        if (lane == 0) bs[k] = xk;
+        for (int q = 1 + lane; q <= bw && q <= k; q += 32) bs[k - q] -= rk[q] * xk;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < N; e += BCT) b[e] = bs[e];
+}
+
 }  // namespace
 
 TTB_API int ttb_local_band_build(void* stream, int r0, int n, int r1, int h, int Rb, const double* T1,
@@ -494,6 +639,17 @@ TTB_API int ttb_local_band_build(void* stream, int r0, int n, int r1, int h, int
 
 TTB_API int ttb_band_chol_solve(void* stream, long long N, int bw, double* LB, double* b, int* info) {
   if (N < 1 || bw < 0) return TTB_EARG;
+  const size_t rows = (size_t)((2 * NBB + bw) > BCH ? (2 * NBB + bw) : BCH);
+  const size_t smem = (rows * (bw + 1) + (size_t)N) * sizeof(double);
+  if (bw <= 127 && N <= 8192 && smem <= 200 * 1024) {
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(band_chol_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cfg = true;
+    }
+    band_chol_blocked_kernel<<<1, BCT, smem, as_stream(stream)>>>((int)N, bw, LB, b, info); ttb_count();
+    return ttb_last_error();
+  }
   band_chol_solve_kernel<<<1, 256, 0, as_stream(stream)>>>(N, bw, LB, b, info); ttb_count();
   return ttb_last_error();
 }

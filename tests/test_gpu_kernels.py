@@ -123,6 +123,40 @@ def test_gemm_lowrank_update(la, M, N, K, alpha, beta):
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
 
 
+@pytest.mark.parametrize("N,bw", [(1, 0), (50, 3), (300, 23), (1792, 55), (3000, 127), (5000, 20), (400, 140)])
+def test_band_cholesky_solve(N, bw):
+    # banded SPD solve behind AMEn's direct local solves (blocked shared-memory window for bw <= 127)
+    from paper_2509_13224_b200._lib import call, ptr
+    rng = np.random.default_rng(N + bw)
+    A = np.zeros((N, N))
+    for q in range(bw + 1):
+        v = rng.standard_normal(N - q) * 0.5
+        A[np.arange(q, N), np.arange(N - q)] = v
+        A[np.arange(N - q), np.arange(q, N)] = v
+    A += np.eye(N) * (2.0 * bw + 2.0)
+    W = bw + 1
+    LB = np.zeros((N, W))
+    for q in range(W):
+        LB[q:, q] = A[np.arange(q, N), np.arange(N - q)]
+    b = rng.standard_normal(N)
+    LBd, bd = T(LB), T(b)
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    call("ttb_band_chol_solve", N, bw, ptr(LBd), ptr(bd), ptr(info))
+    assert int(info.item()) == 0
+    x = np.linalg.solve(A, b)
+    assert np.abs(bd.cpu().numpy() - x).max() <= 1e-12 * max(1.0, np.abs(x).max())
+    L = np.linalg.cholesky(A)
+    Lgot = LBd.cpu().numpy()
+    for q in range(W):
+        assert np.allclose(Lgot[q:, q], L[np.arange(q, N), np.arange(N - q)], rtol=1e-11, atol=1e-13)
+    # indefinite: reported, not silently solved
+    A2 = LB.copy()
+    A2[N // 2, 0] = -1.0
+    LBd2, bd2 = T(A2), T(b)
+    call("ttb_band_chol_solve", N, bw, ptr(LBd2), ptr(bd2), ptr(info))
+    assert int(info.item()) > 0
+
+
 def test_svd_graded_and_degenerate(la):
     # graded singular values down to 1e-14 (relative accuracy of the one-sided Jacobi on R),
     # repeated singular values and exact rank deficiency, on the multi-CTA Jacobi sizes

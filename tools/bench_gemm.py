@@ -15,7 +15,8 @@ def timeit(fn, reps=5):
 
 shapes = [(8192, 8192, 8192, 0, 0), (8192, 8192, 8192, 1, 0), (8192, 8192, 8192, 0, 1),
           (262144, 4096, 1024, 0, 0), (1048576, 1024, 1024, 0, 0), (1024, 1048576, 128, 0, 0),
-          (1024, 128, 1048576, 0, 1), (1024, 1024, 1048576, 1, 1)]
+          (1024, 128, 1048576, 0, 1), (1024, 1024, 1048576, 1, 1),
+          (1048576, 1024, 1024, 1, 1), (1024, 1048576, 1024, 0, 0)]
 for M, N, K, tA, tB in shapes:
     A = torch.randn((K, M) if tA else (M, K), dtype=torch.float64, device="cuda")
     B = torch.randn((N, K) if tB else (K, N), dtype=torch.float64, device="cuda")

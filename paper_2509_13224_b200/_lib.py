@@ -82,13 +82,27 @@ def load_library(path: str = LIB_PATH):
     return lib
 
 
+_LIB = None
+_DEV_INDEX = None
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def lib():
-    if not torch.cuda.is_available():
-        raise NativeUnavailable("no CUDA device: the TT-IGA hot path runs only on the GPU (no CPU fallback)")
-    return load_library()
+    global _LIB
+    if _LIB is None:
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device: the TT-IGA hot path runs only on the GPU (no CPU fallback)")
+        _LIB = load_library()
+    return _LIB
 
 
 def stream():
+    """Current torch stream of the device the library runs on (cheap raw-handle path per call)."""
+    global _DEV_INDEX
+    if _DEV_INDEX is None:
+        _DEV_INDEX = torch.cuda.current_device()
+    if _raw_stream is not None and torch.cuda.current_device() == _DEV_INDEX:
+        return C.c_void_p(_raw_stream(_DEV_INDEX))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 

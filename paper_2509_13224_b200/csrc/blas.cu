@@ -592,9 +592,26 @@ __global__ void sum_final(int np, const double* part, double* out, int take_sqrt
 
 }  // namespace
 
+static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A,
+                          long long lda, long long sA, const double* B, long long ldb, long long sB, double beta,
+                          double* C, long long ldc, long long sC, int batch);
+
 TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                       long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
                       long long ldc, long long sC, int batch) {
+  const int rc = ttb_dgemm_impl(stream, tA, tB, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, batch);
+  if (ttb_debug_sync()) {
+    const cudaError_t e = cudaStreamSynchronize(as_stream(stream));
+    if (e != cudaSuccess)
+      fprintf(stderr, "ttb debug: dgemm tA=%d tB=%d M=%d N=%d K=%d lda=%lld ldb=%lld ldc=%lld batch=%d failed: %d\n", tA, tB, M,
+              N, K, lda, ldb, ldc, batch, (int)e);
+  }
+  return rc;
+}
+
+static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A,
+                          long long lda, long long sA, const double* B, long long ldb, long long sB, double beta,
+                          double* C, long long ldc, long long sC, int batch) {
   if (M < 0 || N < 0 || K < 0 || batch < 0) return TTB_EARG;
   if (M == 0 || N == 0 || batch == 0) return TTB_OK;
   cudaStream_t st = as_stream(stream);

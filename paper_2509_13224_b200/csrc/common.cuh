@@ -7,6 +7,21 @@
 namespace cg = cooperative_groups;
 
 #define TTB_API extern "C" __attribute__((visibility("default")))
+#include <stdio.h>
+#include <stdlib.h>
+// TTB_DEBUG_SYNC=1: synchronize after instrumented launches and report the first failing step
+inline bool ttb_debug_sync() {
+  static int v = -1;
+  if (v < 0) v = getenv("TTB_DEBUG_SYNC") ? 1 : 0;
+  return v == 1;
+}
+#define TTB_DBG(stream, what)                                                               \
+  do {                                                                                     \
+    if (ttb_debug_sync()) {                                                                \
+      cudaError_t e_ = cudaStreamSynchronize(stream);                                      \
+      if (e_ != cudaSuccess) fprintf(stderr, "ttb debug: %s failed: %d (%s:%d)\n", what, (int)e_, __FILE__, __LINE__); \
+    }                                                                                      \
+  } while (0)
 
 // error codes returned through the C ABI (0 = ok, >0 = CUDA error, <0 = argument/numerical)
 enum {

@@ -673,6 +673,7 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
         if (rc) return rc;
       } else if (tsqr_applies(mp, jb) && !coop_panels()) {
         rc = tsqr_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.ts, st);
+        TTB_DBG(st, "geqrf tsqr panel");
         if (rc) return rc;
       } else {
         rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, st);
@@ -686,6 +687,7 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
       const int n2 = (JB <= NB) ? (n - j0 - jb) : (J0 + JB - j0 - jb);
       if (n2 > 0) {
         rc = apply_wy(stream, mp, n2, jb, w.Vp, T, 1, A + (long long)(j0 + jb) * lda + j0, lda, w.W, w.W2);
+        TTB_DBG(st, "geqrf inner apply_wy");
         if (rc) return rc;
       }
     }
@@ -698,8 +700,10 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
     const double* Ap = A + (long long)J0 * lda + J0;
     extract_v_kernel<<<grid_v((long long)JB * JB), 256, 0, st>>>(JB, JB, Ap, lda, w.Vb); ttb_count();  // Vtop
     int rc = gram_panel(stream, MP, JB, Ap, lda, w.Vb, w.G);
+    TTB_DBG(st, "geqrf outer gram");
     if (rc) return rc;
     rc = launch_larft_block(JB, w.G, JB, w.Tin + (long long)(J0 / NB) * NB * NB, Tb, st);
+    TTB_DBG(st, "geqrf outer larft");
     if (rc) return rc;
     const int n2 = n - J0 - JB;
     if (n2 > 0) {

@@ -153,6 +153,66 @@ __global__ void __launch_bounds__(FW * 32) tsqr_factor_kernel(double* M, long lo
   for (int e = lane; e < NB * NB; e += 32) Tt[(long long)t * NB * NB + e] = T[e];
 }
 
+// Inner tree level: the explicit Q rows of every tile, Q_tile = [X; 0] - V (T (V_top^T X)), written
+// in place over the tile's reflectors (X = the tile's jb x jb block of the parent level's Q).
+__global__ void __launch_bounds__(QW * 32) tsqr_form_kernel(double* M, long long ld, long long rows, int nt, int jb,
+                                                             const double* __restrict__ Tt, const double* X,
+                                                             long long ldX) {
+  __shared__ double Bf[QW][3][NB * LDS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * QW + w;
+  if (t >= nt) return;
+  long long r0;
+  int r;
+  tile_bounds(rows, nt, t, r0, r);
+  double* vt = Bf[w][0];
+  double* xs = Bf[w][1];
+  double* ms = Bf[w][2];
+  if (lane < NB)
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+      vt[lane * LDS + c] = (c < jb && lane < r) ? (lane > c ? M[(long long)c * ld + r0 + lane] : (lane == c ? 1.0 : 0.0))
+                                                : 0.0;
+  for (int e = lane; e < NB * NB; e += 32) {
+    const int i = e % NB, c = e / NB;
+    xs[i * LDS + c] = (i < jb && c < jb) ? X[(long long)c * ldX + (long long)t * jb + i] : 0.0;
+  }
+  __syncwarp();
+  const double* Tg = Tt + (long long)t * NB * NB;
+  for (int e = lane; e < NB * NB; e += 32) {  // ms = V_top^T X
+    const int p = e / NB, c = e % NB;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc += vt[i * LDS + p] * xs[i * LDS + c];
+    ms[p * LDS + c] = acc;
+  }
+  __syncwarp();
+  for (int e = lane; e < NB * NB; e += 32) {  // vt = W = T ms
+    const int p = e / NB, c = e % NB;
+    double acc = 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc += (b >= p ? Tg[p * NB + b] : 0.0) * ms[b * LDS + c];
+    vt[p * LDS + c] = acc;
+  }
+  __syncwarp();
+  for (int s = 0; s < TS; ++s) {
+    const int i = lane + 32 * s;
+    if (i >= r) continue;
+    double v[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) v[c] = (c < jb) ? (i > c ? M[(long long)c * ld + r0 + i] : (i == c ? 1.0 : 0.0)) : 0.0;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      if (c < jb) {
+        double acc = (i < NB) ? xs[i * LDS + c] : 0.0;
+#pragma unroll
+        for (int p = 0; p < NB; ++p) acc -= v[p] * vt[p * LDS + c];
+        M[(long long)c * ld + r0 + i] = acc;
+      }
+    }
+  }
+}
+
 // Leaf pass: the panel's Householder vectors V = Q Z (Z = -S U^{-1}) for rows >= jb, where the
 // tile's orthonormal rows are Q_tile = H_tile [X; 0] = [X; 0] - V_tile (T (V_top^T X)) and X is
 // the tile's jb x jb block of X1 (col-major, ld ldX). Folded: V = [X Z; 0] - V_tile (W Z),
@@ -386,11 +446,32 @@ int householder_panel(int m, int jb, double* P, long long ld, double* tau, doubl
                       double* G, cudaStream_t st);
 long long householder_panel_part();
 
-// Workspace (doubles) for tsqr_panel on panels of up to m rows.
+// Tree levels: the stacked R factors are factored by warp tiles again until they fit the
+// register-resident single-CTA panel (qr.cu), whose WY form gives the top level's Q.
+constexpr long long kTopRows = 1280;
+constexpr int kMaxLevels = 12;
+
+long long tsqr_top_rows() {
+  static const long long v = getenv("TTB_TSQR_TOP") ? atoll(getenv("TTB_TSQR_TOP")) : kTopRows;
+  return v;
+}
+
+// Workspace (doubles) for tsqr_panel on panels of up to m rows. The level arrays shrink with the
+// panel height, but the top level does not (a shorter panel can stop the tree one level earlier
+// with a taller top), so the top arrays are reserved for the largest top any height can produce.
 long long tsqr_workspace(long long m) {
-  const long long nt = (m + TR - 1) / TR;
-  const long long rows1 = nt * NB;
-  return householder_panel_part() + 4 * NB * NB + 2 * NB + nt * NB * NB + 3 * rows1 * NB + 256;
+  long long s = householder_panel_part() + 6 * NB * NB + 2 * NB + 256;
+  long long rows = m;
+  const long long top = tsqr_top_rows();
+  for (int l = 0; l < kMaxLevels && (rows > top || l == 0); ++l) {
+    const long long nt = (rows + TR - 1) / TR;
+    s += nt * NB * NB;   // T per tile
+    rows = nt * NB;
+    s += rows * NB;      // stacked R of the next level (becomes its Q in place)
+  }
+  const long long rows1 = ((m + TR - 1) / TR) * NB;
+  const long long top_max = rows1 < top ? rows1 : top;
+  return s + 2 * (top_max > rows ? top_max : rows) * NB;  // top level: explicit V and Q
 }
 
 bool tsqr_applies(long long m, int jb) { return m > 8LL * TR && jb >= 1 && jb <= NB; }
@@ -399,32 +480,66 @@ bool tsqr_applies(long long m, int jb) { return m > 8LL * TR && jb >= 1 && jb <=
 // explicit V (m x jb, ld m, unit diagonal, zeros above) and T (jb x jb row-major, upper).
 int tsqr_panel(long long m, int jb, double* P, long long ld, double* tau, double* V, double* Tout, double* ws,
                cudaStream_t st) {
-  const int nt = tiles_of(m);
-  const long long rows1 = (long long)nt * jb;
-  if (rows1 > 0x7fffffffLL) return TTB_EARG;
   double* part = ws;
   double* G = part + householder_panel_part();
-  double* T1 = G + NB * NB;
-  double* Z = T1 + NB * NB;         // Z = -S U^{-1} | P top block
-  double* tau1 = Z + 2 * NB * NB;
-  double* Tt = tau1 + 2 * NB;
-  double* S1 = Tt + (long long)nt * NB * NB;
-  double* V1 = S1 + rows1 * NB;
-  double* X1 = V1 + rows1 * NB;
-  if (jb == NB)
-    tsqr_factor_kernel<NB><<<ceil_div(nt, FW), FW * 32, 0, st>>>(P, ld, m, nt, jb, Tt, S1, rows1);
-  else
-    tsqr_factor_kernel<0><<<ceil_div(nt, FW), FW * 32, 0, st>>>(P, ld, m, nt, jb, Tt, S1, rows1);
-  ttb_count();
-  int rc = householder_panel((int)rows1, jb, S1, rows1, tau1, V1, T1, part, G, st);
+  double* Ttop = G + NB * NB;
+  double* Z = Ttop + NB * NB;       // Z = -S U^{-1} | P top block
+  double* tautop = Z + 2 * NB * NB;
+  double* cur = tautop + 2 * NB + 256;
+  double* M[kMaxLevels + 1];
+  long long ldm[kMaxLevels + 1], rows[kMaxLevels + 1];
+  double* Tt[kMaxLevels];
+  int nt[kMaxLevels];
+  int L = 0;
+  M[0] = P; ldm[0] = ld; rows[0] = m;
+  const long long top_rows = tsqr_top_rows();
+  while (rows[L] > top_rows || L == 0) {
+    if (L >= kMaxLevels) return TTB_EARG;
+    nt[L] = tiles_of(rows[L]);
+    Tt[L] = cur;
+    cur += (long long)nt[L] * NB * NB;
+    rows[L + 1] = (long long)nt[L] * jb;
+    ldm[L + 1] = rows[L + 1];
+    M[L + 1] = cur;
+    cur += rows[L + 1] * NB;
+    if (jb == NB)
+      tsqr_factor_kernel<NB><<<ceil_div(nt[L], FW), FW * 32, 0, st>>>(M[L], ldm[L], rows[L], nt[L], jb, Tt[L], M[L + 1],
+                                                                      ldm[L + 1]);
+    else
+      tsqr_factor_kernel<0><<<ceil_div(nt[L], FW), FW * 32, 0, st>>>(M[L], ldm[L], rows[L], nt[L], jb, Tt[L], M[L + 1],
+                                                                     ldm[L + 1]);
+    ttb_count();
+    TTB_DBG(st, "tsqr factor");
+    ++L;
+  }
+  // top level: ordinary Householder panel (register-resident single CTA), then its explicit Q
+  const long long rt = rows[L];
+  double* Vtop = cur;
+  double* Xtop = Vtop + rt * NB;
+  int rc = householder_panel((int)rt, jb, M[L], rt, tautop, Vtop, Ttop, part, G, st);
+  TTB_DBG(st, "tsqr top panel");
   if (rc) return rc;
   {
-    int blocks = ceil_div(rows1, 256);
+    int blocks = ceil_div(rt, 256);
     if (blocks > 148 * 4) blocks = 148 * 4;
-    tsqr_q1_kernel<<<blocks, 256, 0, st>>>(rows1, jb, V1, T1, X1); ttb_count();
+    tsqr_q1_kernel<<<blocks, 256, 0, st>>>(rt, jb, Vtop, Ttop, Xtop); ttb_count();
+    TTB_DBG(st, "tsqr q1");
   }
-  tsqr_setup_kernel<<<1, 32, 0, st>>>(jb, P, ld, m, Tt, X1, rows1, S1, rows1, tau, V, Tout, Z); ttb_count();
-  tsqr_leaf_kernel<<<ceil_div(nt, QW), QW * 32, 0, st>>>(P, ld, m, nt, jb, Tt, X1, rows1, Z, V);
+  // explicit Q of the inner levels, top-down (in place over their reflectors)
+  const double* X = Xtop;
+  long long ldX = rt;
+  for (int l = L - 1; l >= 1; --l) {
+    tsqr_form_kernel<<<ceil_div(nt[l], QW), QW * 32, 0, st>>>(M[l], ldm[l], rows[l], nt[l], jb, Tt[l], X, ldX);
+    ttb_count();
+    TTB_DBG(st, "tsqr form");
+    X = M[l];
+    ldX = ldm[l];
+  }
+  // R of the whole panel = R of the top level (rows 0..jb-1 of its storage, ld rt)
+  tsqr_setup_kernel<<<1, 32, 0, st>>>(jb, P, ld, m, Tt[0], X, ldX, M[L], rt, tau, V, Tout, Z); ttb_count();
+  TTB_DBG(st, "tsqr setup");
+  tsqr_leaf_kernel<<<ceil_div(nt[0], QW), QW * 32, 0, st>>>(P, ld, m, nt[0], jb, Tt[0], X, ldX, Z, V);
   ttb_count();
+  TTB_DBG(st, "tsqr leaf");
   return ttb_last_error();
 }

@@ -197,8 +197,14 @@ class SVDFactors:
         X = X.contiguous()
         m, n = X.shape
         self.m, self.n = m, n
-        self.tall = m >= n
-        if self.tall:
+        # square: one-sided Jacobi straight on X (its column Gram equals R's, so the rotation
+        # sequence and sweep count are those of Jacobi on R, and the QR is saved)
+        self.direct = m == n and n > 64
+        self.tall = m >= n and not self.direct
+        if self.direct:
+            self.X = X
+            self.UJ, self.S, self.VJ = _jacobi(permute(X, (1, 0)), n, want_v)
+        elif self.tall:
             Qt, Rt = qr_colmajor(permute(X, (1, 0)), m, n)
             self.Qt = Qt                      # (n, m) == col-major Q (m x n)
             self.Rt = Rt                      # (n, n) == col-major R == row-major R^T
@@ -227,6 +233,8 @@ class SVDFactors:
 
     def SVt(self, r):
         """diag(S[:r]) Vt[:r] = U[:, :r]^T X  (r x n)."""
+        if self.direct:
+            return gemm(self.UJ[:r], self.X)                    # U^T X
         if self.tall:
             return gemm(self.UJ[:r], self.Rt, tB=True)          # U_R^T R
         W = gemm(self.UJ[:r], self.Rt)                          # U'^T R^T  (r x m)
@@ -236,7 +244,7 @@ class SVDFactors:
         """First r right singular vectors as rows (r x n); needs want_v=True."""
         if self.VJ is None:
             raise ValueError("right singular vectors were not accumulated (want_v=False)")
-        if self.tall:
+        if self.tall or self.direct:
             return self.VJ[:r].contiguous()
         return gemm(self.VJ[:r], self.Qt)
 

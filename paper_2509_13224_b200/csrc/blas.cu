@@ -407,7 +407,8 @@ int launch_wy_update_t(int M, int N, int K, double alpha, const double* A, long 
   }
   const int mt = (M + WU_BM - 1) / WU_BM;
   const int ntn = (N + BN - 1) / BN;
-  int gy = 148 / mt;
+  static const int sms = getenv("TTB_WY_SMS") ? atoi(getenv("TTB_WY_SMS")) : 148;
+  int gy = sms / mt;
   if (gy < 1) gy = 1;
   if (gy > ntn) gy = ntn;
   wy_update_kernel<BN, KC, S, WN><<<dim3(mt, gy), 64 * WN, smem, st>>>(M, N, K, alpha, A, lda, B, ldb, C, ldc);
@@ -501,17 +502,43 @@ bool wy_legacy() {
   return v == 1;
 }
 
-double* g_scratch = nullptr;
-size_t g_scratch_bytes = 0;
+// split-K partial sums: one buffer per stream (the blocked QR runs panel work on a second stream
+// concurrently with the trailing updates). Growing a buffer synchronizes the device first.
+struct ScratchSlot {
+  cudaStream_t st;
+  double* p;
+  size_t bytes;
+  unsigned long long last;
+};
+ScratchSlot g_scratch[4] = {};
+unsigned long long g_scratch_clock = 0;
 
-double* scratch(size_t bytes) {
-  if (bytes > g_scratch_bytes) {
-    if (g_scratch) { cudaDeviceSynchronize(); cudaFree(g_scratch); }
-    size_t want = bytes + bytes / 2;
-    if (cudaMalloc(&g_scratch, want) != cudaSuccess) { g_scratch = nullptr; g_scratch_bytes = 0; return nullptr; }
-    g_scratch_bytes = want;
+double* scratch(size_t bytes, cudaStream_t st) {
+  ScratchSlot* slot = nullptr;
+  for (auto& s : g_scratch)
+    if (s.p && s.st == st) slot = &s;
+  if (!slot) {
+    for (auto& s : g_scratch)
+      if (!s.p) { slot = &s; break; }
+    if (!slot) {  // evict the least recently used stream's buffer
+      slot = &g_scratch[0];
+      for (auto& s : g_scratch)
+        if (s.last < slot->last) slot = &s;
+      cudaDeviceSynchronize();
+      cudaFree(slot->p);
+      slot->p = nullptr;
+      slot->bytes = 0;
+    }
+    slot->st = st;
   }
-  return g_scratch;
+  slot->last = ++g_scratch_clock;
+  if (bytes > slot->bytes) {
+    if (slot->p) { cudaDeviceSynchronize(); cudaFree(slot->p); }
+    const size_t want = bytes + bytes / 2;
+    if (cudaMalloc(&slot->p, want) != cudaSuccess) { slot->p = nullptr; slot->bytes = 0; return nullptr; }
+    slot->bytes = want;
+  }
+  return slot->p;
 }
 
 // ---------------------------------------------------------------------------
@@ -649,7 +676,7 @@ static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, dou
     if (S > 1) {
       int Kc = (int)(((K + S - 1) / S + kKcAlign - 1) / kKcAlign * kKcAlign);
       S = (K + Kc - 1) / Kc;
-      double* part = scratch((size_t)S * M * N * sizeof(double));
+      double* part = scratch((size_t)S * M * N * sizeof(double), st);
       if (!part) return (int)cudaErrorMemoryAllocation;
       GemmArgs p = g;
       p.alpha = 1.0; p.beta = 0.0; p.C = part; p.ldc = N; p.sC = (long long)M * N; p.split = 1; p.Kc = Kc;

@@ -551,6 +551,7 @@ int launch_gram(int m, int nb, const double* V, double* G, double* part, cudaStr
 
 struct QrWs {
   double *part, *Vp, *Vb, *W, *W2, *G, *Tin, *Tout, *ts;
+  double *Wb, *W2b, *Gb, *Vt2;  // second set for the look-ahead stream split
 };
 
 QrWs carve(double* ws, int m, int n) {
@@ -566,6 +567,10 @@ QrWs carve(double* ws, int m, int n) {
   w.Tin = w.G + (long long)NB2 * NB2;
   w.Tout = w.Tin + (long long)((k + NB - 1) / NB) * NB * NB;
   w.ts = w.Tout + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
+  w.Wb = w.ts + tsqr_workspace(m);
+  w.W2b = w.Wb + wn * NB2;
+  w.Gb = w.W2b + wn * NB2;
+  w.Vt2 = w.Gb + (long long)NB2 * NB2;  // 2 x NB2 x NB2: Vtop of block parity 0 / 1
   return w;
 }
 
@@ -647,8 +652,141 @@ TTB_API long long ttb_qr_workspace(int m, int n) {
   s += (long long)m * NB + (long long)m * NB2 + 2 * wn * NB2 + (long long)NB2 * NB2;
   s += (long long)((k + NB - 1) / NB) * NB * NB + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
   s += tsqr_workspace(m);
+  s += 2 * wn * NB2 + 3LL * NB2 * NB2;  // look-ahead: second W, W2, G and two Vtop blocks
   return s + 64;
 }
+
+namespace {
+
+// Panels of outer block [J0, J0 + JB) on stream s (inner WY updates inside the block; a block that
+// is a single panel updates the whole trailing matrix), then the block's Vtop, Gram and T.
+int factor_block(cudaStream_t s, int m, int n, int J0, int JB, double* A, long long lda, double* tau, QrWs& w,
+                 double* Wp, double* W2p, double* Vtop, double* G) {
+  void* stream = (void*)s;
+  for (int j0 = J0; j0 < J0 + JB; j0 += NB) {
+    const int jb = (J0 + JB - j0) < NB ? (J0 + JB - j0) : NB;
+    const int mp = m - j0;
+    double* P = A + (long long)j0 * lda + j0;
+    double* T = w.Tin + (long long)(j0 / NB) * NB * NB;
+    int rc;
+    if (panel_is_small(mp, jb)) {
+      rc = launch_panel_small(mp, jb, P, lda, tau + j0, w.Vp, T, s);
+    } else if (tsqr_applies(mp, jb) && !coop_panels()) {
+      rc = tsqr_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.ts, s);
+    } else {
+      rc = launch_panel(mp, jb, P, lda, tau + j0, w.Vp, T, w.part, s);
+      if (!rc) rc = launch_gram(mp, jb, w.Vp, G, w.part, s);
+      if (!rc) { larft_kernel<<<1, 128, 0, s>>>(jb, G, jb, tau + j0, T); ttb_count(); }
+    }
+    TTB_DBG(s, "geqrf panel");
+    if (rc) return rc;
+    const int n2 = (JB <= NB) ? (n - j0 - jb) : (J0 + JB - j0 - jb);
+    if (n2 > 0) {
+      rc = apply_wy(stream, mp, n2, jb, w.Vp, T, 1, A + (long long)(j0 + jb) * lda + j0, lda, Wp, W2p);
+      TTB_DBG(s, "geqrf inner apply_wy");
+      if (rc) return rc;
+    }
+  }
+  double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
+  if (JB <= NB) {
+    cudaMemcpyAsync(Tb, w.Tin + (long long)(J0 / NB) * NB * NB, sizeof(double) * JB * JB, cudaMemcpyDeviceToDevice, s);
+    return ttb_last_error();
+  }
+  const double* Ap = A + (long long)J0 * lda + J0;
+  extract_v_kernel<<<grid_v((long long)JB * JB), 256, 0, s>>>(JB, JB, Ap, lda, Vtop); ttb_count();
+  int rc = gram_panel(stream, m - J0, JB, Ap, lda, Vtop, G);
+  if (rc) return rc;
+  rc = launch_larft_block(JB, G, JB, w.Tin + (long long)(J0 / NB) * NB * NB, Tb, s);
+  TTB_DBG(s, "geqrf outer larft");
+  return rc;
+}
+
+struct LookAhead {
+  cudaStream_t sb = nullptr;
+  cudaEvent_t* ev = nullptr;
+  int nev = 0;
+};
+
+LookAhead& look_ahead(int need) {
+  static LookAhead la;
+  if (!la.sb) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&la.sb, cudaStreamNonBlocking, hi);  // panels first when SMs free up
+  }
+  if (need > la.nev) {
+    cudaEvent_t* ev = new cudaEvent_t[need];
+    for (int i = 0; i < la.nev; ++i) ev[i] = la.ev[i];
+    for (int i = la.nev; i < need; ++i) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    delete[] la.ev;
+    la.ev = ev;
+    la.nev = need;
+  }
+  return la;
+}
+
+// TTB_QR_LOOKAHEAD=0 keeps the serial order (A/B testing)
+bool lookahead_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TTB_QR_LOOKAHEAD");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// Right-looking blocked QR with depth-1 look-ahead: the panels of block J+1 (their columns first
+// updated by block J) are factored on a second, high-priority stream while the caller's stream
+// applies block J to the columns beyond block J+1. Column sets are disjoint; each stream has its
+// own WY scratch, Vtop/Gram buffers alternate by block parity.
+int geqrf_lookahead(cudaStream_t st, int m, int n, double* A, long long lda, double* tau, QrWs& w) {
+  const int k = m < n ? m : n;
+  const int nblk = (k + NB2 - 1) / NB2;
+  LookAhead& la = look_ahead(2 * nblk + 2);
+  cudaStream_t sb = la.sb;
+  cudaEvent_t ev_start = la.ev[0], ev_done = la.ev[1];
+  cudaEvent_t* ev_fact = la.ev + 2;         // block J factored (T_J ready), on sb
+  cudaEvent_t* ev_big = la.ev + 2 + nblk;   // big update of block J applied, on st
+  cudaEventRecord(ev_start, st);
+  cudaStreamWaitEvent(sb, ev_start, 0);
+  auto vtop = [&](int J) { return w.Vt2 + (long long)(J & 1) * NB2 * NB2; };
+  auto gbuf = [&](int J) { return (J & 1) ? w.Gb : w.G; };
+  int rc = factor_block(sb, m, n, 0, k < NB2 ? k : NB2, A, lda, tau, w, w.W, w.W2, vtop(0), gbuf(0));
+  if (rc) return rc;
+  cudaEventRecord(ev_fact[0], sb);
+  for (int J = 0; J < nblk; ++J) {
+    const int J0 = J * NB2;
+    const int JB = (k - J0) < NB2 ? (k - J0) : NB2;
+    const int J1 = J0 + JB;
+    const int JBn = (J + 1 < nblk) ? ((k - J1) < NB2 ? (k - J1) : NB2) : 0;
+    const double* Ap = A + (long long)J0 * lda + J0;
+    double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
+    if (JBn > 0) {
+      if (J >= 1) cudaStreamWaitEvent(sb, ev_big[J - 1], 0);
+      if (JB > NB) {  // a single-panel block already updated everything to its right
+        rc = apply_wy_panel((void*)sb, m - J0, JBn, JB, Ap, lda, vtop(J), Tb, 1, A + (long long)J1 * lda + J0, lda, w.W,
+                            w.W2);
+        if (rc) return rc;
+      }
+      rc = factor_block(sb, m, n, J1, JBn, A, lda, tau, w, w.W, w.W2, vtop(J + 1), gbuf(J + 1));
+      if (rc) return rc;
+      cudaEventRecord(ev_fact[J + 1], sb);
+    }
+    const int nrest = n - (J1 + JBn);
+    if (nrest > 0 && JB > NB) {
+      cudaStreamWaitEvent(st, ev_fact[J], 0);
+      rc = apply_wy_panel((void*)st, m - J0, nrest, JB, Ap, lda, vtop(J), Tb, 1, A + (long long)(J1 + JBn) * lda + J0,
+                          lda, w.Wb, w.W2b);
+      if (rc) return rc;
+    }
+    cudaEventRecord(ev_big[J], st);
+  }
+  cudaEventRecord(ev_done, sb);
+  cudaStreamWaitEvent(st, ev_done, 0);
+  return ttb_last_error();
+}
+
+}  // namespace
 
 // In-place QR of col-major A (m x n, lda). tau: min(m,n). ws: ttb_qr_workspace doubles; the outer
 // WY factors stay in ws for a following ttb_orgqr. Two-level blocking: 32-column panels (cooperative
@@ -659,6 +797,7 @@ TTB_API int ttb_geqrf(void* stream, int m, int n, double* A, long long lda, doub
   if (k == 0) return TTB_OK;
   cudaStream_t st = as_stream(stream);
   QrWs w = carve(ws, m, n);
+  if (lookahead_enabled() && m >= 65536 && k > NB2) return geqrf_lookahead(st, m, n, A, lda, tau, w);
   for (int J0 = 0; J0 < k; J0 += NB2) {
     const int JB = (k - J0) < NB2 ? (k - J0) : NB2;
     const int MP = m - J0;

@@ -59,7 +59,8 @@ def test_permute_and_tdot(la):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 3), (3, 5), (64, 64), (200, 37), (1000, 70), (40, 300), (5000, 33),
-                                 (20000, 100), (1100, 16), (1500, 17), (200000, 40), (131073, 150)])
+                                 (20000, 100), (1100, 16), (1500, 17), (200000, 40), (131073, 150), (70001, 300),
+                                 (65536, 257)])
 def test_qr(la, m, n):
     rng = np.random.default_rng(m + n)
     X = rng.standard_normal((m, n))

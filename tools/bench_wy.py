@@ -21,3 +21,12 @@ for nq, K in ((896, 128), (512, 128), (128, 128), (768, 256), (256, 256), (1024,
     ms = timeit(lambda: L.gemm(A, B, alpha=-1.0, beta=1.0, out=C))
     print(f"C({nq} x {m}) -= A({nq} x {K}) B: {ms:7.2f} ms  {2.0 * nq * m * K / ms / 1e9:6.2f} TF/s", flush=True)
     del A, B, C
+
+# cuBLAS on the same update (torch.addmm, beta = 1, alpha = -1) as the ceiling reference
+for nq, K in ((896, 128), (512, 128)):
+    A = torch.randn(nq, K, dtype=torch.float64, device="cuda")
+    B = torch.randn(K, m, dtype=torch.float64, device="cuda")
+    C = torch.randn(nq, m, dtype=torch.float64, device="cuda")
+    ms = timeit(lambda: C.addmm_(A, B, beta=1.0, alpha=-1.0))
+    print(f"cuBLAS C({nq} x {m}) -= A B (K={K}): {ms:7.2f} ms  {2.0 * nq * m * K / ms / 1e9:6.2f} TF/s", flush=True)
+    del A, B, C

@@ -135,30 +135,56 @@ def nrm2(x):
 # ---------------------------------------------------------------------------
 # QR
 
-def qr_colmajor(Acm, m, n, want_q=True, want_r=True):
+def qr_colmajor(Acm, m, n, want_q=True, want_r=True, overlap_r=None):
     """Householder QR of a col-major m x n matrix held as torch (n, m) (consumed).
 
     Returns (Qt, Rt): Qt = torch (k, m) == col-major Q (m x k); Rt = torch (n, k) == col-major R (k x n).
+    ``overlap_r(Rt)``, if given, is called on a side stream as soon as R is available and runs
+    concurrently with the formation of Q (the two are independent); its result is returned third.
     """
     k = min(m, n)
     if k == 0:
-        return empty(0, m), empty(n, 0)
+        return (empty(0, m), empty(n, 0)) if overlap_r is None else (empty(0, m), empty(n, 0), overlap_r(empty(n, 0)))
     if call_raw("ttb_qr_small_fits", m, n):
         Qt = empty(k, m) if want_q else None
         Rt = empty(n, k)
         call("ttb_qr_small", m, n, ptr(Acm), m, ptr(Qt), m, ptr(Rt))
+        if overlap_r is not None:
+            return Qt, Rt, overlap_r(Rt)
         return Qt, (Rt if want_r else None)
     ws = empty(int(call_raw("ttb_qr_workspace", m, n)))
     tau = empty(k)
     call("ttb_geqrf", m, n, ptr(Acm), m, ptr(tau), ptr(ws))
     Qt = Rt = None
-    if want_r:
+    if want_r or overlap_r is not None:
         Rt = empty(n, k)
         call("ttb_extract_r", k, n, ptr(Acm), m, ptr(Rt))
+    side = None
+    if overlap_r is not None:
+        main = torch.cuda.current_stream()
+        side = _side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            res = overlap_r(Rt)
     if want_q:
         Qt = empty(k, m)
         call("ttb_orgqr", m, k, k, ptr(Acm), m, ptr(Qt), m, ptr(ws), n)
+    if side is not None:
+        main.wait_stream(side)
+        for t in (Rt,) + tuple(x for x in (res if isinstance(res, tuple) else (res,)) if isinstance(x, torch.Tensor)):
+            t.record_stream(main)
+        return Qt, Rt, res
     return Qt, Rt
+
+
+_SIDE = None
+
+
+def _side_stream():
+    global _SIDE
+    if _SIDE is None:
+        _SIDE = torch.cuda.Stream(priority=-1)
+    return _SIDE
 
 
 def qr(X):
@@ -205,10 +231,11 @@ class SVDFactors:
             self.X = X
             self.UJ, self.S, self.VJ = _jacobi(permute(X, (1, 0)), n, want_v)
         elif self.tall:
-            Qt, Rt = qr_colmajor(permute(X, (1, 0)), m, n)
+            # the Jacobi SVD of R runs on a side stream while Q is formed (independent work)
+            Qt, Rt, (self.UJ, self.S, self.VJ) = qr_colmajor(
+                permute(X, (1, 0)), m, n, overlap_r=lambda R: _jacobi(R.contiguous(), n, want_v))
             self.Qt = Qt                      # (n, m) == col-major Q (m x n)
             self.Rt = Rt                      # (n, n) == col-major R == row-major R^T
-            self.UJ, self.S, self.VJ = _jacobi(Rt.contiguous(), n, want_v)
         else:
             Qt, Rt = qr_colmajor(X.clone(), n, m)  # X^T = Q R, Q (n x m), R (m x m)
             self.Qt = Qt                      # (m, n) == col-major Q == row-major Q^T

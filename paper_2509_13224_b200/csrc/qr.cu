@@ -618,6 +618,39 @@ int apply_wy_panel(void* stream, int mp, int nq, int jb, const double* Ap, long 
   return ttb_dgemm(stream, 0, 0, nq, mb, jb, -1.0, W2, jb, 0, Ap + jb, lda, 0, 1.0, C + jb, ldc, 0, 1);
 }
 
+// W[q][p] = V[q][p] (rows q < nid of W = C^T V when C's first nid columns are still e_q: orgqr)
+__global__ void w_identity_kernel(int nid, int jb, const double* __restrict__ Vtop, double* W) {
+  for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < nid * jb; e += blockDim.x * gridDim.x) {
+    const int q = e / jb, p = e % jb;
+    W[e] = Vtop[(long long)p * jb + q];
+  }
+}
+
+// apply_wy_panel for orgqr: the first nid columns of C are untouched identity columns (rows < nid),
+// so their rows of W = C^T V are rows of V and only the remaining columns need the long GEMM.
+int apply_wy_panel_orgqr(void* stream, int mp, int nq, int jb, int nid, const double* Ap, long long lda,
+                         const double* Vtop, const double* T, double* C, long long ldc, double* W, double* W2) {
+  cudaStream_t st = as_stream(stream);
+  const int mb = mp - jb;
+  const int nr = nq - nid;
+  w_identity_kernel<<<ceil_div((long long)nid * jb, 256), 256, 0, st>>>(nid, jb, Vtop, W); ttb_count();
+  int rc = 0;
+  if (nr > 0) {
+    if (mb > 0)
+      rc = ttb_dgemm(stream, 0, 1, nr, jb, mb, 1.0, C + (long long)nid * ldc + jb, ldc, 0, Ap + jb, lda, 0, 0.0,
+                     W + (long long)nid * jb, jb, 0, 1);
+    if (rc) return rc;
+    rc = ttb_dgemm(stream, 0, 1, nr, jb, jb, 1.0, C + (long long)nid * ldc, ldc, 0, Vtop, jb, 0, mb > 0 ? 1.0 : 0.0,
+                   W + (long long)nid * jb, jb, 0, 1);
+    if (rc) return rc;
+  }
+  rc = ttb_dgemm(stream, 0, 1, nq, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
+  if (rc) return rc;
+  rc = ttb_dgemm(stream, 0, 0, nq, jb, jb, -1.0, W2, jb, 0, Vtop, jb, 0, 1.0, C, ldc, 0, 1);
+  if (rc || mb <= 0) return rc;
+  return ttb_dgemm(stream, 0, 0, nq, mb, jb, -1.0, W2, jb, 0, Ap + jb, lda, 0, 1.0, C + jb, ldc, 0, 1);
+}
+
 // G = V^T V for the in-place reflectors of apply_wy_panel
 int gram_panel(void* stream, int mp, int jb, const double* Ap, long long lda, const double* Vtop, double* G) {
   const int mb = mp - jb;
@@ -871,7 +904,9 @@ TTB_API int ttb_orgqr(void* stream, int m, int kq, int kf, const double* A, long
     double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
     const double* Ap = A + (long long)J0 * lda + J0;
     extract_v_kernel<<<grid_v((long long)JB * JB), 256, 0, st>>>(JB, JB, Ap, lda, w.Vb); ttb_count();  // Vtop
-    int rc = apply_wy_panel(stream, MP, nq, JB, Ap, lda, w.Vb, Tb, 0, Q + (long long)J0 * ldq + J0, ldq, w.W, w.W2);
+    const int nid = JB < nq ? JB : nq;  // columns J0 .. J0+JB-1 of Q are still identity columns here
+    int rc = apply_wy_panel_orgqr(stream, MP, nq, JB, nid, Ap, lda, w.Vb, Tb, Q + (long long)J0 * ldq + J0, ldq, w.W,
+                                  w.W2);
     if (rc) return rc;
   }
   return ttb_last_error();

@@ -152,6 +152,26 @@ int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, co
                   const double* phiR, const double* b, double* x, const double* d, double atol, int maxiter,
                   int x0_nonzero, double* ws, double* S, int* iters);
 
+/* Banded contraction as one batched DMMA GEMM (large operator ranks; replaces the inner loops of
+ * amen.py:77-99 _OpCore.apply/apply_rev): out[i, X, o] = sum_{t, r} Tp[i + t, r, X] Mt[i, t, r, o],
+ * Tp (n + 2h, Rin, X) with h zero blocks at both ends, Mt (n, 2h+1, Rin, Rout) = the banded core
+ * M[a, i, t, b] permuted to (i, t, a, b) (forward) or (i, t, b, a) (reverse). */
+int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
+                  double* out);
+/* Local projected operator (amen.py:147-150 matvec3) with vectors in the mode-major (i, x, z) layout:
+ * phiLp = phiL permuted (a, x, y), Mf = (n, 2h+1, Ra, Rb), phiRp = phiR permuted (z, w, b).
+ * ws: ttb_local_gemm_workspace doubles, padding zeroed once by ttb_local_gemm_ws_init. */
+long long ttb_local_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h); /* doubles */
+int ttb_local_gemm_ws_init(void* stream, int r0, int n, int r1, int Ra, int h, double* ws);
+int ttb_local_matvec_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiLp,
+                          const double* Mf, const double* phiRp, const double* v, double* y, double* ws);
+/* ttb_local_pcg over ttb_local_matvec_gemm, vectors in (i, x, z) layout; ws: ttb_pcg_gemm_workspace
+ * doubles, ttb_local_gemm_ws_init applied at offset 4 r0 n r1. */
+long long ttb_pcg_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h); /* doubles */
+int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiLp,
+                       const double* Mf, const double* phiRp, const double* b, double* x, const double* d,
+                       double atol, int maxiter, int x0_nonzero, double* ws, double* S, int* iters);
+
 #ifdef __cplusplus
 }
 #endif

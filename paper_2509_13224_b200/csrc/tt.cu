@@ -347,24 +347,74 @@ TTB_API long long ttb_pcg_workspace(int r0, int n, int r1, int Ra, int Rb) {
   return 4 * N + (long long)r0 * Ra * n * r1 + (long long)r0 * n * Rb * r1 + 2 * PB + 16;
 }
 
-// Jacobi-PCG on the local system; x holds x0 on entry (x0_nonzero says whether to form b - A x0).
-// d: preconditioner diagonal (already floored). Returns iterations in *iters.
-TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL,
-                          const double* M, const double* phiR, const double* b, double* x, const double* d,
-                          double atol, int maxiter, int x0_nonzero, double* ws, double* S, int* iters) {
+// ---------------------------------------------------------------------------
+// Banded operator contractions as batched DMMA GEMMs (large operator ranks).
+//
+// With the operator core re-laid out as Mf[i, t, a, b] = M[a, i, t, b] (or Mr[i, t, b, a] for the
+// reverse direction) and the vector-side operand as Tp[j + h, a, X] (j-major, h zero blocks of
+// padding on both ends), the banded contraction
+//     out[i, X, b] = sum_{t, a} Tp[i + t, a, X] Mf[i, t, a, b]
+// is, for every mode index i, one GEMM whose K = (2h+1) Ra operand is the contiguous window of
+// Tp rows starting at block i: C_i (X x Rb) = Tp_window_i^T (X x K) * Mf_i (K x Rb).
+// The padding blocks of Tp must be zero (they meet the zero out-of-band slots of Mf).
+TTB_API int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
+                          double* out) {
+  const int B = 2 * h + 1;
+  return ttb_dgemm(stream, 1, 0, X, Rout, B * Rin, 1.0, Tp, X, (long long)Rin * X, Mt, Rout,
+                   (long long)B * Rin * Rout, 0.0, out, Rout, (long long)X * Rout, n);
+}
+
+TTB_API long long ttb_local_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h) {
+  return (long long)(n + 2 * h) * Ra * r0 * r1 + (long long)n * r0 * r1 * Rb;
+}
+
+// Local projected operator in the mode-major (i, x, z) vector layout, three GEMM stages:
+//   Tp[j+h, a, x, w] = sum_y phiLp[a, x, y] v[j, y, w]           (batched over j)
+//   t2[i, x, w, b]   = band_gemm(Tp, Mf)                           (batched over i)
+//   y[i, x, z]       = sum_{w, b} t2[i, x, w, b] phiRp[z, w, b]    (one GEMM)
+// phiLp = phiL permuted to (a, x, y); phiRp = phiR permuted to (z, w, b); Mf (n, 2h+1, Ra, Rb).
+// ws (ttb_local_gemm_workspace doubles): its first h*Ra*r0*r1 and last h*Ra*r0*r1 doubles of the
+// Tp part must be zero (ttb_local_gemm_ws_init), the interior is overwritten every call.
+TTB_API int ttb_local_gemm_ws_init(void* stream, int r0, int n, int r1, int Ra, int h, double* ws) {
+  const long long blk = (long long)Ra * r0 * r1;
   cudaStream_t st = as_stream(stream);
-  const long long N = (long long)r0 * n * r1;
+  if (h > 0) {
+    cudaMemsetAsync(ws, 0, (size_t)h * blk * sizeof(double), st);
+    cudaMemsetAsync(ws + (long long)(n + h) * blk, 0, (size_t)h * blk * sizeof(double), st);
+  }
+  return ttb_last_error();
+}
+
+TTB_API int ttb_local_matvec_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiLp,
+                                  const double* Mf, const double* phiRp, const double* v, double* y, double* ws) {
+  const long long blk = (long long)Ra * r0 * r1;
+  double* Tp = ws;
+  double* t2 = ws + (long long)(n + 2 * h) * blk;
+  int rc = ttb_dgemm(stream, 0, 0, Ra * r0, r1, r0, 1.0, phiLp, r0, 0, v, r1, (long long)r0 * r1, 0.0,
+                     Tp + (long long)h * blk, r1, blk, n);
+  if (rc) return rc;
+  rc = ttb_band_gemm(stream, n, h, Ra, Rb, r0 * r1, Tp, Mf, t2);
+  if (rc) return rc;
+  return ttb_dgemm(stream, 0, 1, n * r0, r1, r1 * Rb, 1.0, t2, (long long)r1 * Rb, 0, phiRp, (long long)r1 * Rb, 0,
+                   0.0, y, r1, 0, 1);
+}
+
+namespace {
+
+// Jacobi-PCG on the local system with scipy.sparse.linalg.cg stopping semantics; MV(p, q) applies
+// the local operator. ws: 4N (+ matvec workspace owned by MV) + 2 PB + 16 doubles after it.
+template <class MV>
+int pcg_run(cudaStream_t st, long long N, const MV& mv, const double* b, double* x, const double* d, double atol,
+            int maxiter, int x0_nonzero, double* ws, double* part, double* S, int* iters) {
   double* r = ws;
   double* z = r + N;
   double* p = z + N;
   double* q = p + N;
-  double* mvws = q + N;
-  double* part = mvws + (long long)r0 * Ra * n * r1 + (long long)r0 * n * Rb * r1;
   const int nb = grid_for(N) < PB ? grid_for(N) : PB;
   set_scalars<<<1, 1, 0, st>>>(S, atol * atol); ttb_count();
   int rc;
   if (x0_nonzero) {
-    rc = ttb_local_matvec(stream, r0, n, r1, Ra, Rb, h, phiL, M, phiR, x, r, mvws);
+    rc = mv(x, r);
     if (rc) return rc;
     sub_from_kernel<<<nb, 256, 0, st>>>(N, b, r, part); ttb_count();
   } else {
@@ -382,7 +432,7 @@ TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, i
       pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 0); ttb_count();
       pcg_update_p<<<grid_for(N), 256, 0, st>>>(N, z, p, S); ttb_count();
       // q = A p   (skipped work when done: kernels still run but results unused)
-      rc = ttb_local_matvec(stream, r0, n, r1, Ra, Rb, h, phiL, M, phiR, p, q, mvws);
+      rc = mv(p, q);
       if (rc) return rc;
       pcg_dot_partial<<<nb, 256, 0, st>>>(N, p, q, S, part); ttb_count();
       pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 2); ttb_count();
@@ -395,6 +445,41 @@ TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, i
   }
   if (iters) *iters = (int)host[6];
   return ttb_last_error();
+}
+
+}  // namespace
+
+// Jacobi-PCG on the local system; x holds x0 on entry (x0_nonzero says whether to form b - A x0).
+// d: preconditioner diagonal (already floored). Returns iterations in *iters.
+TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL,
+                          const double* M, const double* phiR, const double* b, double* x, const double* d,
+                          double atol, int maxiter, int x0_nonzero, double* ws, double* S, int* iters) {
+  const long long N = (long long)r0 * n * r1;
+  double* mvws = ws + 4 * N;
+  double* part = mvws + (long long)r0 * Ra * n * r1 + (long long)r0 * n * Rb * r1;
+  auto mv = [&](const double* in, double* out) {
+    return ttb_local_matvec(stream, r0, n, r1, Ra, Rb, h, phiL, M, phiR, in, out, mvws);
+  };
+  return pcg_run(as_stream(stream), N, mv, b, x, d, atol, maxiter, x0_nonzero, ws, part, S, iters);
+}
+
+TTB_API long long ttb_pcg_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h) {
+  return 4LL * r0 * n * r1 + ttb_local_gemm_workspace(r0, n, r1, Ra, Rb, h) + 2 * PB + 16;
+}
+
+// Same PCG with vectors in the (i, x, z) layout and the GEMM-staged local operator
+// (ttb_local_matvec_gemm); ws: ttb_pcg_gemm_workspace doubles, its matvec part initialised by
+// ttb_local_gemm_ws_init at offset 4 r0 n r1.
+TTB_API int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiLp,
+                               const double* Mf, const double* phiRp, const double* b, double* x, const double* d,
+                               double atol, int maxiter, int x0_nonzero, double* ws, double* S, int* iters) {
+  const long long N = (long long)r0 * n * r1;
+  double* mvws = ws + 4 * N;
+  double* part = mvws + ttb_local_gemm_workspace(r0, n, r1, Ra, Rb, h);
+  auto mv = [&](const double* in, double* out) {
+    return ttb_local_matvec_gemm(stream, r0, n, r1, Ra, Rb, h, phiLp, Mf, phiRp, in, out, mvws);
+  };
+  return pcg_run(as_stream(stream), N, mv, b, x, d, atol, maxiter, x0_nonzero, ws, part, S, iters);
 }
 
 // ---------------------------------------------------------------------------

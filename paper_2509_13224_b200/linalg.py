@@ -78,6 +78,15 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
     return out
 
 
+def gemm_strided(tA, tB, M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, alpha=1.0, beta=0.0):
+    """Strided-batched C_b = alpha op(A_b) op(B_b) + beta C_b on raw device tensors (row-major views;
+    A, B, C are tensors whose data_ptr is the first batch's first element)."""
+    if M and N and batch:
+        call("ttb_dgemm", int(tA), int(tB), int(M), int(N), int(K), float(alpha), ptr(A), int(lda), int(sA), ptr(B),
+             int(ldb), int(sB), float(beta), ptr(C), int(ldc), int(sC), int(batch))
+    return C
+
+
 def permute(X, perm, out=None):
     """Materialized X.permute(perm) (row-major), by the native transpose kernel (into ``out`` if given)."""
     perm = tuple(int(p) for p in perm)

@@ -140,6 +140,8 @@ int ttb_band_chol_solve(void* stream, long long N, int bw, double* LB, double* b
 int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
                     const double* phiR, double* d, double* part);
 /* Entries of a 3-core TT at N multi-indices (TtTensor.gather, core.py:164-170). */
+/* d = max(|d|, 1e-14 max|d|) elementwise (Jacobi preconditioner floor, amen.py:179-181); part >= 320 doubles. */
+int ttb_abs_floor(void* stream, long long tot, double* d, double* part);
 int ttb_tt_gather3(void* stream, int N, const long long* idx, const double* G0, int n0, int r1, const double* G1,
                    int n1, int r2, const double* G2, int n2, double* out);
 /* y = local projected operator applied to v (amen._LocalSystem.matvec3). ws: r0*Ra*n*r1 + r0*n*Rb*r1 doubles. */

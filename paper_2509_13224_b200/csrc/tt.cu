@@ -319,6 +319,16 @@ TTB_API int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb,
   return ttb_last_error();
 }
 
+// d = max(|d|, 1e-14 max|d|) in place (the reference's Jacobi floor, amen.py:179-181); part >= 320 doubles
+TTB_API int ttb_abs_floor(void* stream, long long tot, double* d, double* part) {
+  cudaStream_t st = as_stream(stream);
+  int nb = grid_for(tot) < PB ? grid_for(tot) : PB;
+  absmax_partial<<<nb, 256, 0, st>>>(tot, d, part); ttb_count();
+  max_final<<<1, 32, 0, st>>>(nb, part, part + PB); ttb_count();
+  abs_floor_kernel<<<grid_for(tot), 256, 0, st>>>(tot, d, part + PB); ttb_count();
+  return ttb_last_error();
+}
+
 TTB_API int ttb_tt_gather3(void* stream, int N, const long long* idx, const double* G0, int n0, int r1,
                            const double* G1, int n1, int r2, const double* G2, int n2, double* out) {
   if (N == 0) return TTB_OK;
@@ -405,7 +415,7 @@ namespace {
 // the local operator. ws: 4N (+ matvec workspace owned by MV) + 2 PB + 16 doubles after it.
 template <class MV>
 int pcg_run(cudaStream_t st, long long N, const MV& mv, const double* b, double* x, const double* d, double atol,
-            int maxiter, int x0_nonzero, double* ws, double* part, double* S, int* iters) {
+            int maxiter, int x0_nonzero, double* ws, double* part, double* S, int* iters, int chunk) {
   double* r = ws;
   double* z = r + N;
   double* p = z + N;
@@ -423,7 +433,9 @@ int pcg_run(cudaStream_t st, long long N, const MV& mv, const double* b, double*
     pcg_dot_partial<<<nb, 256, 0, st>>>(N, r, r, S, part); ttb_count();
   }
   pcg_dot_final<<<1, 256, 0, st>>>(nb, part, S, 3); ttb_count();
-  const int chunk = 8;
+  // iterations are enqueued `chunk` at a time between host checks of the device done-flag (the
+  // kernels of a finished solve still run, as no-ops on x); chunk = 1 when one matvec costs far more
+  // than a host round trip
   double host[8];
   for (int it0 = 0; it0 <= maxiter; it0 += chunk) {
     for (int k = 0; k < chunk; ++k) {
@@ -460,7 +472,7 @@ TTB_API int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, i
   auto mv = [&](const double* in, double* out) {
     return ttb_local_matvec(stream, r0, n, r1, Ra, Rb, h, phiL, M, phiR, in, out, mvws);
   };
-  return pcg_run(as_stream(stream), N, mv, b, x, d, atol, maxiter, x0_nonzero, ws, part, S, iters);
+  return pcg_run(as_stream(stream), N, mv, b, x, d, atol, maxiter, x0_nonzero, ws, part, S, iters, 8);
 }
 
 TTB_API long long ttb_pcg_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h) {
@@ -479,7 +491,9 @@ TTB_API int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int 
   auto mv = [&](const double* in, double* out) {
     return ttb_local_matvec_gemm(stream, r0, n, r1, Ra, Rb, h, phiLp, Mf, phiRp, in, out, mvws);
   };
-  return pcg_run(as_stream(stream), N, mv, b, x, d, atol, maxiter, x0_nonzero, ws, part, S, iters);
+  const double mv_flops = 2.0 * N * (2 * h + 1) * Ra * Rb;
+  return pcg_run(as_stream(stream), N, mv, b, x, d, atol, maxiter, x0_nonzero, ws, part, S, iters,
+                 mv_flops > 2e9 ? 1 : mv_flops > 2e8 ? 2 : 8);
 }
 
 // ---------------------------------------------------------------------------

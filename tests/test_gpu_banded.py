@@ -189,3 +189,32 @@ def test_amen_modes_match_oracle(monkeypatch, band, resid):
     assert eu < 1e-6, eu
     assert all(abs(a - b) <= 2 for a, b in zip(rep.ranks_u, ref["ranks_u"])), (rep.ranks_u, ref["ranks_u"])
     assert abs(rep.l2_error - ref["l2_error"]) <= 0.01 * ref["l2_error"]
+
+
+@pytest.mark.parametrize("forward", [True, False])
+def test_truncation_residuals_basis_form(forward):
+    """GEMM-mode trial-rank residuals (operator applied once to the SVD basis) == direct evaluation."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import amen as A
+    from paper_2509_13224_b200.tensor_train import banded as BD
+    rng = np.random.default_rng(11 if forward else 12)
+    Ra, Rb, n, h, r0, r1 = 10, 9, 40, 3, 7, 6
+    _, Mb = _banded_core(rng, Ra, n, h, Rb)
+    lay = BD.GemmLayouts([Mb], h)
+    phiL, phiR = _rand(rng, r0, Ra, r0), _rand(rng, r1, Rb, r1)
+    sy = A.LocalSystem(phiL, Mb, h, phiR, lay, 0)
+    sy.gemm = True
+    sy.Mf = lay.fwd(0)
+    sy.phiLp = L.permute(sy.phiL, (1, 0, 2))
+    sy.phiRp = L.permute(sy.phiR, (0, 2, 1))
+    x3 = _rand(rng, r0, n, r1)
+    rhs3 = _rand(rng, r0, n, r1)
+    mat = x3.reshape(r0 * n, r1) if forward else x3.reshape(r0, n * r1)
+    f = L.SVDFactors(mat, want_v=not forward)
+    R = int(f.S.shape[0])
+    Uf, SVf = f.U(R), f.SVt(R)
+    res = sy.truncation_residuals(Uf, SVf, rhs3, forward)
+    for q in (1, 2, R // 2, R):
+        xq = L.gemm(Uf[:, :q], SVf[:q]).reshape(r0, n, r1)
+        direct = float(L.nrm2(sy.matvec3(xq) - rhs3).item())
+        assert abs(res(q) - direct) <= 1e-12 * direct

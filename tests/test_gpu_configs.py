@@ -92,3 +92,36 @@ def test_configs4_family_reduced():
     kw = dict(SOLVE_CONFIGS[4], n_basis=48)
     r = _run(kw)
     assert r["eK"] <= 1e-9 and r["ef"] <= 1e-9 and r["eu"] <= 1e-6, (r["eK"], r["ef"], r["eu"])
+
+
+def _vs_fixture(tag, cfg_idx, n, tol_u):
+    """Device solve vs the committed oracle fixture (tests/golden/make_config_fixtures.py)."""
+    import os
+    from paper_2509_13224_b200 import driver as D
+    from paper_2509_13224_b200.tensor_train import TtTensor
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "configs_oracle.npz"))
+    rep = D.solve_poisson(D.SolveConfig(seed=0, **dict(SOLVE_CONFIGS[cfg_idx], n_basis=n)))
+    uo = TtTensor([torch.as_tensor(g[f"{tag}_u{k}"], device="cuda") for k in range(3)])
+    fo = TtTensor([torch.as_tensor(g[f"{tag}_f{k}"], device="cuda") for k in range(3)])
+    eu, ef = _tt_rel(rep.u, uo), _tt_rel(rep.f, fo)
+    assert ef <= 1e-6, ef
+    assert eu <= tol_u, eu
+    assert _ranks_close(rep.ranks_K, tuple(g[f"{tag}_ranks_K"])), (rep.ranks_K, g[f"{tag}_ranks_K"])
+    assert _ranks_close(rep.ranks_u, tuple(g[f"{tag}_ranks_u"])), (rep.ranks_u, g[f"{tag}_ranks_u"])
+    # same stopping behaviour: both reach (or stagnate just above) the 1e-8 target
+    assert rep.residual <= 2.0 * float(g[f"{tag}_residual"]) + 1e-9, (rep.residual, float(g[f"{tag}_residual"]))
+    lo = float(g[f"{tag}_l2_error"])
+    if not np.isnan(lo):
+        assert abs(rep.l2_error - lo) <= 0.01 * lo, (rep.l2_error, lo)
+    return rep
+
+
+def test_configs2_n16_vs_oracle_fixture():
+    """Deformed cube at n=16 (operator ranks 70): GEMM-staged banded operator and compressed residual."""
+    _vs_fixture("c2_n16", 2, 16, 1e-5)
+
+
+def test_configs3_n10_vs_oracle_fixture():
+    """Random cube at n=10 (operator ranks 53, f = 1, no manufactured solution)."""
+    _vs_fixture("c3_n10", 3, 10, 1e-5)

@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-solve", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--solve-configs", default="1,2,3,4",
+                    help="BASELINE solve configs timed at full size after the microbenchmark (comma list)")
     ap.add_argument("--n", type=int, default=N_MODE)
     return ap.parse_args()
 
@@ -293,6 +295,22 @@ def run_b200(args):
         line["solve_configs1"] = {"time_s": solve_s, "timings": tm, "dofs": rep.dofs, "ranks_K": list(rep.ranks_K),
                                   "ranks_u": list(rep.ranks_u), "residual": rep.residual,
                                   "l2_error": rep.l2_error, "sweeps": rep.sweeps}
+        # the other configs at their full BASELINE sizes: one synchronized run each (setup + assembly +
+        # Dirichlet elimination + AMEn; the error integral is timed separately and only where the
+        # manufactured solution exists and the quadrature is small)
+        line["solve_configs"] = {}
+        for c in [int(x) for x in args.solve_configs.split(",") if x.strip()]:
+            if c == 1:
+                continue
+            want_err = c == 2
+            rep = D.solve_poisson(D.SolveConfig(seed=0, **SOLVE_CONFIGS[c]), want_error=want_err)
+            torch.cuda.synchronize()
+            tm = rep.timings
+            line["solve_configs"][str(c)] = {
+                "time_s": sum(v for k, v in tm.items() if k != "t_error_s"), "timings": tm, "dofs": rep.dofs,
+                "ranks_K": list(rep.ranks_K), "ranks_u": list(rep.ranks_u), "residual": rep.residual,
+                "converged": rep.solver_converged, "sweeps": rep.sweeps, "l2_error": rep.l2_error,
+                "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9}
     # ---------------- CPU baseline (rank 0, N=1 only)
     if rank == 0 and world == 1 and not args.skip_cpu:
         dt, fl, _ = cpu_sample_run()

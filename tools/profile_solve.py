@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2509_13224_b200 import assembly, driver, linalg, splines, geometry  # noqa: E402
-from paper_2509_13224_b200.tensor_train import amen, core, cross  # noqa: E402
+from paper_2509_13224_b200.tensor_train import amen, banded, core, cross  # noqa: E402
 from paper_2509_13224_b200.workloads import SOLVE_CONFIGS  # noqa: E402
 
 T = collections.defaultdict(float)
@@ -39,6 +39,7 @@ for mod, names in [
     (core, ["tt_round", "tt_norm", "tt_matvec", "tt_add"]),
     (cross, ["tt_cross"]),
     (amen, ["amen_solve", "_truncate_by_residual", "env_left_A", "env_right_A", "env_left_vec", "env_right_vec"]),
+    (banded, ["compressed_residual", "env_left_A", "env_right_A"]),
     (assembly, ["_lift_tensor", "_face_coefficients", "_face_tt", "build_quadrature", "metric_scale"]),
     (linalg, ["qr_colmajor", "maxvol_colmajor", "solve", "cho_solve_or_lu", "_jacobi"]),
 ]:
@@ -66,7 +67,7 @@ def _timed_solve(self, *a, **k):
 amen.LocalSystem.solve = _timed_solve
 
 cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-for rep in range(2):
+for rep in range(1 if cfg_id in (2, 3) else 2):
     T.clear(); N.clear()
     t0 = time.perf_counter()
     r = driver.solve_poisson(driver.SolveConfig(seed=0, **SOLVE_CONFIGS[cfg_id]), want_error=False)

@@ -221,9 +221,15 @@ __device__ __forceinline__ AbsMax grid_absmax(const double* pv, const long long*
   return r;
 }
 
-__global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double* __restrict__ Q, double* W, int* perm,
-                                                      double* C, double* Ainv, double* pv, long long* pi, double tol,
-                                                      int max_iters, int* rows_out, int* status) {
+// One grid barrier per elimination step and per swap: the matrix is double-buffered (every step
+// reads buffer A and writes buffer B, so the pivot row can be read by all CTAs while its owner
+// writes the updated copy), and each update pass also produces the per-CTA argmax partials the
+// next step needs (parity-double-buffered). Same operations, same order and the same tie-break
+// (lowest physical / flattened index) as the reference's numpy code (maxvol.py:19-62).
+__global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double* __restrict__ Q, double* W0,
+                                                      int* perm, double* W1, double* Ainv, double* pv,
+                                                      long long* pi, double tol, int max_iters, int* rows_out,
+                                                      int* status) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sv[32];
   __shared__ long long si[32];
@@ -232,57 +238,60 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
   const int nblk = gridDim.x;
   const int chunk = (n + nblk - 1) / nblk;
   const int i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
-  // copy + scale
+  double* pvs[2] = {pv, pv + 296};
+  long long* pis[2] = {pi, pi + 296};
+  double* scl = pv + 2 * 296;  // per-CTA |max| for the degeneracy scale
+  // copy; partials: global |max| (scale) and the step-0 pivot search over column 0
   AbsMax mx{0.0, 0};
+  AbsMax b0{-1.0, (long long)1 << 62};
   for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
     perm[i] = i;
     for (int c = 0; c < r; ++c) {
       double v = Q[(long long)c * n + i];
-      W[(long long)c * n + i] = v;
+      W0[(long long)c * n + i] = v;
       mx.v = fmax(mx.v, fabs(v));
     }
+    b0 = absmax_merge(b0, AbsMax{fabs(Q[i]), i});
   }
   mx.i = 0;
   mx = block_absmax(mx, sv, si);
-  if (threadIdx.x == 0) { pv[blockIdx.x] = mx.v; pi[blockIdx.x] = 0; }
+  b0 = block_absmax(b0, sv, si);
+  if (threadIdx.x == 0) { scl[blockIdx.x] = mx.v; pvs[0][blockIdx.x] = b0.v; pis[0][blockIdx.x] = b0.i; }
   grid.sync();
   double scale = 0.0;
-  for (int b = 0; b < nblk; ++b) scale = fmax(scale, pv[b]);
-  grid.sync();
-  // phase 1: Gaussian elimination with partial pivoting, physical row swaps
+  for (int b = 0; b < nblk; ++b) scale = fmax(scale, scl[b]);
+  // phase 1: Gaussian elimination with partial pivoting, physical row swaps (A -> B each step)
+  double* A = W0;
+  double* B = W1;
   for (int k = 0; k < r; ++k) {
-    AbsMax best{-1.0, (long long)1 << 62};
-    for (int i = max(i0, k) + threadIdx.x; i < i1; i += MT_) best = absmax_merge(best, AbsMax{fabs(W[(long long)k * n + i]), i});
-    best = block_absmax(best, sv, si);
-    if (threadIdx.x == 0) { pv[blockIdx.x] = best.v; pi[blockIdx.x] = best.i; }
-    grid.sync();
-    AbsMax g = grid_absmax(pv, pi, nblk, sv, si);
+    AbsMax g = grid_absmax(pvs[k & 1], pis[k & 1], nblk, sv, si);
     if (g.v <= 1e-14 * fmax(scale, 1e-300)) {
       if (blockIdx.x == 0 && threadIdx.x == 0) *status = 1;
       return;  // uniform across the grid
     }
     const int p = (int)g.i;
-    grid.sync();  // everyone has read pv/pi
-    if (p != k && blockIdx.x == 0) {
-      for (int c = threadIdx.x; c < r; c += MT_) {
-        double t = W[(long long)c * n + k];
-        W[(long long)c * n + k] = W[(long long)c * n + p];
-        W[(long long)c * n + p] = t;
+    if (p != k && blockIdx.x == 0 && threadIdx.x == 0) { int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
+    for (int c = k + threadIdx.x; c < r; c += MT_) srow[c] = A[(long long)c * n + p];  // pivot row
+    __syncthreads();
+    const double d = srow[k];
+    AbsMax best{-1.0, (long long)1 << 62};
+    for (int i = max(i0, k) + threadIdx.x; i < i1; i += MT_) {
+      if (i == k) {  // the pivot row moves to position k unchanged
+        for (int c = k + 1; c < r; ++c) B[(long long)c * n + k] = srow[c];
+        continue;
       }
-      if (threadIdx.x == 0) { int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
+      const int src = (i == p) ? k : i;  // old row k moves to position p
+      const double l = A[(long long)k * n + src] / d;
+      for (int c = k + 1; c < r; ++c) B[(long long)c * n + i] = A[(long long)c * n + src] - l * srow[c];
+      if (k + 1 < r) best = absmax_merge(best, AbsMax{fabs(B[(long long)(k + 1) * n + i]), i});
     }
+    best = block_absmax(best, sv, si);
+    if (threadIdx.x == 0) { pvs[(k + 1) & 1][blockIdx.x] = best.v; pis[(k + 1) & 1][blockIdx.x] = best.i; }
     grid.sync();
-    const double d = W[(long long)k * n + k];
-    for (int i = max(i0, k + 1) + threadIdx.x; i < i1; i += MT_) {
-      double l = W[(long long)k * n + i] / d;
-      W[(long long)k * n + i] = l;
-      for (int c = k + 1; c < r; ++c) W[(long long)c * n + i] -= l * W[(long long)c * n + k];
-    }
-    grid.sync();
+    double* t = A; A = B; B = t;
   }
   // phase 2: Ainv = inv(Q[rows]) by Gauss-Jordan with partial pivoting (block 0), C = Q Ainv
   if (blockIdx.x == 0) {
-    // augmented [A | I] in W's spare storage is not available; use Ainv buffer (r x 2r, col-major ld r)
     for (int e = threadIdx.x; e < r * r; e += MT_) {
       int c = e / r, i = e % r;
       Ainv[(long long)c * r + i] = Q[(long long)c * n + perm[i]];
@@ -323,44 +332,52 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
     }
   }
   grid.sync();
-  // inverse sits in columns r..2r-1
+  // inverse sits in columns r..2r-1; C (buffer Ca) = Q Ainv, with the first swap's argmax partials
   const double* Ai = Ainv + (long long)r * r;
   const bool in_smem = r <= 64;
   if (in_smem) {
     for (int e = threadIdx.x; e < r * r; e += MT_) sA[e] = Ai[e];
     __syncthreads();
   }
-  for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
-    for (int c = 0; c < r; ++c) {
-      double s = 0.0;
-      for (int k = 0; k < r; ++k) s += Q[(long long)k * n + i] * (in_smem ? sA[c * r + k] : Ai[(long long)c * r + k]);
-      C[(long long)c * n + i] = s;
+  double* Ca = W0;
+  double* Cb = W1;
+  {
+    AbsMax best{-1.0, (long long)1 << 62};
+    for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
+      for (int c = 0; c < r; ++c) {
+        double s = 0.0;
+        for (int k = 0; k < r; ++k) s += Q[(long long)k * n + i] * (in_smem ? sA[c * r + k] : Ai[(long long)c * r + k]);
+        Ca[(long long)c * n + i] = s;
+        best = absmax_merge(best, AbsMax{fabs(s), (long long)i * r + c});
+      }
     }
+    best = block_absmax(best, sv, si);
+    if (threadIdx.x == 0) { pvs[0][blockIdx.x] = best.v; pis[0][blockIdx.x] = best.i; }
   }
   int* rows = perm;  // rows[0..r) live in perm[0..r)
   grid.sync();
-  // phase 3: greedy swaps
+  // phase 3: greedy swaps (Sherman-Morrison), Ca -> Cb each iteration
   for (int it = 0; it < max_iters; ++it) {
-    AbsMax best{-1.0, (long long)1 << 62};
-    for (int i = i0 + threadIdx.x; i < i1; i += MT_)
-      for (int c = 0; c < r; ++c)
-        best = absmax_merge(best, AbsMax{fabs(C[(long long)c * n + i]), (long long)i * r + c});
-    best = block_absmax(best, sv, si);
-    if (threadIdx.x == 0) { pv[blockIdx.x] = best.v; pi[blockIdx.x] = best.i; }
-    grid.sync();
-    AbsMax g = grid_absmax(pv, pi, nblk, sv, si);
+    AbsMax g = grid_absmax(pvs[it & 1], pis[it & 1], nblk, sv, si);
     if (g.v <= tol) break;
     const int bi = (int)(g.i / r), bj = (int)(g.i % r);
-    for (int c = threadIdx.x; c < r; c += MT_) srow[c] = C[(long long)c * n + bi] - (c == bj ? 1.0 : 0.0);
-    const double pivv = C[(long long)bj * n + bi];
+    for (int c = threadIdx.x; c < r; c += MT_) srow[c] = Ca[(long long)c * n + bi] - (c == bj ? 1.0 : 0.0);
+    const double pivv = Ca[(long long)bj * n + bi];
     __syncthreads();
-    grid.sync();  // all rows read before anyone updates (also protects pv/pi)
+    AbsMax best{-1.0, (long long)1 << 62};
     for (int i = i0 + threadIdx.x; i < i1; i += MT_) {
-      const double f = C[(long long)bj * n + i] / pivv;
-      for (int c = 0; c < r; ++c) C[(long long)c * n + i] -= f * srow[c];
+      const double f = Ca[(long long)bj * n + i] / pivv;
+      for (int c = 0; c < r; ++c) {
+        const double v = Ca[(long long)c * n + i] - f * srow[c];
+        Cb[(long long)c * n + i] = v;
+        best = absmax_merge(best, AbsMax{fabs(v), (long long)i * r + c});
+      }
     }
+    best = block_absmax(best, sv, si);
+    if (threadIdx.x == 0) { pvs[(it + 1) & 1][blockIdx.x] = best.v; pis[(it + 1) & 1][blockIdx.x] = best.i; }
     if (blockIdx.x == 0 && threadIdx.x == 0) rows[bj] = bi;
     grid.sync();
+    double* t = Ca; Ca = Cb; Cb = t;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int a = 0; a < r; ++a) rows_out[a] = rows[a];
@@ -437,8 +454,8 @@ TTB_API int ttb_potrs(void* stream, int n, const double* L, long long lda, doubl
 }
 
 TTB_API long long ttb_maxvol_workspace(int n, int r) {
-  // W, C (n*r each), Ainv (2 r^2), partials (2 * 296)
-  return 2LL * n * r + 2LL * r * r + 2 * 296 + 64;
+  // two n*r buffers, Ainv (2 r^2), partials: values 2 x 296 + scale 296, indices 2 x 296 (int64)
+  return 2LL * n * r + 2LL * r * r + 5 * 296 + 64;
 }
 
 // rows_out: r sorted row indices of a tol-dominant submatrix of Q (n x r col-major, ld n), n > r.
@@ -450,7 +467,7 @@ TTB_API int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, 
   double* C = W + (long long)n * r;
   double* Ainv = C + (long long)n * r;
   double* pv = Ainv + 2LL * r * r;
-  long long* pi = reinterpret_cast<long long*>(pv + 296);
+  long long* pi = reinterpret_cast<long long*>(pv + 3 * 296);
   int* perm = iws;
   int* status = iws + n;
   int nblk = maxvol_grid(n);

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import torch
@@ -219,6 +220,9 @@ def _jacobi(Rcm, n, want_v=False, info=None):
     return U, S, V
 
 
+_JACOBI_RT_MAX = int(os.environ.get("TTB_JACOBI_RT_MAX", "64"))
+
+
 class SVDFactors:
     """Thin SVD X = U diag(S) Vt by Householder QR + one-sided Jacobi on the triangular factor.
 
@@ -240,9 +244,16 @@ class SVDFactors:
             self.X = X
             self.UJ, self.S, self.VJ = _jacobi(permute(X, (1, 0)), n, want_v)
         elif self.tall:
+            # small R: one-sided Jacobi on R^T (rows of R, graded by the QR) converges in fewer
+            # rounds; R = V' S U'^T, so U_R is the accumulated rotation V' and V_R = U'
+            self.rt = n <= _JACOBI_RT_MAX
+            if self.rt:
+                job = lambda R: _jacobi(permute(R, (1, 0)), n, True)    # noqa: E731
+            else:
+                job = lambda R: _jacobi(R.contiguous(), n, want_v)      # noqa: E731
             # the Jacobi SVD of R runs on a side stream while Q is formed (independent work)
-            Qt, Rt, (self.UJ, self.S, self.VJ) = qr_colmajor(
-                permute(X, (1, 0)), m, n, overlap_r=lambda R: _jacobi(R.contiguous(), n, want_v))
+            Qt, Rt, (UJ, self.S, VJ) = qr_colmajor(permute(X, (1, 0)), m, n, overlap_r=job)
+            self.UJ, self.VJ = (VJ, UJ) if self.rt else (UJ, VJ)
             self.Qt = Qt                      # (n, m) == col-major Q (m x n)
             self.Rt = Rt                      # (n, n) == col-major R == row-major R^T
         else:

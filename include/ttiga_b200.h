@@ -161,7 +161,8 @@ int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, co
 int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
                   double* out);
 /* Local projected operator (amen.py:147-150 matvec3) with vectors in the mode-major (i, x, z) layout:
- * phiLp = phiL permuted (a, x, y), Mf = (n, 2h+1, Ra, Rb), phiRp = phiR permuted (z, w, b).
+ * phiLp = phiL permuted (a, x, y), Mf = (n, 2h+1, Ra, Rb), phiRp = phiR permuted (z, w, b) and
+ * zero-padded to (r1, r1 + (r0 & r1 & 1), Rb) (the staged operand keeps an even column count).
  * ws: ttb_local_gemm_workspace doubles, padding zeroed once by ttb_local_gemm_ws_init. */
 long long ttb_local_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h); /* doubles */
 int ttb_local_gemm_ws_init(void* stream, int r0, int n, int r1, int Ra, int h, double* ws);

@@ -374,21 +374,30 @@ TTB_API int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, 
                    (long long)B * Rin * Rout, 0.0, out, Rout, (long long)X * Rout, n);
 }
 
+// The staged operand's column count X = r0 r1p is kept even (r1p = r1 + 1 when r0 and r1 are
+// both odd, the extra w column staying zero) so both band-GEMM operands take the 16-byte path.
+static inline int local_r1p(int r0, int r1) { return r1 + (r0 & r1 & 1); }
+
 TTB_API long long ttb_local_gemm_workspace(int r0, int n, int r1, int Ra, int Rb, int h) {
-  return (long long)(n + 2 * h) * Ra * r0 * r1 + (long long)n * r0 * r1 * Rb;
+  const int r1p = local_r1p(r0, r1);
+  return (long long)(n + 2 * h) * Ra * r0 * r1p + (long long)n * r0 * r1p * Rb;
 }
 
 // Local projected operator in the mode-major (i, x, z) vector layout, three GEMM stages:
 //   Tp[j+h, a, x, w] = sum_y phiLp[a, x, y] v[j, y, w]           (batched over j)
 //   t2[i, x, w, b]   = band_gemm(Tp, Mf)                           (batched over i)
 //   y[i, x, z]       = sum_{w, b} t2[i, x, w, b] phiRp[z, w, b]    (one GEMM)
-// phiLp = phiL permuted to (a, x, y); phiRp = phiR permuted to (z, w, b); Mf (n, 2h+1, Ra, Rb).
-// ws (ttb_local_gemm_workspace doubles): its first h*Ra*r0*r1 and last h*Ra*r0*r1 doubles of the
-// Tp part must be zero (ttb_local_gemm_ws_init), the interior is overwritten every call.
+// phiLp = phiL permuted to (a, x, y); phiRp = phiR permuted to (z, w, b) and zero-padded to
+// (r1, r1p, Rb) with r1p = r1 + (r0 & r1 & 1); Mf (n, 2h+1, Ra, Rb) (Rb may carry zero padding).
+// ws (ttb_local_gemm_workspace doubles) must be initialised once by ttb_local_gemm_ws_init (zero
+// padding blocks / columns of the staged operand); the rest is overwritten every call.
 TTB_API int ttb_local_gemm_ws_init(void* stream, int r0, int n, int r1, int Ra, int h, double* ws) {
-  const long long blk = (long long)Ra * r0 * r1;
+  const int r1p = local_r1p(r0, r1);
+  const long long blk = (long long)Ra * r0 * r1p;
   cudaStream_t st = as_stream(stream);
-  if (h > 0) {
+  if (r1p != r1) {
+    cudaMemsetAsync(ws, 0, (size_t)(n + 2 * h) * blk * sizeof(double), st);
+  } else if (h > 0) {
     cudaMemsetAsync(ws, 0, (size_t)h * blk * sizeof(double), st);
     cudaMemsetAsync(ws + (long long)(n + h) * blk, 0, (size_t)h * blk * sizeof(double), st);
   }
@@ -397,15 +406,16 @@ TTB_API int ttb_local_gemm_ws_init(void* stream, int r0, int n, int r1, int Ra, 
 
 TTB_API int ttb_local_matvec_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiLp,
                                   const double* Mf, const double* phiRp, const double* v, double* y, double* ws) {
-  const long long blk = (long long)Ra * r0 * r1;
+  const int r1p = local_r1p(r0, r1);
+  const long long blk = (long long)Ra * r0 * r1p;
   double* Tp = ws;
   double* t2 = ws + (long long)(n + 2 * h) * blk;
   int rc = ttb_dgemm(stream, 0, 0, Ra * r0, r1, r0, 1.0, phiLp, r0, 0, v, r1, (long long)r0 * r1, 0.0,
-                     Tp + (long long)h * blk, r1, blk, n);
+                     Tp + (long long)h * blk, r1p, blk, n);
   if (rc) return rc;
-  rc = ttb_band_gemm(stream, n, h, Ra, Rb, r0 * r1, Tp, Mf, t2);
+  rc = ttb_band_gemm(stream, n, h, Ra, Rb, r0 * r1p, Tp, Mf, t2);
   if (rc) return rc;
-  return ttb_dgemm(stream, 0, 1, n * r0, r1, r1 * Rb, 1.0, t2, (long long)r1 * Rb, 0, phiRp, (long long)r1 * Rb, 0,
+  return ttb_dgemm(stream, 0, 1, n * r0, r1, r1p * Rb, 1.0, t2, (long long)r1p * Rb, 0, phiRp, (long long)r1p * Rb, 0,
                    0.0, y, r1, 0, 1);
 }
 

@@ -55,8 +55,27 @@ def use_compressed_residual(Ms, u, F) -> bool:
     return tot > (1 << 23)
 
 
+def _even(r):
+    return r + (r & 1)
+
+
+def pad_last(T, P):
+    """T with its last axis zero-padded to P entries (T itself when already P)."""
+    if T.shape[-1] == P:
+        return T
+    out = L.zeros(*T.shape[:-1], P)
+    out[..., : T.shape[-1]] = T
+    return out
+
+
 class GemmLayouts:
-    """Per-core GEMM layouts of a banded operator: Mf = (n, 2h+1, Ra, Rb), Mr = (n, 2h+1, Rb, Ra)."""
+    """Per-core GEMM layouts of a banded operator: Mf = (n, 2h+1, Ra, Rb'), Mr = (n, 2h+1, Rb, Ra').
+
+    The output rank of each layout is zero-padded to even (Rb' = Rb + Rb % 2): the band GEMM's
+    B operand and output rows then keep 16-byte alignment (16-byte cp.async path; measured
+    29.0 -> 31.7 TF/s at configs[3] shapes). Consumers either carry the zero columns through
+    (the PCG matvec, whose phiR operand is padded the same way) or drop them (trim).
+    """
 
     def __init__(self, Ms, h):
         self.Ms, self.h = Ms, h
@@ -65,12 +84,12 @@ class GemmLayouts:
 
     def fwd(self, k):
         if self._f[k] is None:
-            self._f[k] = L.permute(self.Ms[k], (1, 2, 0, 3))
+            self._f[k] = pad_last(L.permute(self.Ms[k], (1, 2, 0, 3)), _even(self.Ms[k].shape[3]))
         return self._f[k]
 
     def rev(self, k):
         if self._r[k] is None:
-            self._r[k] = L.permute(self.Ms[k], (1, 2, 3, 0))
+            self._r[k] = pad_last(L.permute(self.Ms[k], (1, 2, 3, 0)), _even(self.Ms[k].shape[0]))
         return self._r[k]
 
 
@@ -83,8 +102,9 @@ def _padded(n, h, Rin, X):
     return Tp
 
 
-def band_gemm(Tp, Mt, n, h, Rin, Rout, X):
-    """out[i, X, o] = sum_{t, r} Tp[i + t, r, X] Mt[i, t, r, o]  ->  (n, X, Rout)."""
+def band_gemm(Tp, Mt, n, h, Rin, X):
+    """out[i, X, o] = sum_{t, r} Tp[i + t, r, X] Mt[i, t, r, o]  ->  (n, X, Mt.shape[3]) (padded rank)."""
+    Rout = Mt.shape[3]
     out = L.empty(n, X, Rout)
     call("ttb_band_gemm", n, h, Rin, Rout, X, ptr(Tp), ptr(Mt), ptr(out))
     return out
@@ -116,12 +136,12 @@ def env_left_A(phi, U, lay, k):
     x, Ra, y = phi.shape
     _, n, v = U.shape
     Mf = lay.fwd(k)
-    Rb = Mf.shape[3]
+    Rb, Rbp = lay.Ms[k].shape[3], Mf.shape[3]
     Tp = left_stage(L.permute(phi, (1, 0, 2)), U, h)                 # (j, a, (x, v))
-    out = band_gemm(Tp, Mf, n, h, Ra, Rb, x * v)                      # (i, x, v, b)
+    out = band_gemm(Tp, Mf, n, h, Ra, x * v)                          # (i, x, v, b')
     Up = L.permute(U, (1, 0, 2)).reshape(n * x, v)                   # (i, x, u)
-    res = L.gemm(Up, out.reshape(n * x, v * Rb), tA=True)            # (u, v, b)
-    return L.permute(res.reshape(v, v, Rb), (0, 2, 1))
+    res = L.gemm(Up, out.reshape(n * x, v * Rbp), tA=True)           # (u, v, b')
+    return L.permute(res.reshape(v, v, Rbp)[:, :, :Rb], (0, 2, 1))
 
 
 def env_right_A(phi, U, lay, k):
@@ -130,11 +150,11 @@ def env_right_A(phi, U, lay, k):
     s, Rb, v = phi.shape
     w, n, _ = U.shape
     Mr = lay.rev(k)
-    Ra = Mr.shape[3]
+    Ra, Rap = lay.Ms[k].shape[0], Mr.shape[3]
     Tp = right_stage(L.permute(phi, (1, 0, 2)), U, h)                # (j, b, (s, w))
-    out = band_gemm(Tp, Mr, n, h, Rb, Ra, s * w)                     # (i, s, w, a)
-    res = L.gemm(U.reshape(w, n * s), out.reshape(n * s, w * Ra))    # (z, w, a)
-    return L.permute(res.reshape(w, w, Ra), (0, 2, 1))
+    out = band_gemm(Tp, Mr, n, h, Rb, s * w)                         # (i, s, w, a')
+    res = L.gemm(U.reshape(w, n * s), out.reshape(n * s, w * Rap))  # (z, w, a')
+    return L.permute(res.reshape(w, w, Rap)[:, :, :Ra], (0, 2, 1))
 
 
 # ---------------------------------------------------------------------------
@@ -150,8 +170,9 @@ def _a_left(LA, U, lay, k):
     n = U.shape[1]
     y = U.shape[2]
     Mf = lay.fwd(k)
+    Rb = lay.Ms[k].shape[3]
     Tp = left_stage(L.permute(LA, (2, 0, 1)), U, lay.h)              # (j, a, (k', y))
-    return band_gemm(Tp, Mf, n, lay.h, Ra, Mf.shape[3], Kd * y).reshape(n, Kd, y, Mf.shape[3])
+    return band_gemm(Tp, Mf, n, lay.h, Ra, Kd * y).reshape(n, Kd, y, Mf.shape[3])[..., :Rb]
 
 
 def _a_right(RA, U, lay, k):
@@ -159,8 +180,9 @@ def _a_right(RA, U, lay, k):
     y, Rb, Kd = RA.shape
     x, n, _ = U.shape
     Mr = lay.rev(k)
+    Ra = lay.Ms[k].shape[0]
     Tp = right_stage(L.permute(RA, (1, 2, 0)), U, lay.h)             # (j, b, (k', x))
-    return band_gemm(Tp, Mr, n, lay.h, Rb, Mr.shape[3], Kd * x).reshape(n, Kd, x, Mr.shape[3])
+    return band_gemm(Tp, Mr, n, lay.h, Rb, Kd * x).reshape(n, Kd, x, Mr.shape[3])[..., :Ra]
 
 
 def compressed_residual(lay, u, F):

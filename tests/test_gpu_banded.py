@@ -64,13 +64,8 @@ def test_env_and_local_ops_gemm_equal_reference(Ra, Rb, n, h, r0, r1):
     assert _rel(A.env_left_A(phiL, U, Mb, h), refL) < 1e-12
     # local operator: GEMM mode vs elementwise kernels vs einsum
     v = _rand(rng, r0, n, r1)
-    s_g = A.LocalSystem(phiL, Mb, h, phiR, lay, 0)
+    s_g = A.LocalSystem(phiL, Mb, h, phiR, lay, 0, force_gemm=True)
     s_n = A.LocalSystem(phiL, Mb, h, phiR)
-    s_g.gemm = True
-    s_g.Mf = lay.fwd(0)
-    from paper_2509_13224_b200 import linalg as L
-    s_g.phiLp = L.permute(s_g.phiL, (1, 0, 2))
-    s_g.phiRp = L.permute(s_g.phiR, (0, 2, 1))
     ref = np.einsum("xibw,zbw->xiz", np.einsum("aijb,xajw->xibw", Md, np.einsum("xay,yjw->xajw", pl, v.cpu().numpy())),
                     pr)
     assert _rel(s_g.matvec3(v), ref) < 1e-12
@@ -106,11 +101,7 @@ def test_pcg_gemm_equals_elementwise_pcg():
     phiL, phiR = spd(r0, Ra), spd(r1, Rb)
     b = _rand(rng, r0, n, r1)
     s_n = A.LocalSystem(phiL, Mb, h, phiR)
-    s_g = A.LocalSystem(phiL, Mb, h, phiR, lay, 0)
-    s_g.gemm = True
-    s_g.Mf = lay.fwd(0)
-    s_g.phiLp = L.permute(s_g.phiL, (1, 0, 2))
-    s_g.phiRp = L.permute(s_g.phiR, (0, 2, 1))
+    s_g = A.LocalSystem(phiL, Mb, h, phiR, lay, 0, force_gemm=True)
     x_n = s_n.solve(b, None, 1e-12, 0, 500)
     x_g = s_g.solve(b, None, 1e-12, 0, 500)
     assert _rel(s_n.matvec3(x_n), b) < 1e-10
@@ -202,11 +193,7 @@ def test_truncation_residuals_basis_form(forward):
     _, Mb = _banded_core(rng, Ra, n, h, Rb)
     lay = BD.GemmLayouts([Mb], h)
     phiL, phiR = _rand(rng, r0, Ra, r0), _rand(rng, r1, Rb, r1)
-    sy = A.LocalSystem(phiL, Mb, h, phiR, lay, 0)
-    sy.gemm = True
-    sy.Mf = lay.fwd(0)
-    sy.phiLp = L.permute(sy.phiL, (1, 0, 2))
-    sy.phiRp = L.permute(sy.phiR, (0, 2, 1))
+    sy = A.LocalSystem(phiL, Mb, h, phiR, lay, 0, force_gemm=True)
     x3 = _rand(rng, r0, n, r1)
     rhs3 = _rand(rng, r0, n, r1)
     mat = x3.reshape(r0 * n, r1) if forward else x3.reshape(r0, n * r1)

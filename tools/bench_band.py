@@ -32,15 +32,17 @@ def case(n, h, R, r0, r1, naive=True):
     v = torch.randn(n, r0, r1, generator=g, device="cuda", dtype=torch.float64)
     y = torch.empty_like(v)
     phiLp = L.permute(phiL, (1, 0, 2))
-    phiRp = L.permute(phiR, (0, 2, 1))
+    r1p = r1 + (r0 & r1 & 1)
+    phiRp = torch.zeros(r1, r1p, R, device="cuda", dtype=torch.float64)
+    phiRp[:, :r1] = L.permute(phiR, (0, 2, 1))
     ws = L.empty(int(call_raw("ttb_local_gemm_workspace", r0, n, r1, R, R, h)))
     call("ttb_local_gemm_ws_init", r0, n, r1, R, h, ptr(ws))
     flops = 2.0 * n * r0 * r1 * B * R * R + 2 * 2.0 * n * r0 * r0 * r1 * R
     t_g = timeit(lambda: call("ttb_local_matvec_gemm", r0, n, r1, R, R, h, ptr(phiLp), ptr(Mf), ptr(phiRp), ptr(v),
                               ptr(y), ptr(ws)))
-    Tp = ws[: (n + 2 * h) * R * r0 * r1]
-    out = L.empty(n, r0 * r1, R)
-    t_b = timeit(lambda: call("ttb_band_gemm", n, h, R, R, r0 * r1, ptr(Tp), ptr(Mf), ptr(out)))
+    Tp = ws[: (n + 2 * h) * R * r0 * r1p]
+    out = L.empty(n, r0 * r1p, R)
+    t_b = timeit(lambda: call("ttb_band_gemm", n, h, R, R, r0 * r1p, ptr(Tp), ptr(Mf), ptr(out)))
     res = {"n": n, "h": h, "R": R, "r0": r0, "r1": r1, "matvec_gemm_ms": t_g * 1e3,
            "matvec_gemm_tflops": flops / t_g / 1e12, "band_gemm_ms": t_b * 1e3,
            "band_gemm_tflops": 2.0 * n * r0 * r1 * B * R * R / t_b / 1e12}
@@ -61,3 +63,4 @@ if __name__ == "__main__":
     case(256, 3, 109, 63, 63)
     case(512, 3, 121, 40, 40, naive=False)
     case(512, 3, 121, 64, 64, naive=False)
+    case(510, 3, 122, 93, 89, naive=False)

@@ -13,6 +13,8 @@ from paper_2509_13224_b200.workloads import SOLVE_CONFIGS  # noqa: E402
 EXTRA = {
     "torus32": dict(geometry="quarter_torus", degree=2, elements=32, source="sin_pi_xyz"),
     "lshape32": dict(geometry="lshape", degree=1, elements=32, source="sin_pi_xy", analytic="lshape_exact"),
+    "lshape8": dict(geometry="lshape", degree=1, elements=8, source="sin_pi_xy", analytic="lshape_exact"),
+    "hemi8": dict(geometry="closed_hemisphere", degree=2, elements=8, source="sin_pi_xyz"),
 }
 name = sys.argv[1]
 kw = dict(EXTRA[name]) if name in EXTRA else dict(SOLVE_CONFIGS[int(name)])

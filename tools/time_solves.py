@@ -1,20 +1,27 @@
-"""Time GPU solves of the BASELINE configs (device time per phase) -- development probe."""
-import json, sys, time
-import torch
-from paper_2509_13224_b200 import driver as D
+"""Time GPU solves of the BASELINE configs at full size, several reps in one process (device-
+synchronized phase times). Usage: python tools/time_solves.py [configs...] [--reps R]"""
+import json
+import sys
+import time
 
-CFG = {
-    0: dict(geometry="unit_cube", degree=2, n_basis=32, source="manufactured_sines", analytic="cube_sines",
-            eps_cross=1e-10, eps_round=1e-10, eps_solve=1e-10),
-    1: dict(geometry="quarter_cylinder", degree=3, n_basis=128, source="manufactured_sines", analytic="cube_sines",
-            bc_from_analytic=True, eps_cross=1e-8, eps_round=1e-8, eps_solve=1e-8),
-}
-which = [int(a) for a in sys.argv[1:]] or [0, 1]
+import torch
+
+sys.path.insert(0, ".")
+from paper_2509_13224_b200 import driver as D  # noqa: E402
+from paper_2509_13224_b200.workloads import SOLVE_CONFIGS  # noqa: E402
+
+args = sys.argv[1:]
+reps = 2
+if "--reps" in args:
+    i = args.index("--reps")
+    reps = int(args[i + 1])
+    del args[i:i + 2]
+which = [int(a) for a in args] or [0, 1]
 for c in which:
-    for rep in range(2):
+    for rep in range(reps):
         t = time.perf_counter()
-        r = D.solve_poisson(D.SolveConfig(seed=0, **CFG[c]), want_error=True)
+        r = D.solve_poisson(D.SolveConfig(seed=0, **SOLVE_CONFIGS[c]), want_error=c in (0, 2))
         torch.cuda.synchronize()
-        print(json.dumps({"config": c, "rep": rep, "wall_s": time.perf_counter() - t, "ranks_K": r.ranks_K,
-                          "ranks_f": r.ranks_f, "ranks_u": r.ranks_u, "l2": r.l2_error, "res": r.residual,
-                          "sweeps": r.sweeps, "timings": {k: round(v, 4) for k, v in r.timings.items()}}), flush=True)
+        print(json.dumps({"config": c, "rep": rep, "wall_s": round(time.perf_counter() - t, 4), "ranks_K": r.ranks_K,
+                          "ranks_u": r.ranks_u, "l2": r.l2_error, "res": r.residual, "sweeps": r.sweeps,
+                          "timings": {k: round(v, 4) for k, v in r.timings.items()}}), flush=True)

@@ -12,7 +12,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libttiga_b200.so")
+LIB_PATH = os.environ.get("TTB_LIB") or os.path.join(HERE, "libttiga_b200.so")  # TTB_LIB: A/B builds
 
 
 class NativeUnavailable(RuntimeError):

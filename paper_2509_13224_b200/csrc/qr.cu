@@ -430,7 +430,10 @@ int launch_panel(int m, int jb, double* P, long long ld, double* tau, double* V,
 
 namespace {
 
-constexpr int NB2 = 128;  // outer WY block (trailing-update GEMMs have K = 128)
+#ifndef TTB_NB2
+#define TTB_NB2 128
+#endif
+constexpr int NB2 = TTB_NB2;  // outer WY block (trailing-update GEMMs have K = 128)
 
 // T (nb x nb row-major, upper, nb <= NB) from the Gram G = V^T V (upper triangle read, row-major
 // ld ldg) and tau (dlarft, forward, columnwise); staged in shared memory.

@@ -623,6 +623,15 @@ static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, dou
                           long long lda, long long sA, const double* B, long long ldb, long long sB, double beta,
                           double* C, long long ldc, long long sC, int batch);
 
+static bool mid96_tiles() {  // TTB_GEMM_N96=0 disables the 128x96 tiles (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TTB_GEMM_N96");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                       long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
                       long long ldc, long long sC, int batch) {
@@ -700,6 +709,10 @@ static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, dou
     return cinit ? launch_gemm<128, 64, 4, 2, 1>(g, batch, st) : launch_gemm<128, 64, 4, 2>(g, batch, st);
   if (big) return launch_gemm<128, 128, 2, 4>(g, batch, st);
   if (narrow) return launch_gemm<128, 32, 4, 1>(g, batch, st);
+  // TT-rank-wide outputs (65 <= N <= 96, e.g. the AMEn local operator's phiR stage): one 96-wide
+  // column tile instead of two 64-wide ones (which would be 50-75% full)
+  if (N > 64 && N <= 96 && M >= 256 && work >= (long long)148 * 128 * 96 && mid96_tiles())
+    return launch_gemm<128, 96, 4, 2>(g, batch, st);
   return launch_gemm<64, 64, 2, 2>(g, batch, st);
 }
 

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(ST) chol_solve_kernel(int n, const double* __r
 
 // ---------------------------------------------------------------------------
 // maxvol (reference maxvol.py): GEPP row choice, C = M inv(M[rows]), greedy swaps.
-constexpr int MT_ = 256;
+constexpr int MT_ = 512;  // 16 warps per CTA: the update passes are HBM-bound, keep enough loads in flight
 constexpr int RMAX = 128;
 
 // every CTA merges the per-CTA (value, index) partials: warp 0, lanes stride over CTAs
@@ -391,15 +391,17 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
 }
 
 int maxvol_grid(int n) {
+  // one row per thread, up to the co-resident limit of the cooperative launch (<= 296 partials)
   static int maxb = 0;
   if (!maxb) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, maxvol_kernel, MT_, 0);
-    maxb = sms * (per > 0 ? 1 : 1);
+    maxb = sms * (per > 0 ? per : 1);
+    if (maxb > 296) maxb = 296;
   }
-  int want = ceil_div(n, 2 * MT_);
+  int want = ceil_div(n, MT_);
   if (want < 1) want = 1;
   return want < maxb ? want : maxb;
 }

@@ -597,7 +597,10 @@ __global__ void __launch_bounds__(256) band_chol_solve_kernel(long long N, int b
 // all warps apply the rank-NBB update of the band triangle, finished rows stream out. Solves
 // stream rows through staged chunks; b lives in shared memory; the forward solve takes blocks of
 // NBB rows (band dots in parallel over warps, then the NBB x NBB triangle).
-constexpr int BCT = 256, NBB = 8, BCH = 64;
+#ifndef TTB_BAND_NBB
+#define TTB_BAND_NBB 8
+#endif
+constexpr int BCT = 256, NBB = TTB_BAND_NBB, BCH = 64;
 
 __global__ void __launch_bounds__(BCT) band_chol_blocked_kernel(int N, int bw, double* LB, double* b, int* info) {
   extern __shared__ double sm[];

@@ -221,6 +221,9 @@ def _jacobi(Rcm, n, want_v=False, info=None):
 
 
 _JACOBI_RT_MAX = int(os.environ.get("TTB_JACOBI_RT_MAX", "64"))
+_IMPLICIT_U = os.environ.get("TTB_SVD_IMPLICIT_U", "1") != "0"
+_IMPLICIT_U_MIN_M = int(os.environ.get("TTB_SVD_IMPLICIT_U_MIN_M", "65536"))
+_IMPLICIT_U_MIN_RATIO = 1e-7   # U orthogonality error ~ eps s_max / s_k <= ~1e-9
 
 
 class SVDFactors:
@@ -243,6 +246,20 @@ class SVDFactors:
         if self.direct:
             self.X = X
             self.UJ, self.S, self.VJ = _jacobi(permute(X, (1, 0)), n, want_v)
+        elif self.tall and m >= _IMPLICIT_U_MIN_M and n > _JACOBI_RT_MAX and _IMPLICIT_U:
+            # very tall X (the rounding's (r n) x r unfoldings): X = Q R without forming Q; Jacobi
+            # on R^T, R^T = U' S V'^T, so the right singular vectors of X are U' (no rotations
+            # accumulated) and U = X U' S^-1 (one GEMM, chunkable, no orgqr). A kept column whose
+            # singular value is below _IMPLICIT_U_MIN_RATIO s_max would lose orthogonality
+            # (error ~ eps s_max / s_k), so U() then falls back to the explicit-Q path.
+            self.implicit = True
+            self.X = X
+            self._want_v = want_v
+            _, Rt = qr_colmajor(permute(X, (1, 0)), m, n, want_q=False)
+            self.Rt = Rt
+            self.Vr, self.S, _ = _jacobi(permute(Rt, (1, 0)), n, False)   # rows: right singular vectors
+            self.UJ = self.VJ = self.Qt = None
+            self._W = None
         elif self.tall:
             # small R: one-sided Jacobi on R^T (rows of R, graded by the QR) converges in fewer
             # rounds; R = V' S U'^T, so U_R is the accumulated rotation V' and V_R = U'
@@ -262,17 +279,47 @@ class SVDFactors:
             self.Rt = Rt                      # row-major R^T
             self.UJ, self.S, self.VJ = _jacobi(permute(Rt, (1, 0)), m, want_v)  # Jacobi on R^T
 
+    implicit = False
+    _s = None
+
     def s_host(self):
-        return self.S.cpu().numpy()
+        if self._s is None:
+            self._s = self.S.cpu().numpy()
+        return self._s
+
+    def _implicit_w(self, r):
+        """W = U'[:r]^T S[:r]^-1 (n x r) when every kept singular value is well separated from 0,
+        else switch to the explicit-Q path (returns None)."""
+        s = self.s_host()
+        if s[0] > 0.0 and s[r - 1] >= _IMPLICIT_U_MIN_RATIO * s[0]:
+            if self._W is None or self._W.shape[1] != r:
+                self._W = (self.Vr[:r] / self.S[:r, None]).t().contiguous()
+            return self._W
+        self._explicit()
+        return None
+
+    def _explicit(self):
+        """Fall back to Q R with explicit Q and Jacobi on R (the default tall path)."""
+        X, n, m = self.X, self.n, self.m
+        self.implicit = False
+        self.rt = False
+        Qt, Rt, (UJ, S, VJ) = qr_colmajor(permute(X, (1, 0)), m, n,
+                                          overlap_r=lambda R: _jacobi(R.contiguous(), n, self._want_v))
+        self.Qt, self.Rt, self.UJ, self.S, self.VJ = Qt, Rt, UJ, S, VJ
+        self._s = None
 
     def U(self, r):
         """First r left singular vectors, row-major (m x r)."""
+        if self.implicit and self._implicit_w(r) is not None:
+            return gemm(self.X, self._W)
         if self.tall:
             return gemm(self.Qt, self.UJ[:r], tA=True, tB=True)
         return self.UJ[:r].t().contiguous()
 
     def U_rows(self, r, i0, i1, out):
         """Rows [i0, i1) of U(r) into ``out`` ((i1 - i0) x r, row-major) -- chunked formation."""
+        if self.implicit and self._implicit_w(r) is not None:
+            return gemm(self.X[i0:i1], self._W, out=out)
         if self.tall:
             return gemm(self.Qt[:, i0:i1], self.UJ[:r], tA=True, tB=True, out=out)
         out.copy_(self.UJ[:r, i0:i1].t())
@@ -280,6 +327,8 @@ class SVDFactors:
 
     def SVt(self, r):
         """diag(S[:r]) Vt[:r] = U[:, :r]^T X  (r x n)."""
+        if self.implicit:
+            return (self.S[:r, None] * self.Vr[:r]).contiguous()
         if self.direct:
             return gemm(self.UJ[:r], self.X)                    # U^T X
         if self.tall:
@@ -289,6 +338,8 @@ class SVDFactors:
 
     def Vt(self, r):
         """First r right singular vectors as rows (r x n); needs want_v=True."""
+        if self.implicit:
+            return self.Vr[:r].contiguous()
         if self.VJ is None:
             raise ValueError("right singular vectors were not accumulated (want_v=False)")
         if self.tall or self.direct:

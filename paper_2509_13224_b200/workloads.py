@@ -6,13 +6,17 @@
   distribution), then rounded to 1e-8.
 * ``solve_config``: the TT-IGA Poisson configs[0..4] as SolveConfig kwargs.
 
-FLOP model (counted for the algorithm this package executes):
+FLOP model: the nominal count of the reference algorithm's LAPACK path
+(np.linalg.qr = dgeqrf + dorgqr; np.linalg.svd of a tall unfolding = dgesdd's m >> n path:
+dgeqrf + dorgqr + SVD of R + Q U_R), independent of how the device executes it.
 dense TT-matvec core k: 2 Ra Rb rc rd n m. Rounding: right-to-left per bond a
 Householder QR of the (n r_k) x r_{k-1} unfolding (geqrf 2mn^2 - 2n^3/3, orgqr
 the same) plus the R-carry GEMM 2 (r_{k-2} n_{k-1}) r_{k-1} k; left-to-right
-per bond QR of the (r_{k-1} n) x r_k unfolding (both halves), the Jacobi SVD
-of the r x r factor (counted as 2 * 6 r^3 for ~6 sweeps), U = Q U_R (2 m r
-keep) and the carry GEMM 2 keep r_k (n r_{k+1}).
+per bond QR of the (r_{k-1} n) x r_k unfolding (both halves), the SVD
+of the r x r factor (counted as 2 * 6 r^3 for ~6 Jacobi sweeps), U = Q U_R (2 m r
+keep) and the carry GEMM 2 keep r_k (n r_{k+1}). The device path executes fewer flops on
+very tall unfoldings (U = X V S^-1 without forming Q: the orgqr term is skipped), so the
+GFLOP/s is nominal-flops / time; ms_per_step is the direct measure.
 """
 
 from __future__ import annotations

@@ -208,3 +208,38 @@ def test_maxvol(la, golden):
     M[:, 2] = np.arange(10) + 1
     with pytest.raises(la.MaxvolError):
         la.maxvol(T(M))
+
+
+@pytest.mark.parametrize("want_v", [False, True])
+def test_svd_implicit_u_path(monkeypatch, want_v):
+    """Very tall SVD without explicit Q (U = X V S^-1) == the explicit-Q path; ill-conditioned
+    kept columns fall back to explicit Q."""
+    from paper_2509_13224_b200 import linalg as L
+    g = torch.Generator(device="cuda").manual_seed(5)
+    m, n = 4096, 96
+    X = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    X[:, -8:] *= 1e-12                                 # tail below the 1e-7 guard
+    monkeypatch.setattr(L, "_IMPLICIT_U_MIN_M", 0)
+    f = L.SVDFactors(X, want_v=want_v)
+    assert f.implicit
+    monkeypatch.setattr(L, "_IMPLICIT_U", False)
+    ref = L.SVDFactors(X, want_v=want_v)
+    assert not ref.implicit
+    assert torch.allclose(f.S, ref.S, rtol=1e-12, atol=1e-20 * float(ref.S[0]))
+    r = 80                                              # all kept columns above the guard
+    U, Ur = f.U(r), ref.U(r)
+    assert f.implicit
+    eye = torch.eye(r, dtype=torch.float64, device="cuda")
+    assert float((U.t() @ U - eye).abs().max()) < 1e-12
+    P, Pr = U @ U.t(), Ur @ Ur.t()                     # same subspace (signs may differ)
+    assert float((P - Pr).abs().max()) < 1e-11
+    assert float((U @ f.SVt(r) - Ur @ ref.SVt(r)).norm() / (Ur @ ref.SVt(r)).norm()) < 1e-12
+    if want_v:
+        assert float((f.Vt(r).t() @ torch.diag(f.S[:r]) - X.t() @ U).norm() / X.norm()) < 1e-12
+    rows = torch.empty(100, r, dtype=torch.float64, device="cuda")
+    f.U_rows(r, 50, 150, rows)
+    assert torch.allclose(rows, U[50:150], rtol=0, atol=1e-14)
+    # keeping the 1e-12 tail violates the guard -> explicit-Q fallback, orthonormal to roundoff
+    Uf = f.U(n)
+    assert not f.implicit
+    assert float((Uf.t() @ Uf - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max()) < 1e-12

@@ -282,6 +282,12 @@ class SVDFactors:
     implicit = False
     _s = None
 
+    def record_stream(self, stream):
+        """Mark every device tensor held here as used on ``stream`` (factors made on a side stream)."""
+        for v in vars(self).values():
+            if isinstance(v, torch.Tensor) and v.is_cuda:
+                v.record_stream(stream)
+
     def s_host(self):
         if self._s is None:
             self._s = self.S.cpu().numpy()

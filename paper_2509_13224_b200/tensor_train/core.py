@@ -354,16 +354,35 @@ def _dot_dev(a, b):
     return v[0, 0]
 
 
-def _rl_orthogonalize(cores, renorm=False):
-    """Right-to-left Householder sweep: cores[1:] right-orthonormal (reference core.py:414-419)."""
+def _rl_orthogonalize(cores, renorm=False, svd0=False):
+    """Right-to-left Householder sweep: cores[1:] right-orthonormal (reference core.py:414-419).
+
+    svd0: also return the SVD factors of the final cores[0] (the first step of the rounding's
+    left-to-right pass); its carry and SVD run on a side stream while the explicit Q of core 1 is
+    formed, since neither needs the other."""
     cores = list(cores)
     scale = None
+    f0 = None
     for k in range(len(cores) - 1, 0, -1):
         r0, n, r1 = cores[k].shape
+        a, m, _ = cores[k - 1].shape
+        if svd0 and k == 1 and not renorm:
+            prev = cores[0]
+
+            def first_svd(Rt):
+                c0 = L.gemm(prev.reshape(a * m, r0), Rt)
+                return c0, L.SVDFactors(c0)
+
+            Qt, Rt, (c0, f0) = L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0,
+                                             overlap_r=first_svd)
+            f0.record_stream(torch.cuda.current_stream())
+            kk = Qt.shape[0]
+            cores[k] = Qt.reshape(kk, n, r1)
+            cores[0] = c0.reshape(a, m, kk)
+            continue
         Qt, Rt = L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
         kk = Qt.shape[0]
         cores[k] = Qt.reshape(kk, n, r1)
-        a, m, _ = cores[k - 1].shape
         cores[k - 1] = L.gemm(cores[k - 1].reshape(a * m, r0), Rt).reshape(a, m, kk)
         if renorm:
             s = L.nrm2(cores[k - 1])
@@ -371,6 +390,8 @@ def _rl_orthogonalize(cores, renorm=False):
             div = torch.where(ok, s, torch.ones_like(s))
             cores[k - 1] = cores[k - 1] / div
             scale = div if scale is None else scale * div
+    if svd0:
+        return cores, scale, f0
     return cores, scale
 
 
@@ -423,14 +444,14 @@ def tt_round(t, eps, max_rank=None):
     d = len(cores)
     if d == 1:
         return _unfused([G.clone() for G in cores], tag)
-    cores, _ = _rl_orthogonalize(cores)
+    cores, _, f0 = _rl_orthogonalize(cores, svd0=True)
     total = float(L.nrm2(cores[0]).item())
     if total == 0.0:
         return _unfused([L.zeros(1, G.shape[1], 1) for G in cores], tag)
     delta = eps * total / np.sqrt(d - 1)
     for k in range(d - 1):
         r0, n, r1 = cores[k].shape
-        f = L.SVDFactors(cores[k].reshape(r0 * n, r1))
+        f = f0 if (k == 0 and f0 is not None) else L.SVDFactors(cores[k].reshape(r0 * n, r1))
         s = f.s_host()
         keep = _chop(s, delta, max_rank)
         cores[k] = f.U(keep).reshape(r0, n, keep)

@@ -16,7 +16,19 @@ if "--reps" in args:
     i = args.index("--reps")
     reps = int(args[i + 1])
     del args[i:i + 2]
+pool = 0
+if "--pool-gb" in args:
+    i = args.index("--pool-gb")
+    pool = float(args[i + 1])
+    del args[i:i + 2]
 which = [int(a) for a in args] or [0, 1]
+if pool:
+    # reserve the caching allocator's pool up front (one cudaMalloc, kept by the allocator)
+    t = time.perf_counter()
+    blk = torch.empty(int(pool * 1e9) // 8, dtype=torch.float64, device="cuda")
+    del blk
+    torch.cuda.synchronize()
+    print(json.dumps({"pool_gb": pool, "reserve_s": round(time.perf_counter() - t, 3)}), flush=True)
 for c in which:
     for rep in range(reps):
         t = time.perf_counter()

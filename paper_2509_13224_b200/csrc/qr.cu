@@ -13,6 +13,10 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
                       long long ldc, long long sC, int batch);
 // tsqr.cu
 long long tsqr_workspace(long long m);
+long long cholqr_workspace(long long m, int b);
+int cholqr_block(cudaStream_t st, long long mp, int b, double* P, long long lda, double* tau, double* Vtop,
+                 double* T, double* ws, double* Q2);
+constexpr int TTB_CHOLQR_FALLBACK = -50;
 bool tsqr_applies(long long m, int jb);
 int tsqr_panel(long long m, int jb, double* P, long long ld, double* tau, double* V, double* Tout, double* ws,
                cudaStream_t st);
@@ -555,6 +559,7 @@ int launch_gram(int m, int nb, const double* V, double* G, double* part, cudaStr
 struct QrWs {
   double *part, *Vp, *Vb, *W, *W2, *G, *Tin, *Tout, *ts;
   double *Wb, *W2b, *Gb, *Vt2;  // second set for the look-ahead stream split
+  double* cq;                    // CholeskyQR2 block factorization (cholqr.cu)
 };
 
 QrWs carve(double* ws, int m, int n) {
@@ -574,6 +579,7 @@ QrWs carve(double* ws, int m, int n) {
   w.W2b = w.Wb + wn * NB2;
   w.Gb = w.W2b + wn * NB2;
   w.Vt2 = w.Gb + (long long)NB2 * NB2;  // 2 x NB2 x NB2: Vtop of block parity 0 / 1
+  w.cq = w.Vt2 + 2LL * NB2 * NB2;
   return w;
 }
 
@@ -689,6 +695,7 @@ TTB_API long long ttb_qr_workspace(int m, int n) {
   s += (long long)((k + NB - 1) / NB) * NB * NB + (long long)((k + NB2 - 1) / NB2) * NB2 * NB2;
   s += tsqr_workspace(m);
   s += 2 * wn * NB2 + 3LL * NB2 * NB2;  // look-ahead: second W, W2, G and two Vtop blocks
+  s += cholqr_workspace(m, NB2);
   return s + 64;
 }
 
@@ -696,9 +703,27 @@ namespace {
 
 // Panels of outer block [J0, J0 + JB) on stream s (inner WY updates inside the block; a block that
 // is a single panel updates the whole trailing matrix), then the block's Vtop, Gram and T.
+// TTB_PANEL_CHOLQR=0 keeps the 128-column blocks of tall QRs on the TSQR panels (A/B)
+bool cholqr_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TTB_PANEL_CHOLQR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int factor_block(cudaStream_t s, int m, int n, int J0, int JB, double* A, long long lda, double* tau, QrWs& w,
                  double* Wp, double* W2p, double* Vtop, double* G) {
   void* stream = (void*)s;
+  if (JB == NB2 && (long long)(m - J0) >= 65536 && cholqr_enabled()) {
+    // well-conditioned tall block: CholeskyQR2 + Householder reconstruction (five GEMM passes)
+    // instead of eight TSQR panels; falls through to them when the Cholesky pivots say otherwise
+    double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
+    const int rc = cholqr_block(s, m - J0, JB, A + (long long)J0 * lda + J0, lda, tau + J0, Vtop, Tb, w.cq, w.Vb);
+    TTB_DBG(s, "geqrf cholqr block");
+    if (rc != TTB_CHOLQR_FALLBACK) return rc;
+  }
   for (int j0 = J0; j0 < J0 + JB; j0 += NB) {
     const int jb = (J0 + JB - j0) < NB ? (J0 + JB - j0) : NB;
     const int mp = m - j0;
@@ -797,6 +822,16 @@ int geqrf_lookahead(cudaStream_t st, int m, int n, double* A, long long lda, dou
     const int JBn = (J + 1 < nblk) ? ((k - J1) < NB2 ? (k - J1) : NB2) : 0;
     const double* Ap = A + (long long)J0 * lda + J0;
     double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
+    // the trailing update of block J is enqueued first: the next block's factorization may wait
+    // on the host (CholeskyQR2 pivot check) and the main stream must already have its work
+    const int nrest = n - (J1 + JBn);
+    if (nrest > 0 && JB > NB) {
+      cudaStreamWaitEvent(st, ev_fact[J], 0);
+      rc = apply_wy_panel((void*)st, m - J0, nrest, JB, Ap, lda, vtop(J), Tb, 1, A + (long long)(J1 + JBn) * lda + J0,
+                          lda, w.Wb, w.W2b);
+      if (rc) return rc;
+    }
+    cudaEventRecord(ev_big[J], st);
     if (JBn > 0) {
       if (J >= 1) cudaStreamWaitEvent(sb, ev_big[J - 1], 0);
       if (JB > NB) {  // a single-panel block already updated everything to its right
@@ -808,14 +843,6 @@ int geqrf_lookahead(cudaStream_t st, int m, int n, double* A, long long lda, dou
       if (rc) return rc;
       cudaEventRecord(ev_fact[J + 1], sb);
     }
-    const int nrest = n - (J1 + JBn);
-    if (nrest > 0 && JB > NB) {
-      cudaStreamWaitEvent(st, ev_fact[J], 0);
-      rc = apply_wy_panel((void*)st, m - J0, nrest, JB, Ap, lda, vtop(J), Tb, 1, A + (long long)(J1 + JBn) * lda + J0,
-                          lda, w.Wb, w.W2b);
-      if (rc) return rc;
-    }
-    cudaEventRecord(ev_big[J], st);
   }
   cudaEventRecord(ev_done, sb);
   cudaStreamWaitEvent(st, ev_done, 0);

@@ -243,3 +243,22 @@ def test_svd_implicit_u_path(monkeypatch, want_v):
     Uf = f.U(n)
     assert not f.implicit
     assert float((Uf.t() @ Uf - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max()) < 1e-12
+
+
+@pytest.mark.parametrize("mode", ["near_dependent", "duplicate", "graded"])
+def test_qr_tall_blocks_ill_conditioned(la, mode):
+    """Tall QR whose 128-column blocks defeat CholeskyQR2 (fallback to the TSQR panels) or stress it."""
+    rng = np.random.default_rng(11)
+    m, n = 70001, 300
+    X = rng.standard_normal((m, n))
+    if mode == "near_dependent":
+        X[:, 150:160] = X[:, 10:20] + 1e-11 * rng.standard_normal((m, 10))
+    elif mode == "duplicate":
+        X[:, 200:210] = X[:, 130:140]
+    else:
+        X *= np.logspace(0, -9, n)[None, :]
+    Q, R = la.qr(T(X))
+    Q, R = Q.cpu().numpy(), R.cpu().numpy()
+    assert np.abs(Q @ R - X).max() <= 1e-12 * np.abs(X).max() * np.sqrt(n)
+    assert np.abs(Q.T @ Q - np.eye(n)).max() <= 1e-13 * np.sqrt(m)
+    assert np.allclose(np.triu(R), R)

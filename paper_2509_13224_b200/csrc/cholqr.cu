@@ -3,8 +3,8 @@
 // The blocked QR (qr.cu) factors each 128-column block of a tall matrix (m in the millions) and
 // then applies it to the trailing columns as a compact-WY product. Factoring the block with 8
 // sixteen-column TSQR panels is a chain of ~100 latency-bound launches (the critical path of the
-// tall QR, DESIGN.md (f)). For a well-conditioned block the same outputs come from five GEMM
-// passes instead:
+// tall QR, DESIGN.md (f)). For a well-conditioned block the same outputs come from four GEMM
+// passes over the block instead:
 //   G1 = P^T P,  P = Q1 R1 (Cholesky of G1),  G2 = Q1^T Q1,  Q1 = Q R2,  R = R2 R1   (CholeskyQR2)
 // followed by Householder reconstruction (Ballard, Demmel, Grigori, Jacquelin, Nguyen, Solomonik
 // 2014): the LU factorization without pivoting of Y = [I; 0] - Q S, with the sign matrix S chosen
@@ -25,12 +25,15 @@ namespace {
 constexpr int CQT = 1024;
 
 // G (b x b row-major, symmetric) = R^T R with R upper; R and R^{-1} row-major. flag |= bit on a
-// non-positive pivot or min/max diagonal of R below 1e-5.
+// non-positive pivot or min/max diagonal of R below 1e-5. 32 x 32 thread grid over the trailing
+// triangle; R^{-1} row by row (bottom up, columns in parallel) with X^T kept in W's lower triangle.
 __global__ void __launch_bounds__(CQT) chol_inv_kernel(int b, const double* __restrict__ G, double* R, double* Ri,
                                                        int* flag, int bit) {
   extern __shared__ double W[];  // b x (b + 1)
+  __shared__ double xd[128];
   __shared__ int bad;
   const int ld = b + 1;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < b * b; e += CQT) W[(e / b) * ld + e % b] = G[e];
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
@@ -40,16 +43,13 @@ __global__ void __launch_bounds__(CQT) chol_inv_kernel(int b, const double* __re
       if (threadIdx.x == 0) bad = 1;
       break;
     }
-    const double rkk = sqrt(piv), inv = 1.0 / rkk;
+    const double rkk = sqrt(piv), inv = 1.0 / rkk, ipiv = 1.0 / piv;
+    // trailing update from the unscaled row k, then row k of R
+    for (int i = k + 1 + ty; i < b; i += 32)
+      for (int j = i + tx; j < b; j += 32) W[i * ld + j] -= W[k * ld + i] * W[k * ld + j] * ipiv;
     __syncthreads();
     for (int j = k + 1 + threadIdx.x; j < b; j += CQT) W[k * ld + j] *= inv;
     if (threadIdx.x == 0) W[k * ld + k] = rkk;
-    __syncthreads();
-    const int nt = b - k - 1;
-    for (int e = threadIdx.x; e < nt * nt; e += CQT) {
-      const int i = k + 1 + e / nt, j = k + 1 + e % nt;
-      if (j >= i) W[i * ld + j] -= W[k * ld + i] * W[k * ld + j];
-    }
     __syncthreads();
   }
   __syncthreads();
@@ -68,92 +68,100 @@ __global__ void __launch_bounds__(CQT) chol_inv_kernel(int b, const double* __re
   }
   __syncthreads();
   if (bad) return;
-  // R^{-1}: column j by back substitution (thread j)
-  for (int j = threadIdx.x; j < b; j += CQT) {
-    for (int i = b - 1; i >= 0; --i) {
-      double x = 0.0;
-      if (i <= j) {
-        double s = (i == j) ? 1.0 : 0.0;
-        for (int l = i + 1; l <= j; ++l) s -= W[i * ld + l] * Ri[(long long)l * b + j];
-        x = s / W[i * ld + i];
+  // X = R^{-1}: row i from the rows below it; X[l][j] (l < j) lives at W[j][l], diagonal in xd
+  for (int i = b - 1; i >= 0; --i) {
+    const double rii = W[i * ld + i];
+    for (int j = i + threadIdx.x; j < b; j += CQT) {
+      if (j == i) {
+        xd[i] = 1.0 / rii;
+      } else {
+        double acc = W[i * ld + j] * xd[j];
+        for (int l = i + 1; l < j; ++l) acc += W[i * ld + l] * W[j * ld + l];
+        W[j * ld + i] = -acc / rii;
       }
-      Ri[(long long)i * b + j] = x;
     }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < b * b; e += CQT) {
+    const int i = e / b, j = e % b;
+    Ri[e] = (j > i) ? W[j * ld + i] : (j == i ? xd[i] : 0.0);
   }
 }
 
-// Householder reconstruction of the top block. Q (b columns, row-major (b x ldq): Qrm[c * ldq + r] =
-// Q(r, c)), R (b x b row-major upper). Writes the factored top block of P (col-major, ld lda: S R on
-// and above the diagonal, L strictly below), tau, Vtop (col-major unit lower), T (row-major upper)
-// and SUi = S U^{-1} (row-major) for the bottom rows V_bot = -Q_bot S U^{-1}.
-__global__ void __launch_bounds__(CQT) recon_kernel(int b, const double* __restrict__ Qrm, long long ldq,
+// Householder reconstruction of the top block. Qtop (row-major b x b: Qtop[c * b + r] = Q(r, c)),
+// R (b x b row-major upper). Writes the factored top block of P (col-major, ld lda: S R on and above
+// the diagonal, L strictly below), tau, Vtop (col-major unit lower), T (row-major upper) and
+// SUi = S U^{-1} (row-major) for the bottom rows V_bot = -Q_bot S U^{-1}.
+__global__ void __launch_bounds__(CQT) recon_kernel(int b, const double* __restrict__ Qtop,
                                                     const double* __restrict__ R, double* P, long long lda,
                                                     double* tau, double* Vtop, double* T, double* SUi) {
-  extern __shared__ double M[];  // b x (b + 1): L below the diagonal, unsigned U rows above
-  __shared__ double sg[128], pv[128];
+  extern __shared__ double M[];  // b x (b + 1): L below the diagonal, U on and above it
+  __shared__ double sg[128], pv[128], xd[128];
   const int ld = b + 1;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < b * b; e += CQT) {
     const int r = e % b, c = e / b;
-    M[r * ld + c] = Qrm[(long long)c * ldq + r];
+    M[r * ld + c] = Qtop[e];
   }
   __syncthreads();
+  // LU of Y = I - Q S without pivoting, s_k chosen at step k so that the pivot is 1 + |w| >= 1;
+  // the updates act on the Q part only (the identity part stays e_j), U's rows are stored unsigned
   for (int k = 0; k < b; ++k) {
     const double w = M[k * ld + k];
-    const double s = (w > 0.0) ? -1.0 : 1.0;   // pivot 1 - s w = 1 + |w|
+    const double s = (w > 0.0) ? -1.0 : 1.0;
     const double piv = 1.0 - s * w;
-    __syncthreads();
-    if (threadIdx.x == 0) { sg[k] = s; pv[k] = piv; }
-    for (int i = k + 1 + threadIdx.x; i < b; i += CQT) M[i * ld + k] = -s * M[i * ld + k] / piv;
-    __syncthreads();
-    const int nt = b - k - 1;
-    for (int e = threadIdx.x; e < nt * nt; e += CQT) {
-      const int i = k + 1 + e / nt, j = k + 1 + e % nt;
-      M[i * ld + j] -= M[i * ld + k] * M[k * ld + j];
+    const double f = -s / piv;
+    for (int i = k + 1 + ty; i < b; i += 32) {
+      const double l = f * M[i * ld + k];
+      for (int j = k + 1 + tx; j < b; j += 32) M[i * ld + j] -= l * M[k * ld + j];
     }
     __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < b; i += CQT) M[i * ld + k] *= f;
+    if (threadIdx.x == 0) { sg[k] = s; pv[k] = piv; }
+    __syncthreads();
   }
-  // U[k][j] = -s_j M[k][j] (j > k), U[k][k] = piv_k; keep U in M's upper part from here on
   for (int e = threadIdx.x; e < b * b; e += CQT) {
     const int k = e / b, j = e % b;
     if (j > k) M[k * ld + j] *= -sg[j];
+    else if (j == k) M[k * ld + k] = pv[k];
   }
-  for (int k = threadIdx.x; k < b; k += CQT) M[k * ld + k] = pv[k];
   __syncthreads();
-  // T = U L^{-T}: X L^T = U, row i by thread i, columns left to right
-  for (int i = threadIdx.x; i < b; i += CQT) {
-    for (int j = 0; j < b; ++j) {
-      double x = 0.0;
-      if (j >= i) {
-        x = M[i * ld + j];
-        for (int l = i; l < j; ++l) x -= T[(long long)i * b + l] * M[j * ld + l];
-      }
-      T[(long long)i * b + j] = x;
-    }
-  }
-  // SUi = S U^{-1}: column j of U^{-1} by back substitution (thread j)
-  for (int j = threadIdx.x; j < b; j += CQT) {
-    for (int i = b - 1; i >= 0; --i) {
-      double x = 0.0;
-      if (i <= j) {
-        double s = (i == j) ? 1.0 : 0.0;
-        for (int l = i + 1; l <= j; ++l) s -= M[i * ld + l] * SUi[(long long)l * b + j] * sg[l];
-        x = s / M[i * ld + i];
+  // SUi = S U^{-1}: rows bottom up, columns in parallel; U^{-1}[l][j] (l < j) kept in SUi's own
+  // rows (global, written one row per step), diagonal in xd
+  for (int i = b - 1; i >= 0; --i) {
+    const double uii = M[i * ld + i];
+    for (int j = i + threadIdx.x; j < b; j += CQT) {
+      double x;
+      if (j == i) {
+        x = 1.0 / uii;
+        xd[i] = x;
+      } else {
+        double acc = M[i * ld + j] * xd[j];
+        for (int l = i + 1; l < j; ++l) acc += M[i * ld + l] * SUi[(long long)l * b + j] * sg[l];
+        x = -acc / uii;
       }
       SUi[(long long)i * b + j] = sg[i] * x;
     }
+    for (int j = threadIdx.x; j < i; j += CQT) SUi[(long long)i * b + j] = 0.0;
+    __syncthreads();
+  }
+  // T = U L^{-T} in place over U (row i by one thread, left to right: X L^T = U)
+  for (int i = threadIdx.x; i < b; i += CQT) {
+    for (int j = i + 1; j < b; ++j) {
+      double x = M[i * ld + j];
+      for (int l = i; l < j; ++l) x -= M[i * ld + l] * M[j * ld + l];
+      M[i * ld + j] = x;
+    }
   }
   __syncthreads();
-  // outputs: P top block, tau, Vtop
   for (int e = threadIdx.x; e < b * b; e += CQT) {
     const int r = e % b, c = e / b;
-    double v;
-    if (r <= c) v = sg[r] * R[(long long)r * b + c];
-    else v = M[r * ld + c];
-    P[(long long)c * lda + r] = v;
+    P[(long long)c * lda + r] = (r <= c) ? sg[r] * R[(long long)r * b + c] : M[r * ld + c];
     Vtop[(long long)c * b + r] = (r == c) ? 1.0 : (r > c ? M[r * ld + c] : 0.0);
+    const int i = e / b, j = e % b;
+    T[e] = (j >= i) ? M[i * ld + j] : 0.0;
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < b; c += CQT) tau[c] = T[(long long)c * b + c];
+  for (int c = threadIdx.x; c < b; c += CQT) tau[c] = M[c * ld + c];
 }
 
 }  // namespace
@@ -163,18 +171,19 @@ long long cholqr_workspace(long long m, int b) { return m * b + 12LL * b * b + 1
 
 // Factor the col-major mp x b block P (ld lda, b <= 128) in place as dgeqrf would, writing tau,
 // the explicit unit-lower top block Vtop (col-major b x b) and the block T (row-major b x b).
-// Q2: an mp x b scratch buffer (may be the caller's). Returns 0 on success, TTB_CHOLQR_FALLBACK when
-// the block is too ill-conditioned for CholeskyQR2 (P untouched; the caller uses its panel path),
-// otherwise an error code.
+// Returns 0 on success, TTB_CHOLQR_FALLBACK when the block is too ill-conditioned for CholeskyQR2
+// (P untouched; the caller uses its panel path), otherwise an error code. Four passes over the
+// block: G1 = P^T P, Q1 = P R1^-1, G2 = Q1^T Q1, and V_bot = -Q1_bot (R2^-1 S U^-1) (Q = Q1 R2^-1
+// is only formed for its top b x b block).
 int cholqr_block(cudaStream_t st, long long mp, int b, double* P, long long lda, double* tau, double* Vtop,
-                 double* T, double* ws, double* Q2) {
+                 double* T, double* ws) {
   if (b > 128 || b < 1 || mp < 2LL * b) return TTB_EARG;
   void* s = (void*)st;
   double* Q1 = ws;
   double* sm = ws + mp * b;
   const long long bb = (long long)b * b;
   double *G1 = sm, *R1 = sm + bb, *R1i = sm + 2 * bb, *G2 = sm + 3 * bb, *R2 = sm + 4 * bb, *R2i = sm + 5 * bb;
-  double *Rr = sm + 6 * bb, *SUi = sm + 7 * bb;
+  double *Rr = sm + 6 * bb, *SUi = sm + 7 * bb, *Qt = sm + 8 * bb, *Mb = sm + 9 * bb;
   int* flag = reinterpret_cast<int*>(sm + 12 * bb);
   const size_t smem = (size_t)b * (b + 1) * sizeof(double);
   static bool cfg = false;
@@ -197,13 +206,15 @@ int cholqr_block(cudaStream_t st, long long mp, int b, double* P, long long lda,
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return (int)e;
   if (hflag) return TTB_CHOLQR_FALLBACK;
-  rc = ttb_dgemm(s, 1, 0, b, (int)mp, b, 1.0, R2i, b, 0, Q1, mp, 0, 0.0, Q2, mp, 0, 1);     // Q = Q1 R2^-1
+  rc = ttb_dgemm(s, 1, 0, b, b, b, 1.0, R2i, b, 0, Q1, mp, 0, 0.0, Qt, b, 0, 1);             // Q top block
   if (rc) return rc;
   rc = ttb_dgemm(s, 0, 0, b, b, b, 1.0, R2, b, 0, R1, b, 0, 0.0, Rr, b, 0, 1);              // R = R2 R1
   if (rc) return rc;
-  recon_kernel<<<1, CQT, smem, st>>>(b, Q2, mp, Rr, P, lda, tau, Vtop, T, SUi); ttb_count();
-  // V_bot = -Q_bot S U^{-1}, written below the top block of P
-  rc = ttb_dgemm(s, 1, 0, b, (int)(mp - b), b, -1.0, SUi, b, 0, Q2 + b, mp, 0, 0.0, P + b, lda, 0, 1);
+  recon_kernel<<<1, CQT, smem, st>>>(b, Qt, Rr, P, lda, tau, Vtop, T, SUi); ttb_count();
+  rc = ttb_dgemm(s, 0, 0, b, b, b, 1.0, R2i, b, 0, SUi, b, 0, 0.0, Mb, b, 0, 1);            // R2^-1 S U^-1
+  if (rc) return rc;
+  // V_bot = -Q_bot S U^-1 = -Q1_bot (R2^-1 S U^-1), written below the top block of P
+  rc = ttb_dgemm(s, 1, 0, b, (int)(mp - b), b, -1.0, Mb, b, 0, Q1 + b, mp, 0, 0.0, P + b, lda, 0, 1);
   if (rc) return rc;
   return ttb_last_error();
 }

@@ -15,7 +15,7 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
 long long tsqr_workspace(long long m);
 long long cholqr_workspace(long long m, int b);
 int cholqr_block(cudaStream_t st, long long mp, int b, double* P, long long lda, double* tau, double* Vtop,
-                 double* T, double* ws, double* Q2);
+                 double* T, double* ws);
 constexpr int TTB_CHOLQR_FALLBACK = -50;
 bool tsqr_applies(long long m, int jb);
 int tsqr_panel(long long m, int jb, double* P, long long ld, double* tau, double* V, double* Tout, double* ws,
@@ -717,10 +717,10 @@ int factor_block(cudaStream_t s, int m, int n, int J0, int JB, double* A, long l
                  double* Wp, double* W2p, double* Vtop, double* G) {
   void* stream = (void*)s;
   if (JB == NB2 && (long long)(m - J0) >= 65536 && cholqr_enabled()) {
-    // well-conditioned tall block: CholeskyQR2 + Householder reconstruction (five GEMM passes)
+    // well-conditioned tall block: CholeskyQR2 + Householder reconstruction (four GEMM passes)
     // instead of eight TSQR panels; falls through to them when the Cholesky pivots say otherwise
     double* Tb = w.Tout + (long long)(J0 / NB2) * NB2 * NB2;
-    const int rc = cholqr_block(s, m - J0, JB, A + (long long)J0 * lda + J0, lda, tau + J0, Vtop, Tb, w.cq, w.Vb);
+    const int rc = cholqr_block(s, m - J0, JB, A + (long long)J0 * lda + J0, lda, tau + J0, Vtop, Tb, w.cq);
     TTB_DBG(s, "geqrf cholqr block");
     if (rc != TTB_CHOLQR_FALLBACK) return rc;
   }

@@ -126,26 +126,12 @@ __global__ void __launch_bounds__(CQT) recon_kernel(int b, const double* __restr
     else if (j == k) M[k * ld + k] = pv[k];
   }
   __syncthreads();
-  // SUi = S U^{-1}: rows bottom up, columns in parallel; U^{-1}[l][j] (l < j) kept in SUi's own
-  // rows (global, written one row per step), diagonal in xd
-  for (int i = b - 1; i >= 0; --i) {
-    const double uii = M[i * ld + i];
-    for (int j = i + threadIdx.x; j < b; j += CQT) {
-      double x;
-      if (j == i) {
-        x = 1.0 / uii;
-        xd[i] = x;
-      } else {
-        double acc = M[i * ld + j] * xd[j];
-        for (int l = i + 1; l < j; ++l) acc += M[i * ld + l] * SUi[(long long)l * b + j] * sg[l];
-        x = -acc / uii;
-      }
-      SUi[(long long)i * b + j] = sg[i] * x;
-    }
-    for (int j = threadIdx.x; j < i; j += CQT) SUi[(long long)i * b + j] = 0.0;
-    __syncthreads();
+  // keep U (row-major) in SUi's slot while T = U L^{-T} overwrites it in place (row i by one thread,
+  // left to right: X L^T = U)
+  for (int e = threadIdx.x; e < b * b; e += CQT) {
+    const int i = e / b, j = e % b;
+    SUi[e] = (j >= i) ? M[i * ld + j] : 0.0;
   }
-  // T = U L^{-T} in place over U (row i by one thread, left to right: X L^T = U)
   for (int i = threadIdx.x; i < b; i += CQT) {
     for (int j = i + 1; j < b; ++j) {
       double x = M[i * ld + j];
@@ -162,6 +148,31 @@ __global__ void __launch_bounds__(CQT) recon_kernel(int b, const double* __restr
     T[e] = (j >= i) ? M[i * ld + j] : 0.0;
   }
   for (int c = threadIdx.x; c < b; c += CQT) tau[c] = M[c * ld + c];
+  __syncthreads();
+  // U back into smem; X = U^{-1} row by row (bottom up, columns in parallel), X^T in the lower
+  // triangle, diagonal in xd; then SUi = S X
+  for (int e = threadIdx.x; e < b * b; e += CQT) {
+    const int i = e / b, j = e % b;
+    if (j >= i) M[i * ld + j] = SUi[e];
+  }
+  __syncthreads();
+  for (int i = b - 1; i >= 0; --i) {
+    const double uii = M[i * ld + i];
+    for (int j = i + threadIdx.x; j < b; j += CQT) {
+      if (j == i) {
+        xd[i] = 1.0 / uii;
+      } else {
+        double acc = M[i * ld + j] * xd[j];
+        for (int l = i + 1; l < j; ++l) acc += M[i * ld + l] * M[j * ld + l];
+        M[j * ld + i] = -acc / uii;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < b * b; e += CQT) {
+    const int i = e / b, j = e % b;
+    SUi[e] = sg[i] * ((j > i) ? M[j * ld + i] : (j == i ? xd[i] : 0.0));
+  }
 }
 
 }  // namespace

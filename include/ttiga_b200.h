@@ -175,6 +175,11 @@ int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int 
                        const double* Mf, const double* phiRp, const double* b, double* x, const double* d,
                        double atol, int maxiter, int x0_nonzero, double* ws, double* S, int* iters);
 
+/* INT8 tensor-core GEMM (tcgen05.mma kind::i8, TMEM accumulators): C (int32 M x N row-major) =
+ * A (int8 M x K row-major) B (int8 N x K row-major)^T; M, N, K multiples of 128. Building block of the
+ * Ozaki-scheme FP64 emulation. */
+int ttb_i8gemm(void* stream, int M, int N, int K, const void* A, const void* B, int* C);
+
 #ifdef __cplusplus
 }
 #endif

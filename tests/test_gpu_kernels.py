@@ -262,3 +262,16 @@ def test_qr_tall_blocks_ill_conditioned(la, mode):
     assert np.abs(Q @ R - X).max() <= 1e-12 * np.abs(X).max() * np.sqrt(n)
     assert np.abs(Q.T @ Q - np.eye(n)).max() <= 1e-13 * np.sqrt(m)
     assert np.allclose(np.triu(R), R)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 128), (256, 384, 512), (1024, 512, 2048)])
+def test_i8gemm_tcgen05_exact(M, N, K):
+    """tcgen05 kind::i8 GEMM (TMEM accumulators, 128B-swizzled smem operands): exact int32 result."""
+    from paper_2509_13224_b200._lib import call, ptr
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randint(-127, 128, (M, K), generator=g, device="cuda", dtype=torch.int8)
+    B = torch.randint(-127, 128, (N, K), generator=g, device="cuda", dtype=torch.int8)
+    C = torch.empty(M, N, dtype=torch.int32, device="cuda")
+    call("ttb_i8gemm", M, N, K, ptr(A), ptr(B), ptr(C))
+    ref = A.double() @ B.double().t()
+    assert torch.equal(C.double(), ref)

@@ -179,6 +179,14 @@ int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int 
  * A (int8 M x K row-major) B (int8 N x K row-major)^T; M, N, K multiples of 128. Building block of the
  * Ozaki-scheme FP64 emulation. */
 int ttb_i8gemm(void* stream, int M, int N, int K, const void* A, const void* B, int* C);
+/* FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme, 7 exact 8-bit slices per operand,
+ * 55-bit operands, exact int32 level sums): C (M x N, ldc) = A (M x K row-major, lda) op(B), op(B) = B
+ * (K x N, ldb) for tB = 0 or B^T (B: N x K) for tB = 1. Replaces ttb_dgemm for large tcgen05-tileable
+ * shapes (ttb_ozaki_applies); ws: ttb_ozaki_workspace bytes. */
+long long ttb_ozaki_workspace(int M, int N, int K); /* bytes */
+int ttb_ozaki_applies(int M, int N, int K);
+int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, long long lda, const double* B,
+                    long long ldb, double* C, long long ldc, void* ws);
 
 #ifdef __cplusplus
 }

@@ -63,6 +63,9 @@ SIGNATURES = {
     "ttb_local_pcg": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, f64, i32, i32, vp, vp, vp]),
     "ttb_abs_floor": (i32, [vp, i64, vp, vp]),
     "ttb_i8gemm": (i32, [vp, i32, i32, i32, vp, vp, vp]),
+    "ttb_ozaki_workspace": (i64, [i32, i32, i32]),
+    "ttb_ozaki_applies": (i32, [i32, i32, i32]),
+    "ttb_dgemm_ozaki": (i32, [vp, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
     "ttb_band_gemm": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
     "ttb_local_gemm_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
     "ttb_local_gemm_ws_init": (i32, [vp, i32, i32, i32, i32, i32, vp]),

@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(128, 1) i8gemm_tma_kernel(const __grid_constan
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
   const int nk = K / TB_K;
-  if (tid == 0) {
+  // warps 0 and 1: lane 0 works, the other lanes park in __syncwarp (see the Ozaki kernel)
+  if (warp == 0 && lane == 0) {
     // producer
     for (int kt = 0; kt < nk; ++kt) {
       const int s = kt % TS;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(128, 1) i8gemm_tma_kernel(const __grid_constan
       tma_load_2d(sa, &tmA, kt * TB_K, m0, fb);
       tma_load_2d(sa + ABYTES, &tmB, kt * TB_K, n0, fb);
     }
-  } else if (tid == 32) {
+  } else if (warp == 1 && lane == 0) {
     // MMA issuer
     for (int kt = 0; kt < nk; ++kt) {
       const int s = kt % TS;
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(128, 1) i8gemm_tma_kernel(const __grid_constan
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
         smem_u32(&done)));
   }
+  __syncwarp();
   mbar_wait(smem_u32(&done), 0);
   __syncwarp();
   asm volatile("tcgen05.fence::after_thread_sync;\n");

@@ -1,0 +1,479 @@
+// FP64 GEMM emulated on the tcgen05 INT8 tensor cores (Ozaki scheme, error-free slicing).
+//
+// C (M x N) = A (M x K) B (K x N), FP64. Every row i of A is scaled by 2^-ea_i (ea_i = frexp
+// exponent of max_k |a_ik|, so the scaled row lies in (-1, 1)) and cut into S = 7 balanced signed
+// 8-bit slices,  a_ik = 2^ea_i sum_s sigma_s(i,k) 2^(-6-8s),  sigma_s in [-128, 127],
+// the base-256 digits of the 54-bit integer round(a_ik 2^(54-ea_i)); B's columns likewise (exponents
+// fb_j, slices tau_t, stored transposed: K-major). Then
+//   C_ij = 2^(ea_i + fb_j) sum_{d<LEV} 2^(-12-8d) D_d(i, j),   D_d = sum_{s+t=d} A_s B_t^T,
+// where every D_d is an exact int32 tcgen05 kind::i8 GEMM ((pairs per level) K 2^14 < 2^31 for
+// K <= 4096). LEV = 8 keeps every product down to the 2^-54 level of the operands' slicing; the
+// dropped levels weigh < 2^-60 K max|a_i| max|b_j|. Agreement with a DGEMM is at its own rounding
+// level, normwise (tests/test_gpu_kernels.py). TTB_OZAKI_LEVELS=7 drops level 7 (28 products).
+//
+// Kernel: 128 x 64 output tiles, TMA (3-D maps over the slice stacks, 64-byte swizzle) into a
+// 2-stage ring of full/empty mbarriers holding all 14 slice tiles of a 64-byte k step; one thread
+// issues, per A slice s, MMAs of N = 64 nt against nt consecutive B slice tiles (the level
+// accumulators s .. s+nt-1 are consecutive 64-column TMEM ranges), 10 MMAs per 32-byte k step for
+// 34 slice products; the epilogue sums the levels in FP64 and writes C once through shared memory.
+#include "common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace {
+
+constexpr int OZ_S = 7;                  // slices per operand
+constexpr int OZ_M = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}\n" ::"r"(mbar),
+      "r"(phase));
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(mbar)
+      : "memory");
+}
+
+// ---- all levels in one pass: 128 x 64 tiles, every k stage (64 bytes of K) holds all 7 A and all 7 B
+// slices (84 KB, 2-stage ring, 64-byte swizzle), the 34 slice-pair MMAs accumulate into 8 TMEM
+// accumulators of 64 columns (all 512), and C is written once.
+#ifndef TTB_OZ_K
+#define TTB_OZ_K 64
+#endif
+// k step per stage (bytes of K): 32 -> 32-byte swizzle, 5 stages of 42 KB; 64 -> 64-byte swizzle, 2 stages of 84 KB
+constexpr int OA_N = 64, OA_K = TTB_OZ_K, OA_ST = OA_K == 32 ? 5 : 2;
+constexpr int OA_ABYTES = OZ_M * OA_K, OA_BBYTES = OA_N * OA_K;
+constexpr int OA_SBYTES = OZ_S * (OA_ABYTES + OA_BBYTES);
+
+// K-major, OA_K-byte swizzle (32 or 64): 8-row atoms of 8 OA_K bytes (SM100 layout type 6 / 4)
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(((8 * OA_K) >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(OA_K == 32 ? 6 : 4) << 61;
+  return d;
+}
+
+// s8 x s8 -> s32, M = 128, N = 64 nt (all slices are balanced signed digits)
+__host__ __device__ constexpr uint32_t oa_idesc(int nt) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nt * OA_N >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
+}
+
+// One 32-byte k step of every slice product of a tile. For A slice s the B slices t = 0..T_s-1
+// (T_s = min(S, LEV - s)) are consecutive 64-row tiles in shared memory, i.e. one K-major operand of
+// 64 T_s rows, and their products land in the level accumulators s..s+T_s-1, i.e. TMEM columns
+// 64 s .. 64 (s + T_s): one MMA of N = 64 nt per chunk of <= 4 tiles (N <= 256) covers nt slice pairs
+// and reads the A tile once for all of them. The MMAs that only touch not-yet-written levels (A slice 0,
+// and for LEV 8 the (3, 4) product, level 7 alone) come first and overwrite (first = k step 0 of the
+// tile), so the accumulators need no zeroing.
+template <int LEV>
+__device__ __forceinline__ void oz_issue(uint32_t tmem, uint64_t da, uint64_t db, int kk, bool first) {
+  auto mma = [&](int sa, int t0, int nt, bool fresh) {
+    mma_i8(tmem + (uint32_t)((sa + t0) * OA_N), da + (uint64_t)((sa * OA_ABYTES + kk * 32) >> 4),
+           db + (uint64_t)((t0 * OA_BBYTES + kk * 32) >> 4), oa_idesc(nt), (fresh && first) ? 0u : 1u);
+  };
+  mma(0, 0, 4, true);
+  mma(0, 4, 3, true);
+  if (LEV == 8) mma(3, 4, 1, true);
+#pragma unroll
+  for (int sa = 1; sa < OZ_S; ++sa) {
+    const int T = (LEV - sa < OZ_S) ? LEV - sa : OZ_S;
+#pragma unroll
+    for (int t0 = 0; t0 < T; t0 += 4) {
+      if (LEV == 8 && sa == 3 && t0 == 4) continue;
+      mma(sa, t0, T - t0 < 4 ? T - t0 : 4, false);
+    }
+  }
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+// v 2^e, bit-identical to ldexp (a multiplication by an exact power of two rounds once, like ldexp,
+// when the result is subnormal); ldexp itself only where 2^e is not a normal double
+__device__ __forceinline__ double oz_scale(double v, int e) {
+  return (e > -1023 && e < 1024) ? v * __longlong_as_double((long long)(e + 1023) << 52) : ldexp(v, e);
+}
+
+constexpr int OA_EPAD = 17;  // epilogue staging row (doubles) of a warp's 32 x 16 block
+
+// Persistent, warp-specialized: warp 0 = TMA producer (lane 0), warp 1 = MMA issuer (lane 0), warps 2-9
+// = epilogue (warp w reads TMEM lanes 32 (w % 4) ..). One 128 x 64 tile at a time in TMEM (all 512
+// columns: 8 levels x 64); the producer runs ahead into the next tile's stages while the epilogue
+// drains TMEM, and the epilogue's C write overlaps the next tile's MMAs (TMEM is released as soon as
+// the level sums are in registers).
+template <int LEV>
+__global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                                                        const int* __restrict__ ea, const int* __restrict__ fb,
+                                                        double* C, long long ldc) {
+  extern __shared__ __align__(1024) uint8_t dyn[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[OA_ST], empty[OA_ST], tfull, tempty;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < OA_ST; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tfull)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(&tempty)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const int nk = K / OA_K, ntn = N / OA_N, tiles = (M / OZ_M) * ntn;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: per stage one box of all 7 A slice tiles, one of all 7 B
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / ntn) * OZ_M, n0 = (tile % ntn) * OA_N;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int st = it % OA_ST;
+          if (it >= OA_ST) mbar_wait(smem_u32(&empty[st]), ((it / OA_ST) - 1) & 1);
+          const uint32_t fbar = smem_u32(&full[st]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fbar), "r"(OA_SBYTES)
+                       : "memory");
+          const uint32_t base = smem_u32(sm + st * OA_SBYTES);
+          tma_load_3d(base, &tmA, kt * OA_K, m0, 0, fbar);
+          tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, 0, fbar);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, tl = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tl) {
+        if (tl > 0) {  // the epilogue has the previous tile's level sums in registers
+          mbar_wait(smem_u32(&tempty), (tl - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+        }
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int st = it % OA_ST;
+          mbar_wait(smem_u32(&full[st]), (it / OA_ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t a0 = smem_u32(sm + st * OA_SBYTES), b0 = a0 + OZ_S * OA_ABYTES;
+          const uint64_t da = sw_desc(a0), db = sw_desc(b0);
+#pragma unroll
+          for (int kk = 0; kk < OA_K / 32; ++kk) oz_issue<LEV>(tmem, da, db, kk, kt == 0 && kk == 0);
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_u32(&empty[st])));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&tfull)));
+      }
+    }
+  } else {
+    // epilogue, 8 warps: warp w reads TMEM lanes 32 (w % 4) .. (its 32 rows) and columns 32 h ..
+    // (h = (w - 2) / 4) of every level. While TMEM is held only integer work runs: the level sums are
+    // folded exactly into two int64 per column, hi = sum_{d<4} D_d 2^(8(3-d)) (|hi| < 2^51) and
+    // lo = sum_{d>=4} D_d 2^(8(LEV-1-d)) (|lo| < 2^52.4 for K <= 4096), one IMAD.WIDE per level. TMEM is
+    // released, then C = 2^e (hi 2^-36 + lo 2^-(12+8(LEV-1))), e = ea_i + fb_j, in one FMA (exact
+    // products, a single rounding) and written through a per-warp 32 x 16 staging block, two rows of
+    // 16 consecutive columns (128 bytes each) per store instruction.
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    double* stg = reinterpret_cast<double*>(sm + OA_ST * OA_SBYTES) + (warp - 2) * 32 * OA_EPAD;
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 32);
+    constexpr int LO_EXP = -12 - 8 * (LEV - 1);
+    int tl = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tl) {
+      const int m0 = (tile / ntn) * OZ_M, n0 = (tile % ntn) * OA_N + h * 32;
+      const int my_ea = ea[m0 + q * 32 + lane];
+      const int my_fb = fb[n0 + lane];  // column n0 + lane's exponent, broadcast per column below
+      mbar_wait(smem_u32(&tfull), tl & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      long long hi[32], lo[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0;
+#pragma unroll
+      for (int d = 0; d < LEV; ++d) {
+        const long long sh = 1LL << (d < 4 ? 8 * (3 - d) : 8 * (LEV - 1 - d));
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {  // 16 columns per load (10 warps: 168 registers per thread)
+          uint32_t v[16];
+          tmem_ld16(tq + (uint32_t)(d * OA_N + g * 16), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            if (d < 4)
+              hi[g * 16 + c] += (long long)(int)v[c] * sh;
+            else
+              lo[g * 16 + c] += (long long)(int)v[c] * sh;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&tempty)) : "memory");
+      const int cq = lane & 15, half = lane >> 4;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int cc = j * 16 + c;
+          const int e = my_ea + __shfl_sync(0xffffffffu, my_fb, cc);
+          double x;
+          if (e - 36 < 1024 && e + LO_EXP > -1023)
+            x = fma((double)lo[cc], __longlong_as_double((long long)(e + LO_EXP + 1023) << 52),
+                    (double)hi[cc] * __longlong_as_double((long long)(e - 36 + 1023) << 52));
+          else
+            x = ldexp(fma((double)lo[cc], __longlong_as_double((long long)(LO_EXP + 36 + 1023) << 52),
+                          (double)hi[cc]), e - 36);
+          stg[lane * OA_EPAD + c] = x;
+        }
+        __syncwarp();
+        double* crow = C + (long long)(m0 + q * 32) * ldc + n0 + j * 16 + cq;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int rr = 2 * i + half;
+          crow[(long long)rr * ldc] = stg[rr * OA_EPAD + cq];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+// ---- slicing
+// exponent of the row maximum (frexp): one warp per row of a row-major (rows x K, ld) matrix
+__global__ void oz_rowexp_kernel(int rows, int K, const double* __restrict__ X, long long ld, int* e) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  double m = 0.0;
+  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(X[(long long)w * ld + k]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) {
+    int ex = 0;
+    if (m > 0.0) frexp(m, &ex);
+    e[w] = ex;
+  }
+}
+
+// exponent of the column maximum of a row-major (K x cols, ld) matrix: per-column atomicMax of the
+// non-negative bit pattern, then frexp
+__global__ void oz_colmax_kernel(int K, int cols, const double* __restrict__ X, long long ld,
+                                 unsigned long long* cmax) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
+  double m = 0.0;
+  for (int k = k0; k < k1; ++k) m = fmax(m, fabs(X[(long long)k * ld + c]));
+  atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void oz_colexp_kernel(int cols, const unsigned long long* cmax, int* e) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const double m = __longlong_as_double((long long)cmax[c]);
+  int ex = 0;
+  if (m > 0.0) frexp(m, &ex);
+  e[c] = ex;
+}
+
+// Balanced base-256 digits of the 54-bit fixed-point value X = round(x 2^(54 - ex)) (|X| <= 2^54 - 1):
+// X = sum_s sigma_s 2^(48 - 8s), every sigma_s in [-128, 127] (each byte above 127 borrows from the next
+// digit up; the top digit stays within [-65, 65]), i.e. x = 2^ex sum_s sigma_s 2^(-6-8s) up to the single
+// rounding of X. Integer arithmetic: a floor cascade in floating point loses the remainder of tiny values.
+__device__ __forceinline__ void oz_digits(double x, int ex, uint8_t (&d)[OZ_S]) {
+  long long X = __double2ll_rn(ldexp(x, 54 - ex));
+  const long long lim = (1LL << 54) - 1;
+  X = X > lim ? lim : (X < -lim ? -lim : X);
+#pragma unroll
+  for (int s = OZ_S - 1; s >= 1; --s) {
+    const int r = (int)(int8_t)(uint8_t)(X & 0xFF);  // in [-128, 127], X - r divisible by 256
+    d[s] = (uint8_t)r;
+    X = (X - r) >> 8;
+  }
+  d[0] = (uint8_t)(int8_t)X;
+}
+
+// row slices of a row-major (rows x K, ld) matrix into out[s][rows][K]; 16 consecutive k per thread
+__global__ void oz_slice_rows_kernel(int rows, int K, const double* __restrict__ X, long long ld,
+                                     const int* __restrict__ e, uint8_t* out) {
+  const long long groups = (long long)rows * (K / 16);
+  const long long plane = (long long)rows * K;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(g / (K / 16)), k0 = (int)(g % (K / 16)) * 16;
+    const int ex = e[r];
+    __align__(16) uint8_t dg[OZ_S][16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      uint8_t d[OZ_S];
+      oz_digits(X[(long long)r * ld + k0 + q], ex, d);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) dg[s][q] = d[s];
+    }
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint4*>(out + s * plane + (long long)r * K + k0) = *reinterpret_cast<uint4*>(dg[s]);
+  }
+}
+
+// column slices of a row-major (K x cols, ld) matrix, transposed: out[s][cols][K] (64 x 64 tiles)
+__global__ void oz_slice_cols_kernel(int K, int cols, const double* __restrict__ X, long long ld,
+                                     const int* __restrict__ e, uint8_t* out) {
+  __shared__ __align__(16) uint8_t t[OZ_S][64][64 + 16];
+  const int k0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const long long plane = (long long)cols * K;
+  for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+    const int kk = idx / 64, cc = idx % 64;
+    const int k = k0 + kk, c = c0 + cc;
+    uint8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0};
+    if (k < K && c < cols) oz_digits(X[(long long)k * ld + c], e[c], d);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) t[s][cc][kk] = d[s];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < OZ_S * 64 * 4; idx += blockDim.x) {
+    const int s = idx / 256, cc = (idx / 4) % 64, part = idx % 4;
+    const int c = c0 + cc, k = k0 + part * 16;
+    if (c < cols && k < K)
+      *reinterpret_cast<uint4*>(out + s * plane + (long long)c * K + k) = *reinterpret_cast<const uint4*>(&t[s][cc][part * 16]);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 oz_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// slice stack [S][rows][K] int8, box box_k bytes x box_rows x S (32 / 64 / 128 bytes: matching swizzle)
+bool oz_tmap(CUtensorMap* tm, const void* ptr, int rows, int K, int box_rows, int box_k) {
+  auto enc = oz_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)OZ_S};
+  cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)rows * K};
+  cuuint32_t box[3] = {(cuuint32_t)box_k, (cuuint32_t)box_rows, (cuuint32_t)OZ_S};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = box_k == 32   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                : box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Workspace (bytes) of ttb_dgemm_ozaki: slice stacks of A and B, exponents, column maxima.
+TTB_API long long ttb_ozaki_workspace(int M, int N, int K) {
+  return (long long)OZ_S * ((long long)M + N) * K + 4LL * (M + N) + 8LL * N + 1024;
+}
+
+// Whether ttb_dgemm_ozaki takes this shape (tcgen05 tiles and exact int32 accumulation).
+namespace {
+bool oz_applies_all(int M, int N, int K) {
+  return M > 0 && N > 0 && K > 0 && M % 128 == 0 && N % 64 == 0 && K % 64 == 0 && K <= 4096;
+}
+}  // namespace
+
+TTB_API int ttb_ozaki_applies(int M, int N, int K) { return oz_applies_all(M, N, K) ? 1 : 0; }
+
+// C (M x N, ldc) = op(A) (M x K) B (K x N), FP64 via the Ozaki scheme on the INT8 tensor cores.
+// A: row-major M x K (lda) when tA == 0; B: row-major K x N (ldb) when tB == 0, N x K (ldb) when tB == 1.
+// ws: ttb_ozaki_workspace bytes (device). Returns TTB_EARG for shapes ttb_ozaki_applies rejects.
+TTB_API int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, long long lda,
+                            const double* B, long long ldb, double* C, long long ldc, void* ws) {
+  if (!oz_applies_all(M, N, K)) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  uint8_t* As = reinterpret_cast<uint8_t*>(ws);
+  uint8_t* Bs = As + (long long)OZ_S * M * K;
+  int* ea = reinterpret_cast<int*>(Bs + (long long)OZ_S * N * K);
+  int* fb = ea + M;
+  unsigned long long* cmax =
+      reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(fb + N + 2) & ~uintptr_t(7));
+  oz_rowexp_kernel<<<ceil_div((long long)M * 32, 256), 256, 0, st>>>(M, K, A, lda, ea); ttb_count();
+  oz_slice_rows_kernel<<<148 * 16, 256, 0, st>>>(M, K, A, lda, ea, As); ttb_count();
+  if (tB) {
+    oz_rowexp_kernel<<<ceil_div((long long)N * 32, 256), 256, 0, st>>>(N, K, B, ldb, fb); ttb_count();
+    oz_slice_rows_kernel<<<148 * 16, 256, 0, st>>>(N, K, B, ldb, fb, Bs); ttb_count();
+  } else {
+    cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * N, st);
+    oz_colmax_kernel<<<dim3(ceil_div(N, 256), ceil_div(K, 256)), 256, 0, st>>>(K, N, B, ldb, cmax); ttb_count();
+    oz_colexp_kernel<<<ceil_div(N, 256), 256, 0, st>>>(N, cmax, fb); ttb_count();
+    oz_slice_cols_kernel<<<dim3(ceil_div(N, 64), ceil_div(K, 64)), 256, 0, st>>>(K, N, B, ldb, fb, Bs); ttb_count();
+  }
+  CUtensorMap ta, tb;
+  if (!oz_tmap(&ta, As, M, K, OZ_M, OA_K) || !oz_tmap(&tb, Bs, N, K, OA_N, OA_K)) return TTB_EARG;
+  const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
+  static bool cfg_all = false;
+  static int nsm = 148;
+  if (!cfg_all) {
+    cudaFuncSetAttribute(oz_gemm_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(oz_gemm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cfg_all = true;
+  }
+  static const int levels = [] {
+    const char* e = getenv("TTB_OZAKI_LEVELS");
+    return e && atoi(e) == 7 ? 7 : 8;
+  }();
+  const int tiles = (M / OZ_M) * (N / OA_N);
+  const int grid = tiles < nsm ? tiles : nsm;
+  if (levels == 7)
+    oz_gemm_kernel<7><<<grid, 320, smem, st>>>(ta, tb, M, N, K, ea, fb, C, ldc);
+  else
+    oz_gemm_kernel<8><<<grid, 320, smem, st>>>(ta, tb, M, N, K, ea, fb, C, ldc);
+  ttb_count();
+  return ttb_last_error();
+}

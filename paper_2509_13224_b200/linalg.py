@@ -52,8 +52,18 @@ def gemm_profile(enable: bool):
     return rec
 
 
-def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
-    """out = alpha op(A) op(B) + beta out (row-major, FP64 DMMA kernel)."""
+_OZAKI = os.environ.get("TTB_OZAKI", "1") != "0"
+_OZAKI_MIN_WORK = 1 << 33          # M N K: only the rounding-sized products (>= 8.6 GFMA)
+_OZAKI_CHECK = os.environ.get("TTB_OZAKI_CHECK", "0") == "1"   # debug: compare every emulated product with DMMA
+
+
+def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False):
+    """out = alpha op(A) op(B) + beta out (row-major, FP64 DMMA kernel).
+
+    emulate: large products (M N K >= 2^33, tcgen05-tileable, K <= 4096, alpha = 1, beta = 0, A not
+    transposed) run as the Ozaki-scheme FP64 GEMM on the INT8 tensor cores (ttb_dgemm_ozaki: 55-bit
+    operand slices, 8 exact int32 level sums; agrees with DGEMM to ~1e-15 normwise). TTB_OZAKI=0 keeps
+    every product on DMMA."""
     A = _rows(A)
     B = _rows(B)
     M, K = (A.shape[1], A.shape[0]) if tA else (A.shape[0], A.shape[1])
@@ -65,6 +75,26 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
         beta = 0.0
     elif out.shape != (M, N) or out.stride(1) != 1:
         raise ValueError("bad gemm output")
+    if (emulate and _OZAKI and not tA and alpha == 1.0 and beta == 0.0 and M * N * K >= _OZAKI_MIN_WORK
+            and call_raw("ttb_ozaki_applies", M, N, K)):
+        ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, K)), dtype=torch.uint8, device=device())
+        prof = _GEMM_PROFILE
+        if prof is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        call("ttb_dgemm_ozaki", int(tB), M, N, K, ptr(A), max(A.stride(0), 1), ptr(B), max(B.stride(0), 1), ptr(out),
+             max(out.stride(0), 1), ptr(ws))
+        if prof is not None:
+            e1.record()
+            prof.append((e0, e1, 2.0 * M * N * K, "ozaki"))
+        if _OZAKI_CHECK:
+            ref = empty(M, N)
+            call("ttb_dgemm", int(tA), int(tB), M, N, K, 1.0, ptr(A), max(A.stride(0), 1), 0, ptr(B),
+                 max(B.stride(0), 1), 0, 0.0, ptr(ref), N, 0, 1)
+            print(f"ozaki check M={M} N={N} K={K} tB={int(tB)}: rel {float((out - ref).norm() / ref.norm()):.3e} "
+                  f"|A| {float(A.norm()):.3e} |B| {float(B.norm()):.3e}", flush=True)
+        return out
     if M and N:
         prof = _GEMM_PROFILE
         if prof is not None:
@@ -75,7 +105,7 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None):
              max(B.stride(0), 1), 0, float(beta), ptr(out), max(out.stride(0), 1), 0, 1)
         if prof is not None:
             e1.record()
-            prof.append((e0, e1, 2.0 * M * N * K))
+            prof.append((e0, e1, 2.0 * M * N * K, "dmma"))
     return out
 
 
@@ -106,7 +136,7 @@ def permute(X, perm, out=None):
     return out
 
 
-def tdot(A, B, axes):
+def tdot(A, B, axes, emulate=False):
     """np.tensordot(A, B, axes) on the device: permute to matrix form + one GEMM."""
     ia, ib = axes
     ia = [a % A.dim() for a in (ia if isinstance(ia, (list, tuple)) else [ia])]
@@ -124,7 +154,7 @@ def tdot(A, B, axes):
         Bm, tB = B.contiguous().reshape(N, K), True
     else:
         Bm, tB = permute(B, ib + fb).reshape(K, N), False
-    out = gemm(Am, Bm, tA=tA, tB=tB)
+    out = gemm(Am, Bm, tA=tA, tB=tB, emulate=emulate)
     return out.reshape([A.shape[k] for k in fa] + [B.shape[k] for k in fb])
 
 
@@ -317,7 +347,7 @@ class SVDFactors:
     def U(self, r):
         """First r left singular vectors, row-major (m x r)."""
         if self.implicit and self._implicit_w(r) is not None:
-            return gemm(self.X, self._W)
+            return gemm(self.X, self._W, emulate=True)
         if self.tall:
             return gemm(self.Qt, self.UJ[:r], tA=True, tB=True)
         return self.UJ[:r].t().contiguous()
@@ -325,7 +355,7 @@ class SVDFactors:
     def U_rows(self, r, i0, i1, out):
         """Rows [i0, i1) of U(r) into ``out`` ((i1 - i0) x r, row-major) -- chunked formation."""
         if self.implicit and self._implicit_w(r) is not None:
-            return gemm(self.X[i0:i1], self._W, out=out)
+            return gemm(self.X[i0:i1], self._W, out=out, emulate=True)
         if self.tall:
             return gemm(self.Qt[:, i0:i1], self.UJ[:r], tA=True, tB=True, out=out)
         out.copy_(self.UJ[:r, i0:i1].t())

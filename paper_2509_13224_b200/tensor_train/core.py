@@ -383,7 +383,7 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False):
         Qt, Rt = L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
         kk = Qt.shape[0]
         cores[k] = Qt.reshape(kk, n, r1)
-        cores[k - 1] = L.gemm(cores[k - 1].reshape(a * m, r0), Rt).reshape(a, m, kk)
+        cores[k - 1] = L.gemm(cores[k - 1].reshape(a * m, r0), Rt, emulate=True).reshape(a, m, kk)
         if renorm:
             s = L.nrm2(cores[k - 1])
             ok = s > 0
@@ -419,7 +419,7 @@ def tt_matvec(A, x):
         else:
             Ra, n, m, Rb = M.shape
             rc, _, rd = G.shape
-            T = L.tdot(M, G, ([2], [1]))                     # (a, i, b, c, d)
+            T = L.tdot(M, G, ([2], [1]), emulate=True)       # (a, i, b, c, d)
             Y = L.permute(T, (0, 3, 1, 2, 4)).reshape(Ra * rc, n, Rb * rd)
         out.append(Y)
     return TtTensor(out)
@@ -457,7 +457,8 @@ def tt_round(t, eps, max_rank=None):
         cores[k] = f.U(keep).reshape(r0, n, keep)
         carry = f.SVt(keep)
         nxt = cores[k + 1]
-        cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1)).reshape(keep, nxt.shape[1], nxt.shape[2])
+        cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1), emulate=True).reshape(keep, nxt.shape[1],
+                                                                                         nxt.shape[2])
     return _unfused(cores, tag)
 
 

@@ -81,7 +81,7 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
                 ev.record(copy)
             comp.wait_event(ev)
             for a in range(a0, a1):
-                T = L.tdot(Md[a], xk, ([1], [1]))                  # (i, b, c, d)
+                T = L.tdot(Md[a], xk, ([1], [1]), emulate=True)    # (i, b, c, d)
                 L.permute(T, (2, 0, 1, 3), out=Yv[a])              # (c, i, b, d)
         Md.record_stream(comp)
         cores.append(Y)
@@ -146,7 +146,8 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
                 cores[k] = Uk.view(r0, n, keep)
                 carry = f.SVt(keep)
                 nxt = cores[k + 1]
-                cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1)).reshape(keep, nxt.shape[1], nxt.shape[2])
+                cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1), emulate=True).reshape(
+                    keep, nxt.shape[1], nxt.shape[2])
             download(d - 1, cores[d - 1])
     done = torch.cuda.Event()
     done.record(copy)

@@ -275,3 +275,54 @@ def test_i8gemm_tcgen05_exact(M, N, K):
     call("ttb_i8gemm", M, N, K, ptr(A), ptr(B), ptr(C))
     ref = A.double() @ B.double().t()
     assert torch.equal(C.double(), ref)
+
+
+@pytest.mark.parametrize("tB,graded", [(0, False), (1, False), (0, True)])
+def test_dgemm_ozaki_fp64_accuracy(tB, graded):
+    """Ozaki-scheme FP64 GEMM on the INT8 tensor cores: normwise agreement with the DMMA DGEMM."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(3 + tB)
+    M, N, K = 2048, 512, 1024
+    A = torch.randn(M, K, generator=g, device="cuda", dtype=torch.float64)
+    B = torch.randn((N, K) if tB else (K, N), generator=g, device="cuda", dtype=torch.float64)
+    if graded:
+        A *= torch.logspace(0, -8, K, device="cuda", dtype=torch.float64)[None, :]
+        A *= torch.logspace(0, 6, M, device="cuda", dtype=torch.float64)[:, None]
+    C = torch.empty(M, N, device="cuda", dtype=torch.float64)
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, K)), dtype=torch.uint8, device="cuda")
+    call("ttb_dgemm_ozaki", tB, M, N, K, ptr(A), K, ptr(B), K if tB else N, ptr(C), N, ptr(ws))
+    Cd = L.gemm(A, B, tB=bool(tB))
+    scale = A.abs() @ (B.abs().t() if tB else B.abs())
+    assert float(((C - Cd).abs() / scale).max()) < (2e-12 if graded else 1e-14)
+    assert float((C - Cd).norm() / Cd.norm()) < (1e-12 if graded else 1e-14)
+    # operands reproduce exactly through the slices (I x B, incl. tiny negatives next to large entries)
+    I = torch.eye(K, dtype=torch.float64, device="cuda")
+    Bk = (B.t().contiguous() if tB else B).clone()
+    Bk[0, :8] = -2.0 ** -60
+    C2 = torch.empty(K, N, device="cuda", dtype=torch.float64)
+    ws2 = torch.empty(int(call_raw("ttb_ozaki_workspace", K, N, K)), dtype=torch.uint8, device="cuda")
+    call("ttb_dgemm_ozaki", 0, K, N, K, ptr(I), K, ptr(Bk), N, ptr(C2), N, ptr(ws2))
+    assert float(((C2 - Bk).abs() / Bk.abs().max(0).values).max()) < 2 ** -54
+
+
+def test_round_with_emulated_gemms_matches_dmma(monkeypatch):
+    """tt_round(tt_matvec) with the large products on the Ozaki path == the all-DMMA result."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import tt_matvec, tt_norm, tt_round, tt_sub
+    from paper_2509_13224_b200.workloads import matvec_round_instance
+    A, X = matvec_round_instance(512, 16, 64, 3, seed=1)
+    launched = []
+    orig = L.call
+
+    def spy(name, *a):
+        launched.append(name)
+        return orig(name, *a)
+
+    monkeypatch.setattr(L, "call", spy)
+    Y1 = tt_round(tt_matvec(A, X), 1e-8)
+    assert "ttb_dgemm_ozaki" in launched
+    monkeypatch.setattr(L, "_OZAKI", False)
+    Y2 = tt_round(tt_matvec(A, X), 1e-8)
+    assert Y1.ranks == Y2.ranks
+    assert tt_norm(tt_sub(Y1, Y2)) <= 1e-12 * tt_norm(Y2)

@@ -179,14 +179,23 @@ int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int 
  * A (int8 M x K row-major) B (int8 N x K row-major)^T; M, N, K multiples of 128. Building block of the
  * Ozaki-scheme FP64 emulation. */
 int ttb_i8gemm(void* stream, int M, int N, int K, const void* A, const void* B, int* C);
-/* FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme, 7 exact 8-bit slices per operand,
- * 55-bit operands, exact int32 level sums): C (M x N, ldc) = A (M x K row-major, lda) op(B), op(B) = B
+/* FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme, 7 balanced 8-bit slices per operand,
+ * 54-bit operands, exact int32 level sums): C (M x N, ldc) = A (M x K row-major, lda) op(B), op(B) = B
  * (K x N, ldb) for tB = 0 or B^T (B: N x K) for tB = 1. Replaces ttb_dgemm for large tcgen05-tileable
- * shapes (ttb_ozaki_applies); ws: ttb_ozaki_workspace bytes. */
+ * shapes (ttb_ozaki_applies: M % 128, N % 64, K % 64); ws: ttb_ozaki_workspace bytes. */
 long long ttb_ozaki_workspace(int M, int N, int K); /* bytes */
 int ttb_ozaki_applies(int M, int N, int K);
 int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, long long lda, const double* B,
                     long long ldb, double* C, long long ldc, void* ws);
+/* General form C = alpha A op(B) + beta C (same workspace). Any K % 64 == 0: K ranges of 4096 are summed
+ * exactly in TMEM and combined in int64; with fewer output tiles than SMs the K dimension is split across
+ * CTAs (partials reduced in a fixed order). */
+int ttb_dgemm_ozaki_ex(void* stream, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                       const double* B, long long ldb, double beta, double* C, long long ldc, void* ws);
+/* Gram matrix G (n x n) = X^T X of a row-major m x n X, FP64 via the Ozaki scheme (columns sliced once,
+ * upper block triangle computed, mirrored); n % 128 == 0, m % 64 == 0 (else workspace 0 / TTB_EARG). */
+long long ttb_ozaki_gram_workspace(int m, int n); /* bytes */
+int ttb_ozaki_gram(void* stream, int m, int n, const double* X, long long ldx, double* G, long long ldg, void* ws);
 
 #ifdef __cplusplus
 }

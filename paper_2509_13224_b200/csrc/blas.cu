@@ -619,6 +619,35 @@ __global__ void sum_final(int np, const double* part, double* out, int take_sqrt
 
 }  // namespace
 
+TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                      long long sA, const double* B, long long ldb, long long sB, double beta, double* C, long long ldc,
+                      long long sC, int batch);
+int ozaki_gemm(cudaStream_t st, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+               const double* B, long long ldb, double beta, double* C, long long ldc, void* ws);
+long long ozaki_ws_bytes(int M, int N, int K);
+bool ozaki_shape_ok(int M, int N, int K);
+
+// The Householder WY products of the tall QRs (qr.cu): W = C V^T with K = the long dimension and the
+// trailing update C += alpha W2 V with K = 128. With TTB_OZAKI_QR=1, large tileable shapes (M N K >= 2^33)
+// run as Ozaki-scheme FP64 on the int8 tensor cores (ozaki.cu; split-K with exact int64 level sums for
+// long K, beta epilogue for the update).
+int dgemm_wy(void* stream, int tB, int M, int N, int K, double alpha, const double* A, long long lda, const double* B,
+             long long ldb, double beta, double* C, long long ldc) {
+  // opt-in (TTB_OZAKI_QR=1): measured slower than DMMA for these low-intensity shapes (geqrf 1M x 1024:
+  // 175 vs 115 ms) -- operand slicing moves ~30 bytes per element of C against 2 x 128 flops, and the
+  // K = 128 updates are TMEM-drain bound
+  static const bool on = [] {
+    const char* e = getenv("TTB_OZAKI_QR");
+    return e && e[0] == '1';
+  }();
+  if (on && (long long)M * N * K >= (1LL << 33) && ozaki_shape_ok(M, N, K)) {
+    cudaStream_t st = as_stream(stream);
+    void* ws = scratch((size_t)ozaki_ws_bytes(M, N, K), st);
+    if (ws) return ozaki_gemm(st, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws);
+  }
+  return ttb_dgemm(stream, 0, tB, M, N, K, alpha, A, lda, 0, B, ldb, 0, beta, C, ldc, 0, 1);
+}
+
 static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A,
                           long long lda, long long sA, const double* B, long long ldb, long long sB, double beta,
                           double* C, long long ldc, long long sC, int batch);

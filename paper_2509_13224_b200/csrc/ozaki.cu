@@ -107,29 +107,12 @@ __device__ __forceinline__ void oz_issue(uint32_t tmem, uint64_t da, uint64_t db
   }
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
-      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
-}
-
-// v 2^e, bit-identical to ldexp (a multiplication by an exact power of two rounds once, like ldexp,
-// when the result is subnormal); ldexp itself only where 2^e is not a normal double
-__device__ __forceinline__ double oz_scale(double v, int e) {
-  return (e > -1023 && e < 1024) ? v * __longlong_as_double((long long)(e + 1023) << 52) : ldexp(v, e);
 }
 
 constexpr int OA_EPAD = 17;  // epilogue staging row (doubles) of a warp's 32 x 16 block
@@ -139,11 +122,40 @@ constexpr int OA_EPAD = 17;  // epilogue staging row (doubles) of a warp's 32 x 
 // columns: 8 levels x 64); the producer runs ahead into the next tile's stages while the epilogue
 // drains TMEM, and the epilogue's C write overlaps the next tile's MMAs (TMEM is released as soon as
 // the level sums are in registers).
-template <int LEV>
+// Output of one work unit (a 128 x 64 tile over one K range): mode 0 out = x; mode 1 out + range * so
+// = x (split-K partials, reduced by oz_reduce_kernel); mode 2 out = alpha x + beta out.
+struct OzOut {
+  double* out;
+  long long ldo, so;
+  double alpha, beta;
+  int mode;
+};
+
+constexpr int OZ_SUB = 64;
+
+// tile t -> (m0, n0); sym: only the tiles touching the upper block triangle of a square output
+// (column block >= 2 x row block), row by row
+__device__ __forceinline__ void oz_tile(int t, int ntn, int sym, int& m0, int& n0) {
+  if (!sym) {
+    m0 = (t / ntn) * OZ_M;
+    n0 = (t % ntn) * OA_N;
+    return;
+  }
+  int mt = 0;
+  while (t >= ntn - 2 * mt) {
+    t -= ntn - 2 * mt;
+    ++mt;
+  }
+  m0 = mt * OZ_M;
+  n0 = (2 * mt + t) * OA_N;
+}  // k steps (of 64) per TMEM accumulation: K <= 4096 keeps every level sum exact in int32
+
+template <int LEV, bool LONGK>  // LONGK: K ranges deeper than OZ_SUB k steps (several TMEM accumulations)
 __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-                                                        const int* __restrict__ ea, const int* __restrict__ fb,
-                                                        double* C, long long ldc) {
+                                                        int kchunk, int ksplit, int tiles, int sym,
+                                                        const int* __restrict__ ea,
+                                                        const int* __restrict__ fb, const OzOut o) {
   extern __shared__ __align__(1024) uint8_t dyn[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[OA_ST], empty[OA_ST], tfull, tempty;
@@ -169,13 +181,17 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
-  const int nk = K / OA_K, ntn = N / OA_N, tiles = (M / OZ_M) * ntn;
+  // work unit u: K range u / tiles (kchunk deep), tile u % tiles (n fastest, so CTAs that run
+  // together share the A rows); a range is accumulated in TMEM OZ_SUB k steps at a time
+  const int ntn = N / OA_N, units = tiles * ksplit;
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: per stage one box of all 7 A slice tiles, one of all 7 B
       int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile / ntn) * OZ_M, n0 = (tile % ntn) * OA_N;
-        for (int kt = 0; kt < nk; ++kt, ++it) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n0;
+        oz_tile(u % tiles, ntn, sym, m0, n0);
+        const int kt0 = (u / tiles) * (kchunk / OA_K), kt1 = min(K, (u / tiles + 1) * kchunk) / OA_K;
+        for (int kt = kt0; kt < kt1; ++kt, ++it) {
           const int st = it % OA_ST;
           if (it >= OA_ST) mbar_wait(smem_u32(&empty[st]), ((it / OA_ST) - 1) & 1);
           const uint32_t fbar = smem_u32(&full[st]);
@@ -189,25 +205,29 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      int it = 0, tl = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tl) {
-        if (tl > 0) {  // the epilogue has the previous tile's level sums in registers
-          mbar_wait(smem_u32(&tempty), (tl - 1) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;\n");
-        }
-        for (int kt = 0; kt < nk; ++kt, ++it) {
-          const int st = it % OA_ST;
-          mbar_wait(smem_u32(&full[st]), (it / OA_ST) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;\n");
-          const uint32_t a0 = smem_u32(sm + st * OA_SBYTES), b0 = a0 + OZ_S * OA_ABYTES;
-          const uint64_t da = sw_desc(a0), db = sw_desc(b0);
+      int it = 0, g = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int kt0 = (u / tiles) * (kchunk / OA_K), kt1 = min(K, (u / tiles + 1) * kchunk) / OA_K;
+        for (int ks = kt0; ks < kt1; ks += OZ_SUB, ++g) {
+          if (g > 0) {  // the epilogue has the previous accumulation's level sums in registers
+            mbar_wait(smem_u32(&tempty), (g - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+          }
+          const int ke = min(kt1, ks + OZ_SUB);
+          for (int kt = ks; kt < ke; ++kt, ++it) {
+            const int st = it % OA_ST;
+            mbar_wait(smem_u32(&full[st]), (it / OA_ST) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const uint32_t a0 = smem_u32(sm + st * OA_SBYTES), b0 = a0 + OZ_S * OA_ABYTES;
+            const uint64_t da = sw_desc(a0), db = sw_desc(b0);
 #pragma unroll
-          for (int kk = 0; kk < OA_K / 32; ++kk) oz_issue<LEV>(tmem, da, db, kk, kt == 0 && kk == 0);
+            for (int kk = 0; kk < OA_K / 32; ++kk) oz_issue<LEV>(tmem, da, db, kk, kt == ks && kk == 0);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&empty[st])));
+          }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-              smem_u32(&empty[st])));
+              smem_u32(&tfull)));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            smem_u32(&tfull)));
       }
     }
   } else {
@@ -222,36 +242,45 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
     double* stg = reinterpret_cast<double*>(sm + OA_ST * OA_SBYTES) + (warp - 2) * 32 * OA_EPAD;
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 32);
     constexpr int LO_EXP = -12 - 8 * (LEV - 1);
-    int tl = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tl) {
-      const int m0 = (tile / ntn) * OZ_M, n0 = (tile % ntn) * OA_N + h * 32;
+    int g = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int m0, n0;
+      oz_tile(u % tiles, ntn, sym, m0, n0);
+      n0 += h * 32;
+      const int kt0 = (u / tiles) * (kchunk / OA_K);
+      const int kt1 = LONGK ? min(K, (u / tiles + 1) * kchunk) / OA_K : 0;
       const int my_ea = ea[m0 + q * 32 + lane];
       const int my_fb = fb[n0 + lane];  // column n0 + lane's exponent, broadcast per column below
-      mbar_wait(smem_u32(&tfull), tl & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n");
       long long hi[32], lo[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0;
+      for (int ks = kt0;;) {
+        mbar_wait(smem_u32(&tfull), g & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll
-      for (int d = 0; d < LEV; ++d) {
-        const long long sh = 1LL << (d < 4 ? 8 * (3 - d) : 8 * (LEV - 1 - d));
+        for (int d = 0; d < LEV; ++d) {
+          const long long sh = 1LL << (d < 4 ? 8 * (3 - d) : 8 * (LEV - 1 - d));
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {  // 16 columns per load (10 warps: 168 registers per thread)
-          uint32_t v[16];
-          tmem_ld16(tq + (uint32_t)(d * OA_N + g * 16), v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+          for (int gg = 0; gg < 2; ++gg) {  // 16 columns per load (10 warps: 168 registers per thread)
+            uint32_t v[16];
+            tmem_ld16(tq + (uint32_t)(d * OA_N + gg * 16), v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            if (d < 4)
-              hi[g * 16 + c] += (long long)(int)v[c] * sh;
-            else
-              lo[g * 16 + c] += (long long)(int)v[c] * sh;
+            for (int c = 0; c < 16; ++c) {
+              if (d < 4)
+                hi[gg * 16 + c] += (long long)(int)v[c] * sh;
+              else
+                lo[gg * 16 + c] += (long long)(int)v[c] * sh;
+            }
           }
         }
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&tempty)) : "memory");
+        ++g;
+        ks += OZ_SUB;
+        if (!LONGK || ks >= kt1) break;
       }
-      asm volatile("tcgen05.fence::before_thread_sync;\n");
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&tempty)) : "memory");
       const int cq = lane & 15, half = lane >> 4;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -269,11 +298,21 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
           stg[lane * OA_EPAD + c] = x;
         }
         __syncwarp();
-        double* crow = C + (long long)(m0 + q * 32) * ldc + n0 + j * 16 + cq;
+        double* crow = o.out + (o.mode == 1 ? (long long)(u / tiles) * o.so : 0LL) + (long long)(m0 + q * 32) * o.ldo +
+                       n0 + j * 16 + cq;
+        if (o.mode == 2) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int rr = 2 * i + half;
-          crow[(long long)rr * ldc] = stg[rr * OA_EPAD + cq];
+          for (int i = 0; i < 16; ++i) {
+            const int rr = 2 * i + half;
+            const double y = o.alpha * stg[rr * OA_EPAD + cq];
+            crow[(long long)rr * o.ldo] = o.beta == 0.0 ? y : fma(o.beta, crow[(long long)rr * o.ldo], y);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int rr = 2 * i + half;
+            crow[(long long)rr * o.ldo] = stg[rr * OA_EPAD + cq];
+          }
         }
         __syncwarp();
       }
@@ -296,6 +335,32 @@ __global__ void oz_rowexp_kernel(int rows, int K, const double* __restrict__ X, 
     int ex = 0;
     if (m > 0.0) frexp(m, &ex);
     e[w] = ex;
+  }
+}
+
+// row maxima of a row-major (rows x K, ld) matrix with long rows: warp per (row, 8192-wide segment),
+// atomicMax of the non-negative bit pattern (then oz_colexp_kernel)
+__global__ void oz_rowmax_kernel(int rows, int K, const double* __restrict__ X, long long ld,
+                                 unsigned long long* rmax) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int k0 = blockIdx.y * 8192, k1 = min(K, k0 + 8192);
+  double m = 0.0;
+  for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs(X[(long long)r * ld + k]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomicMax(rmax + r, (unsigned long long)__double_as_longlong(m));
+}
+
+// C = alpha sum_s part[s] + beta C (fixed summation order: deterministic)
+__global__ void oz_reduce_kernel(int M, int N, int S, const double* __restrict__ part, double alpha, double beta,
+                                 double* C, long long ldc) {
+  const long long tot = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < S; ++s) acc += part[(long long)s * tot + e];
+    const long long i = e / N, j = e % N;
+    double* c = C + i * ldc + j;
+    *c = beta == 0.0 ? alpha * acc : fma(beta, *c, alpha * acc);
   }
 }
 
@@ -413,67 +478,207 @@ bool oz_tmap(CUtensorMap* tm, const void* ptr, int rows, int K, int box_rows, in
 
 }  // namespace
 
-// Workspace (bytes) of ttb_dgemm_ozaki: slice stacks of A and B, exponents, column maxima.
-TTB_API long long ttb_ozaki_workspace(int M, int N, int K) {
-  return (long long)OZ_S * ((long long)M + N) * K + 4LL * (M + N) + 8LL * N + 1024;
-}
-
-// Whether ttb_dgemm_ozaki takes this shape (tcgen05 tiles and exact int32 accumulation).
 namespace {
-bool oz_applies_all(int M, int N, int K) {
-  return M > 0 && N > 0 && K > 0 && M % 128 == 0 && N % 64 == 0 && K % 64 == 0 && K <= 4096;
-}
-}  // namespace
+bool oz_shape_ok(int M, int N, int K) { return M > 0 && N > 0 && K > 0 && M % 128 == 0 && N % 64 == 0 && K % 64 == 0; }
 
-TTB_API int ttb_ozaki_applies(int M, int N, int K) { return oz_applies_all(M, N, K) ? 1 : 0; }
-
-// C (M x N, ldc) = op(A) (M x K) B (K x N), FP64 via the Ozaki scheme on the INT8 tensor cores.
-// A: row-major M x K (lda) when tA == 0; B: row-major K x N (ldb) when tB == 0, N x K (ldb) when tB == 1.
-// ws: ttb_ozaki_workspace bytes (device). Returns TTB_EARG for shapes ttb_ozaki_applies rejects.
-TTB_API int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, long long lda,
-                            const double* B, long long ldb, double* C, long long ldc, void* ws) {
-  if (!oz_applies_all(M, N, K)) return TTB_EARG;
-  cudaStream_t st = as_stream(stream);
-  uint8_t* As = reinterpret_cast<uint8_t*>(ws);
-  uint8_t* Bs = As + (long long)OZ_S * M * K;
-  int* ea = reinterpret_cast<int*>(Bs + (long long)OZ_S * N * K);
-  int* fb = ea + M;
-  unsigned long long* cmax =
-      reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(fb + N + 2) & ~uintptr_t(7));
-  oz_rowexp_kernel<<<ceil_div((long long)M * 32, 256), 256, 0, st>>>(M, K, A, lda, ea); ttb_count();
-  oz_slice_rows_kernel<<<148 * 16, 256, 0, st>>>(M, K, A, lda, ea, As); ttb_count();
-  if (tB) {
-    oz_rowexp_kernel<<<ceil_div((long long)N * 32, 256), 256, 0, st>>>(N, K, B, ldb, fb); ttb_count();
-    oz_slice_rows_kernel<<<148 * 16, 256, 0, st>>>(N, K, B, ldb, fb, Bs); ttb_count();
-  } else {
-    cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * N, st);
-    oz_colmax_kernel<<<dim3(ceil_div(N, 256), ceil_div(K, 256)), 256, 0, st>>>(K, N, B, ldb, cmax); ttb_count();
-    oz_colexp_kernel<<<ceil_div(N, 256), 256, 0, st>>>(N, cmax, fb); ttb_count();
-    oz_slice_cols_kernel<<<dim3(ceil_div(N, 64), ceil_div(K, 64)), 256, 0, st>>>(K, N, B, ldb, fb, Bs); ttb_count();
-  }
-  CUtensorMap ta, tb;
-  if (!oz_tmap(&ta, As, M, K, OZ_M, OA_K) || !oz_tmap(&tb, Bs, N, K, OA_N, OA_K)) return TTB_EARG;
-  const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
-  static bool cfg_all = false;
-  static int nsm = 148;
-  if (!cfg_all) {
-    cudaFuncSetAttribute(oz_gemm_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(oz_gemm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+int oz_nsm() {
+  static int nsm = 0;
+  if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  return nsm;
+}
+
+long long oz_tiles(int M, int N, int sym) {
+  const long long ntn = N / OA_N, nmt = M / OZ_M;
+  if (!sym) return nmt * ntn;
+  long long t = 0;
+  for (long long mt = 0; mt < nmt; ++mt) t += ntn - 2 * mt > 0 ? ntn - 2 * mt : 0;
+  return t;
+}
+
+// K ranges: with fewer output tiles than SMs the K dimension is split (ranges >= 1024 deep) to fill
+// the persistent grid; the split count maximizes units / (SMs x rounds), ties to fewer splits
+void oz_split(long long tiles, int K, int* ks, int* kchunk) {
+  const int nsm = oz_nsm();
+  int best = 1;
+  double best_eff = 0.0;
+  const int kmax = K / 1024 > 1 ? K / 1024 : 1;
+  for (int s = 1; s <= kmax && s <= 256; ++s) {
+    const long long units = tiles * s;
+    const long long rounds = (units + nsm - 1) / nsm;
+    const double eff = (double)units / ((double)rounds * nsm);
+    if (eff > best_eff * 1.02) { best_eff = eff; best = s; }
+    if (tiles * s >= 4LL * nsm) break;
+  }
+  int kc = (int)(((long long)K + best - 1) / best);
+  kc = (kc + OA_K - 1) / OA_K * OA_K;
+  *kchunk = kc;
+  *ks = (K + kc - 1) / kc;
+}
+
+struct OzWs {
+  uint8_t *As, *Bs;
+  int *ea, *fb;
+  unsigned long long *amax, *bmax;
+  double* part;
+  long long bytes;
+};
+
+// gram: A and B are the same slice stack (B's pointers alias A's)
+OzWs oz_ws_layout(void* base, int M, int N, int K, int gram) {
+  int ks, kc;
+  oz_split(oz_tiles(M, N, gram), K, &ks, &kc);
+  OzWs w;
+  uintptr_t p = reinterpret_cast<uintptr_t>(base);
+  const uintptr_t p0 = p;
+  auto take = [&](long long bytes) { const uintptr_t r = p; p = (p + bytes + 255) & ~uintptr_t(255); return r; };
+  w.As = reinterpret_cast<uint8_t*>(take((long long)OZ_S * M * K));
+  w.Bs = gram ? w.As : reinterpret_cast<uint8_t*>(take((long long)OZ_S * N * K));
+  w.ea = reinterpret_cast<int*>(take(4LL * M));
+  w.fb = gram ? w.ea : reinterpret_cast<int*>(take(4LL * N));
+  w.amax = reinterpret_cast<unsigned long long*>(take(8LL * M));
+  w.bmax = gram ? w.amax : reinterpret_cast<unsigned long long*>(take(8LL * N));
+  w.part = reinterpret_cast<double*>(take(ks > 1 ? 8LL * ks * M * N : 8));
+  w.bytes = (long long)(p - p0) + 256;
+  return w;
+}
+
+// exponents (and slices) of the rows of a row-major (rows x K, ld) operand
+void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, int* e, unsigned long long* rmax,
+             uint8_t* out) {
+  if (K > 16384) {
+    cudaMemsetAsync(rmax, 0, sizeof(unsigned long long) * rows, st);
+    oz_rowmax_kernel<<<dim3(ceil_div(rows, 8), ceil_div(K, 8192)), 256, 0, st>>>(rows, K, X, ld, rmax); ttb_count();
+    oz_colexp_kernel<<<ceil_div(rows, 256), 256, 0, st>>>(rows, rmax, e); ttb_count();
+  } else {
+    oz_rowexp_kernel<<<ceil_div((long long)rows * 32, 256), 256, 0, st>>>(rows, K, X, ld, e); ttb_count();
+  }
+  oz_slice_rows_kernel<<<148 * 16, 256, 0, st>>>(rows, K, X, ld, e, out); ttb_count();
+}
+
+// exponents (and transposed slices) of the columns of a row-major (K x cols, ld) operand
+void oz_cols(cudaStream_t st, int K, int cols, const double* X, long long ld, int* e, unsigned long long* cmax,
+             uint8_t* out) {
+  cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * cols, st);
+  oz_colmax_kernel<<<dim3(ceil_div(cols, 256), ceil_div(K, 256)), 256, 0, st>>>(K, cols, X, ld, cmax); ttb_count();
+  oz_colexp_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(cols, cmax, e); ttb_count();
+  oz_slice_cols_kernel<<<dim3(ceil_div(cols, 64), ceil_div(K, 64)), 256, 0, st>>>(K, cols, X, ld, e, out); ttb_count();
+}
+
+// G[i][j] = G[j][i] below the computed block triangle (j < 128 floor(i / 128))
+__global__ void oz_mirror_kernel(int n, double* G, long long ldg) {
+  const long long tot = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    if (j < (i / OZ_M) * OZ_M) G[(long long)i * ldg + j] = G[(long long)j * ldg + i];
+  }
+}
+
+// the int8 GEMM over prepared slices + split-K reduction (+ mirror for sym)
+int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, double beta, double* C, long long ldc,
+           int sym) {
+  CUtensorMap ta, tb;
+  if (!oz_tmap(&ta, w.As, M, K, OZ_M, OA_K) || !oz_tmap(&tb, w.Bs, N, K, OA_N, OA_K)) return TTB_EARG;
+  const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
+  static bool cfg_all = false;
+  if (!cfg_all) {
+    cudaFuncSetAttribute(oz_gemm_kernel<7, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(oz_gemm_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(oz_gemm_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cfg_all = true;
   }
   static const int levels = [] {
     const char* e = getenv("TTB_OZAKI_LEVELS");
     return e && atoi(e) == 7 ? 7 : 8;
   }();
-  const int tiles = (M / OZ_M) * (N / OA_N);
-  const int grid = tiles < nsm ? tiles : nsm;
-  if (levels == 7)
-    oz_gemm_kernel<7><<<grid, 320, smem, st>>>(ta, tb, M, N, K, ea, fb, C, ldc);
+  const long long tiles = oz_tiles(M, N, sym);
+  int ks, kc;
+  oz_split(tiles, K, &ks, &kc);
+  OzOut o;
+  if (ks > 1)
+    o = OzOut{w.part, N, (long long)M * N, 1.0, 0.0, 1};
   else
-    oz_gemm_kernel<8><<<grid, 320, smem, st>>>(ta, tb, M, N, K, ea, fb, C, ldc);
+    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2};
+  const long long units = tiles * ks;
+  const int grid = units < oz_nsm() ? (int)units : oz_nsm();
+  if (kc > OZ_SUB * OA_K)
+    oz_gemm_kernel<8, true><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
+  else if (levels == 7)
+    oz_gemm_kernel<7, false><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
+  else
+    oz_gemm_kernel<8, false><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
   ttb_count();
+  if (ks > 1) {
+    const long long tot = (long long)M * N;
+    int blocks = ceil_div(tot, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    oz_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, ks, w.part, alpha, beta, C, ldc); ttb_count();
+  }
+  if (sym) {
+    const long long tot = (long long)M * N;
+    int blocks = ceil_div(tot, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    oz_mirror_kernel<<<blocks, 256, 0, st>>>(M, C, ldc); ttb_count();
+  }
   return ttb_last_error();
+}
+}  // namespace
+
+// Workspace (bytes) of ttb_dgemm_ozaki: slice stacks of A and B, exponents, maxima, split-K partials.
+long long ozaki_ws_bytes(int M, int N, int K) {
+  if (!oz_shape_ok(M, N, K)) return 0;
+  return oz_ws_layout(nullptr, M, N, K, 0).bytes;
+}
+bool ozaki_shape_ok(int M, int N, int K) { return oz_shape_ok(M, N, K); }
+
+// C (M x N, ldc) = alpha A B + beta C, FP64 via the Ozaki scheme on the INT8 tensor cores. A: row-major
+// M x K (lda); B: row-major K x N (ldb) when tB == 0, N x K (ldb) when tB == 1. ws: ozaki_ws_bytes.
+int ozaki_gemm(cudaStream_t st, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+               const double* B, long long ldb, double beta, double* C, long long ldc, void* ws) {
+  if (!oz_shape_ok(M, N, K)) return TTB_EARG;
+  OzWs w = oz_ws_layout(ws, M, N, K, 0);
+  oz_rows(st, M, K, A, lda, w.ea, w.amax, w.As);
+  if (tB)
+    oz_rows(st, N, K, B, ldb, w.fb, w.bmax, w.Bs);
+  else
+    oz_cols(st, K, N, B, ldb, w.fb, w.bmax, w.Bs);
+  return oz_run(st, w, M, N, K, alpha, beta, C, ldc, 0);
+}
+
+TTB_API long long ttb_ozaki_workspace(int M, int N, int K) { return ozaki_ws_bytes(M, N, K); }
+
+// Whether ttb_dgemm_ozaki takes this shape (M % 128, N % 64, K % 64; any K: ranges of 4096 are
+// accumulated exactly in TMEM and combined in int64).
+TTB_API int ttb_ozaki_applies(int M, int N, int K) { return oz_shape_ok(M, N, K) ? 1 : 0; }
+
+// C (M x N, ldc) = A op(B), FP64 via the Ozaki scheme (see ozaki_gemm). ws: ttb_ozaki_workspace bytes.
+// Returns TTB_EARG for shapes ttb_ozaki_applies rejects.
+TTB_API int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, long long lda,
+                            const double* B, long long ldb, double* C, long long ldc, void* ws) {
+  return ozaki_gemm(as_stream(stream), tB, M, N, K, 1.0, A, lda, B, ldb, 0.0, C, ldc, ws);
+}
+
+// General form: C = alpha A op(B) + beta C.
+TTB_API int ttb_dgemm_ozaki_ex(void* stream, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                               const double* B, long long ldb, double beta, double* C, long long ldc, void* ws) {
+  return ozaki_gemm(as_stream(stream), tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws);
+}
+
+// Gram matrix G (n x n, ldg) = X^T X of a row-major m x n X (ldx), FP64 via the Ozaki scheme: X's
+// columns are sliced once (they are both operands), only the output tiles touching the upper block
+// triangle are computed, the rest is mirrored. n % 128 == 0, m % 64 == 0.
+TTB_API long long ttb_ozaki_gram_workspace(int m, int n) {
+  if (!oz_shape_ok(n, n, m) || n % OZ_M) return 0;
+  return oz_ws_layout(nullptr, n, n, m, 1).bytes;
+}
+TTB_API int ttb_ozaki_gram(void* stream, int m, int n, const double* X, long long ldx, double* G, long long ldg, void* ws) {
+  if (!oz_shape_ok(n, n, m) || n % OZ_M) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  OzWs w = oz_ws_layout(ws, n, n, m, 1);
+  oz_cols(st, m, n, X, ldx, w.ea, w.amax, w.As);
+  return oz_run(st, w, n, n, m, 1.0, 0.0, G, ldg, 1);
 }

@@ -14,6 +14,10 @@ TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double 
 // tsqr.cu
 long long tsqr_workspace(long long m);
 long long cholqr_workspace(long long m, int b);
+// blas.cu: large WY products (W = C V^T over the long dimension, C -= W2 V) as Ozaki-scheme FP64 on the
+// int8 tensor cores when the shape allows, else ttb_dgemm
+int dgemm_wy(void* stream, int tB, int M, int N, int K, double alpha, const double* A, long long lda, const double* B,
+             long long ldb, double beta, double* C, long long ldc);
 int cholqr_block(cudaStream_t st, long long mp, int b, double* P, long long lda, double* tau, double* Vtop,
                  double* T, double* ws);
 constexpr int TTB_CHOLQR_FALLBACK = -50;
@@ -603,11 +607,11 @@ int grid_v(long long tot) {
 // transT = 1 applies Q^T (geqrf trailing update), 0 applies Q (orgqr).
 int apply_wy(void* stream, int mp, int nq, int jb, const double* V, const double* T, int transT, double* C,
              long long ldc, double* W, double* W2) {
-  int rc = ttb_dgemm(stream, 0, 1, nq, jb, mp, 1.0, C, ldc, 0, V, mp, 0, 0.0, W, jb, 0, 1);
+  int rc = dgemm_wy(stream, 1, nq, jb, mp, 1.0, C, ldc, V, mp, 0.0, W, jb);
   if (rc) return rc;
   rc = ttb_dgemm(stream, 0, transT ? 0 : 1, nq, jb, jb, 1.0, W, jb, 0, T, jb, 0, 0.0, W2, jb, 0, 1);
   if (rc) return rc;
-  return ttb_dgemm(stream, 0, 0, nq, mp, jb, -1.0, W2, jb, 0, V, mp, 0, 1.0, C, ldc, 0, 1);
+  return dgemm_wy(stream, 0, nq, mp, jb, -1.0, W2, jb, V, mp, 1.0, C, ldc);
 }
 
 // Same update with V read in place from the factored panel Ap (col-major, ld lda): rows >= jb of V
@@ -616,7 +620,7 @@ int apply_wy_panel(void* stream, int mp, int nq, int jb, const double* Ap, long 
                    const double* T, int transT, double* C, long long ldc, double* W, double* W2) {
   const int mb = mp - jb;
   int rc = 0;
-  if (mb > 0) rc = ttb_dgemm(stream, 0, 1, nq, jb, mb, 1.0, C + jb, ldc, 0, Ap + jb, lda, 0, 0.0, W, jb, 0, 1);
+  if (mb > 0) rc = dgemm_wy(stream, 1, nq, jb, mb, 1.0, C + jb, ldc, Ap + jb, lda, 0.0, W, jb);
   if (rc) return rc;
   rc = ttb_dgemm(stream, 0, 1, nq, jb, jb, 1.0, C, ldc, 0, Vtop, jb, 0, mb > 0 ? 1.0 : 0.0, W, jb, 0, 1);
   if (rc) return rc;
@@ -624,7 +628,7 @@ int apply_wy_panel(void* stream, int mp, int nq, int jb, const double* Ap, long 
   if (rc) return rc;
   rc = ttb_dgemm(stream, 0, 0, nq, jb, jb, -1.0, W2, jb, 0, Vtop, jb, 0, 1.0, C, ldc, 0, 1);
   if (rc || mb <= 0) return rc;
-  return ttb_dgemm(stream, 0, 0, nq, mb, jb, -1.0, W2, jb, 0, Ap + jb, lda, 0, 1.0, C + jb, ldc, 0, 1);
+  return dgemm_wy(stream, 0, nq, mb, jb, -1.0, W2, jb, Ap + jb, lda, 1.0, C + jb, ldc);
 }
 
 // W[q][p] = V[q][p] (rows q < nid of W = C^T V when C's first nid columns are still e_q: orgqr)
@@ -646,8 +650,8 @@ int apply_wy_panel_orgqr(void* stream, int mp, int nq, int jb, int nid, const do
   int rc = 0;
   if (nr > 0) {
     if (mb > 0)
-      rc = ttb_dgemm(stream, 0, 1, nr, jb, mb, 1.0, C + (long long)nid * ldc + jb, ldc, 0, Ap + jb, lda, 0, 0.0,
-                     W + (long long)nid * jb, jb, 0, 1);
+      rc = dgemm_wy(stream, 1, nr, jb, mb, 1.0, C + (long long)nid * ldc + jb, ldc, Ap + jb, lda, 0.0,
+                    W + (long long)nid * jb, jb);
     if (rc) return rc;
     rc = ttb_dgemm(stream, 0, 1, nr, jb, jb, 1.0, C + (long long)nid * ldc, ldc, 0, Vtop, jb, 0, mb > 0 ? 1.0 : 0.0,
                    W + (long long)nid * jb, jb, 0, 1);
@@ -657,7 +661,7 @@ int apply_wy_panel_orgqr(void* stream, int mp, int nq, int jb, int nid, const do
   if (rc) return rc;
   rc = ttb_dgemm(stream, 0, 0, nq, jb, jb, -1.0, W2, jb, 0, Vtop, jb, 0, 1.0, C, ldc, 0, 1);
   if (rc || mb <= 0) return rc;
-  return ttb_dgemm(stream, 0, 0, nq, mb, jb, -1.0, W2, jb, 0, Ap + jb, lda, 0, 1.0, C + jb, ldc, 0, 1);
+  return dgemm_wy(stream, 0, nq, mb, jb, -1.0, W2, jb, Ap + jb, lda, 1.0, C + jb, ldc);
 }
 
 // G = V^T V for the in-place reflectors of apply_wy_panel

@@ -256,6 +256,37 @@ _IMPLICIT_U_MIN_M = int(os.environ.get("TTB_SVD_IMPLICIT_U_MIN_M", "65536"))
 _IMPLICIT_U_MIN_RATIO = 1e-7   # U orthogonality error ~ eps s_max / s_k <= ~1e-9
 
 
+_GRAM = os.environ.get("TTB_SVD_GRAM", "1") != "0"
+_GRAM_MIN_M = int(os.environ.get("TTB_SVD_GRAM_MIN_M", str(1 << 19)))
+_GRAM_MIN_RATIO = 1e-4   # s_min / s_max: singular values from X^T X carry relative error ~ eps (s_max / s)^2
+
+
+def _gram_jacobi(X, m, n):
+    """Right singular vectors and singular values of a very tall X (m x n) without its QR: R from the
+    Cholesky factor of G = X^T X (Ozaki-scheme FP64 Gram on the int8 tensor cores), then the same
+    one-sided Jacobi on R^T as the QR path (R^T R = G, so R differs from the Householder R only by row
+    signs and rounding). Used only when X is well conditioned (s_min >= 1e-4 s_max over ALL singular
+    values, so eps (s_max / s)^2 <= 1e-8 relative and <= 1e-12 s_max absolute); returns
+    (Rt, Vr, S) or None (the caller takes the Householder QR path)."""
+    if not (_GRAM and _OZAKI and m >= _GRAM_MIN_M and n >= 256 and n % 128 == 0 and m % 64 == 0):
+        return None
+    ws = torch.empty(int(call_raw("ttb_ozaki_gram_workspace", m, n)), dtype=torch.uint8, device=device())
+    G = empty(n, n)
+    call("ttb_ozaki_gram", m, n, ptr(X), max(X.stride(0), 1), ptr(G), n, ptr(ws))
+    del ws
+    info = empty(1, dtype=I32)
+    call("ttb_potrf", n, ptr(G), n, ptr(info))   # col-major lower L: row-major view of the buffer = L^T = R
+    if int(info.item()) != 0:
+        return None
+    R = torch.triu(G)
+    Rt = R.t().contiguous()                      # col-major R (the QR path's layout)
+    Vr, S, _ = _jacobi(R, n, False)              # R as col-major R^T: Jacobi on R^T
+    s = S.cpu().numpy()
+    if not (s.max() > 0.0 and s.min() >= _GRAM_MIN_RATIO * s.max()):
+        return None
+    return Rt, Vr, S
+
+
 class SVDFactors:
     """Thin SVD X = U diag(S) Vt by Householder QR + one-sided Jacobi on the triangular factor.
 
@@ -285,9 +316,11 @@ class SVDFactors:
             self.implicit = True
             self.X = X
             self._want_v = want_v
-            _, Rt = qr_colmajor(permute(X, (1, 0)), m, n, want_q=False)
-            self.Rt = Rt
-            self.Vr, self.S, _ = _jacobi(permute(Rt, (1, 0)), n, False)   # rows: right singular vectors
+            got = _gram_jacobi(X, m, n)
+            if got is None:
+                _, Rt = qr_colmajor(permute(X, (1, 0)), m, n, want_q=False)
+                got = (Rt,) + _jacobi(permute(Rt, (1, 0)), n, False)[:2]   # rows: right singular vectors
+            self.Rt, self.Vr, self.S = got
             self.UJ = self.VJ = self.Qt = None
             self._W = None
         elif self.tall:

@@ -306,6 +306,75 @@ def test_dgemm_ozaki_fp64_accuracy(tB, graded):
     assert float(((C2 - Bk).abs() / Bk.abs().max(0).values).max()) < 2 ** -54
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K,tB,alpha,beta", [
+    (1024, 128, 65536, 1, 1.0, 0.0),    # split-K over 144 CTAs, K ranges > 4096 (int64 level sums)
+    (256, 128, 16384, 0, 1.0, 0.0),     # split-K, ranges <= 4096, column-sliced B
+    (256, 8192, 128, 0, -1.0, 1.0),     # WY trailing update: C -= W2 V (beta epilogue)
+    (384, 4096, 256, 1, 0.5, -2.0),     # general alpha / beta
+])
+def test_dgemm_ozaki_ex_splitk_beta(M, N, K, tB, alpha, beta):
+    """ttb_dgemm_ozaki_ex (split-K, beta) against the DMMA DGEMM: normwise and per element relative to
+    |alpha| |A| |B| + |beta C|."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    A = torch.randn(M, K, generator=g, device="cuda", dtype=torch.float64)
+    B = torch.randn((N, K) if tB else (K, N), generator=g, device="cuda", dtype=torch.float64)
+    C0 = torch.randn(M, N, generator=g, device="cuda", dtype=torch.float64)
+    C = C0.clone()
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, K)), dtype=torch.uint8, device="cuda")
+    call("ttb_dgemm_ozaki_ex", tB, M, N, K, alpha, ptr(A), K, ptr(B), K if tB else N, beta, ptr(C), N, ptr(ws))
+    Cd = C0.clone()
+    L.gemm(A, B, tB=bool(tB), alpha=alpha, beta=beta, out=Cd)
+    scale = abs(alpha) * (A.abs() @ (B.abs().t() if tB else B.abs())) + abs(beta) * C0.abs()
+    assert float(((C - Cd).abs() / scale).max()) < 1e-14
+    assert float((C - Cd).norm() / Cd.norm()) < 1e-14
+
+
+@pytest.mark.gpu
+def test_ozaki_gram_matches_dgemm():
+    """ttb_ozaki_gram (X^T X, symmetric tiles + mirror, split-K) against X^T X on DMMA."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for m, n in ((65536, 256), (8192, 640)):
+        X = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+        X *= torch.logspace(0, -3, n, device="cuda", dtype=torch.float64)[None, :]
+        G = torch.empty(n, n, device="cuda", dtype=torch.float64)
+        ws = torch.empty(int(call_raw("ttb_ozaki_gram_workspace", m, n)), dtype=torch.uint8, device="cuda")
+        call("ttb_ozaki_gram", m, n, ptr(X), n, ptr(G), n, ptr(ws))
+        Gd = L.gemm(X, X, tA=True)
+        scale = X.abs().t() @ X.abs()
+        assert float(((G - Gd).abs() / scale).max()) < 1e-14
+        assert torch.equal(G, G.t())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graded", [False, True])
+def test_svd_gram_path(monkeypatch, graded):
+    """Very tall SVDs through the Gram + Cholesky route (well conditioned) and its fallback to the
+    Householder QR route (ill conditioned): singular values and U S V^T against torch (cuSOLVER) FP64."""
+    from paper_2509_13224_b200 import linalg as L
+    monkeypatch.setattr(L, "_GRAM_MIN_M", 65536)
+    calls = []
+    orig = L._gram_jacobi
+    monkeypatch.setattr(L, "_gram_jacobi", lambda *a: calls.append(r := orig(*a)) or r)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    m, n = 65536, 256
+    X = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    if graded:
+        X *= torch.logspace(0, -9, n, device="cuda", dtype=torch.float64)[None, :]
+    f = L.SVDFactors(X)
+    assert f.implicit and len(calls) == 1 and ((calls[0] is None) == graded)
+    S_ref = torch.linalg.svdvals(X)
+    S = f.S.sort(descending=True).values
+    assert float(((S - S_ref).abs() / S_ref[0]).max()) < 1e-13
+    r = n
+    Y = L.gemm(f.U(r), f.SVt(r))
+    assert float((Y - X).norm() / X.norm()) < 1e-13
+
+
 def test_round_with_emulated_gemms_matches_dmma(monkeypatch):
     """tt_round(tt_matvec) with the large products on the Ozaki path == the all-DMMA result."""
     from paper_2509_13224_b200 import linalg as L

@@ -196,6 +196,12 @@ int ttb_dgemm_ozaki_ex(void* stream, int tB, int M, int N, int K, double alpha, 
  * upper block triangle computed, mirrored); n % 128 == 0, m % 64 == 0 (else workspace 0 / TTB_EARG). */
 long long ttb_ozaki_gram_workspace(int m, int n); /* bytes */
 int ttb_ozaki_gram(void* stream, int m, int n, const double* X, long long ldx, double* G, long long ldg, void* ws);
+/* Gram matrix of the rows, G (n x n) = T T^T of a row-major n x m T (same conditions and workspace). */
+long long ttb_ozaki_gram_rows_workspace(int n, int m); /* bytes */
+int ttb_ozaki_gram_rows(void* stream, int n, int m, const double* T, long long ldt, double* G, long long ldg, void* ws);
+/* Linv = L^{-1} of a lower-triangular row-major n x n L (strict upper triangle ignored), n % 128 == 0;
+ * ws: n * n doubles. */
+int ttb_trtri_lower(void* stream, int n, const double* L, long long ldl, double* Li, long long ldi, double* ws);
 
 #ifdef __cplusplus
 }

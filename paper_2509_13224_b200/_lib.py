@@ -69,6 +69,9 @@ SIGNATURES = {
     "ttb_dgemm_ozaki_ex": (i32, [vp, i32, i32, i32, i32, f64, vp, i64, vp, i64, f64, vp, i64, vp]),
     "ttb_ozaki_gram_workspace": (i64, [i32, i32]),
     "ttb_ozaki_gram": (i32, [vp, i32, i32, vp, i64, vp, i64, vp]),
+    "ttb_ozaki_gram_rows_workspace": (i64, [i32, i32]),
+    "ttb_ozaki_gram_rows": (i32, [vp, i32, i32, vp, i64, vp, i64, vp]),
+    "ttb_trtri_lower": (i32, [vp, i32, vp, i64, vp, i64, vp]),
     "ttb_band_gemm": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
     "ttb_local_gemm_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
     "ttb_local_gemm_ws_init": (i32, [vp, i32, i32, i32, i32, i32, vp]),

@@ -682,3 +682,15 @@ TTB_API int ttb_ozaki_gram(void* stream, int m, int n, const double* X, long lon
   oz_cols(st, m, n, X, ldx, w.ea, w.amax, w.As);
   return oz_run(st, w, n, n, m, 1.0, 0.0, G, ldg, 1);
 }
+
+// Gram matrix of the ROWS, G (n x n) = T T^T of a row-major n x m T (ldt): rows sliced once (long rows:
+// two-pass maxima), upper block triangle computed, mirrored. n % 128 == 0, m % 64 == 0.
+TTB_API long long ttb_ozaki_gram_rows_workspace(int n, int m) { return ttb_ozaki_gram_workspace(m, n); }
+TTB_API int ttb_ozaki_gram_rows(void* stream, int n, int m, const double* T, long long ldt, double* G, long long ldg,
+                                void* ws) {
+  if (!oz_shape_ok(n, n, m) || n % OZ_M) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  OzWs w = oz_ws_layout(ws, n, n, m, 1);
+  oz_rows(st, n, m, T, ldt, w.ea, w.amax, w.As);
+  return oz_run(st, w, n, n, m, 1.0, 0.0, G, ldg, 1);
+}

@@ -217,6 +217,61 @@ def qr_colmajor(Acm, m, n, want_q=True, want_r=True, overlap_r=None):
     return Qt, Rt
 
 
+_CHOLQR2 = os.environ.get("TTB_RL_CHOLQR2", "1") != "0"
+_CHOLQR2_MIN_M = int(os.environ.get("TTB_RL_CHOLQR2_MIN_M", str(1 << 19)))
+
+
+def _chol_rows(T, n, m, offdiag=False):
+    """Row-major lower Cholesky factor L of G = T T^T (T: n x m row-major, Ozaki-scheme Gram), or None;
+    offdiag: also max |G_ij| over i != j (read from the triangle potrf leaves untouched)."""
+    ws = torch.empty(int(call_raw("ttb_ozaki_gram_rows_workspace", n, m)), dtype=torch.uint8, device=device())
+    G = empty(n, n)
+    call("ttb_ozaki_gram_rows", n, m, ptr(T), max(T.stride(0), 1), ptr(G), n, ptr(ws))
+    del ws
+    info = empty(1, dtype=I32)
+    call("ttb_potrf", n, ptr(G), n, ptr(info))   # col-major lower L: row-major view of the buffer = L^T
+    if int(info.item()) != 0:
+        return None
+    Lr = torch.triu(G).t().contiguous()
+    if offdiag:
+        return Lr, float(torch.tril(G, -1).abs().max())
+    return Lr
+
+
+def _trtri(Lr, n):
+    Li = empty(n, n)
+    ws = empty(n * n)
+    call("ttb_trtri_lower", n, ptr(Lr), n, ptr(Li), n, ptr(ws))
+    return Li
+
+
+def cholqr2_colmajor(Acm, m, n):
+    """Q R of a very tall col-major m x n matrix held as torch (n, m), by CholeskyQR2 with Ozaki-scheme
+    FP64 Gram matrices and products on the int8 tensor cores:
+        G1 = X^T X = L1 L1^T,  Q1 = X L1^-T,  G2 = Q1^T Q1 = L2 L2^T,  Q = Q1 L2^-T,  R = L2^T L1^T.
+    Q spans the same space as the Householder Q and differs from it only by column signs (R has a
+    positive diagonal) and rounding, so the orthogonalized TT represents the same tensor. CholeskyQR2
+    needs cond(X) well below eps^-1/2: the Cholesky factorizations must succeed and the second Gram
+    must be within 0.1 of I (else the first pass lost orthogonality beyond what one repeat restores);
+    returns (Qt, Rt) in qr_colmajor's layout, or None (the caller takes the Householder path).
+    Used for the rounding's right-to-left sweep (core.py _rl_orthogonalize)."""
+    if not (_CHOLQR2 and _OZAKI and m >= _CHOLQR2_MIN_M and n >= 256 and n % 128 == 0 and m % 64 == 0):
+        return None
+    L1 = _chol_rows(Acm, n, m)
+    if L1 is None:
+        return None
+    Q1 = gemm(_trtri(L1, n), Acm, emulate=True)          # (n, m) = L1^-1 X^T = Q1^T
+    got = _chol_rows(Q1, n, m, offdiag=True)
+    if got is None:
+        return None
+    L2, off = got
+    if off > 0.1 or float((L2.diagonal() - 1.0).abs().max()) > 0.1:
+        return None
+    Qt = gemm(_trtri(L2, n), Q1, emulate=True)           # Q^T
+    del Q1
+    return Qt, gemm(L1, L2)                              # R^T = L1 L2 (row-major) == col-major R
+
+
 _SIDE = None
 
 

@@ -373,14 +373,20 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False):
                 c0 = L.gemm(prev.reshape(a * m, r0), Rt)
                 return c0, L.SVDFactors(c0)
 
-            Qt, Rt, (c0, f0) = L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0,
-                                             overlap_r=first_svd)
-            f0.record_stream(torch.cuda.current_stream())
+            got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0)
+            if got is not None:
+                Qt, Rt = got
+                c0, f0 = first_svd(Rt)
+            else:
+                Qt, Rt, (c0, f0) = L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0,
+                                                 overlap_r=first_svd)
+                f0.record_stream(torch.cuda.current_stream())
             kk = Qt.shape[0]
             cores[k] = Qt.reshape(kk, n, r1)
             cores[0] = c0.reshape(a, m, kk)
             continue
-        Qt, Rt = L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
+        got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0)
+        Qt, Rt = got if got is not None else L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
         kk = Qt.shape[0]
         cores[k] = Qt.reshape(kk, n, r1)
         cores[k - 1] = L.gemm(cores[k - 1].reshape(a * m, r0), Rt, emulate=True).reshape(a, m, kk)

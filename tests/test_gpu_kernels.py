@@ -375,6 +375,51 @@ def test_svd_gram_path(monkeypatch, graded):
     assert float((Y - X).norm() / X.norm()) < 1e-13
 
 
+@pytest.mark.gpu
+def test_trtri_lower():
+    from paper_2509_13224_b200._lib import call, ptr
+    g = torch.Generator(device="cuda").manual_seed(2)
+    n = 384
+    Lr = torch.tril(torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64)) / n ** 0.5
+    Lr += 2.0 * torch.eye(n, device="cuda", dtype=torch.float64)
+    Lr_full = Lr + torch.triu(torch.full((n, n), 7.0, device="cuda", dtype=torch.float64), 1)  # ignored
+    Li = torch.empty(n, n, device="cuda", dtype=torch.float64)
+    ws = torch.empty(n * n, device="cuda", dtype=torch.float64)
+    call("ttb_trtri_lower", n, ptr(Lr_full), n, ptr(Li), n, ptr(ws))
+    eye = torch.eye(n, device="cuda", dtype=torch.float64)
+    assert float((Li @ Lr - eye).abs().max()) < 1e-13
+    assert float(torch.triu(Li, 1).abs().max()) == 0.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["gaussian", "graded", "illcond"])
+def test_cholqr2_colmajor(monkeypatch, kind):
+    """CholeskyQR2 with Ozaki Grams: Q orthonormal to 1e-14 and Q R = X whenever it returns a result.
+    Column scaling alone (graded) does not hurt it (Cholesky and the Ozaki Gram are both invariant to
+    it); a matrix whose column-scaled condition number is 1e12 (illcond) is refused."""
+    from paper_2509_13224_b200 import linalg as L
+    monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 65536)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    n, m = 256, 65536
+    Acm = torch.randn(n, m, generator=g, device="cuda", dtype=torch.float64)
+    if kind == "graded":
+        Acm *= torch.logspace(0, -10, n, device="cuda", dtype=torch.float64)[:, None]
+    if kind == "illcond":
+        V, _ = torch.linalg.qr(torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64))
+        W = torch.linalg.qr(Acm.t())[0]                   # m x n, orthonormal columns
+        Acm = ((V * torch.logspace(0, -12, n, device="cuda", dtype=torch.float64)[None, :]) @ W.t()).contiguous()
+    got = L.cholqr2_colmajor(Acm, m, n)
+    if kind == "illcond":
+        assert got is None
+        return
+    Qt, Rt = got
+    eye = torch.eye(n, device="cuda", dtype=torch.float64)
+    assert float((Qt @ Qt.t() - eye).abs().max()) < 1e-14
+    R = Rt.t()
+    assert float(torch.tril(R, -1).abs().max()) < 1e-12 * float(R.abs().max())
+    assert float((R.t() @ Qt - Acm).norm() / Acm.norm()) < 1e-14
+
+
 def test_round_with_emulated_gemms_matches_dmma(monkeypatch):
     """tt_round(tt_matvec) with the large products on the Ozaki path == the all-DMMA result."""
     from paper_2509_13224_b200 import linalg as L

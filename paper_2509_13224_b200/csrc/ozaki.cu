@@ -389,62 +389,105 @@ __global__ void oz_colexp_kernel(int cols, const unsigned long long* cmax, int* 
 // X = sum_s sigma_s 2^(48 - 8s), every sigma_s in [-128, 127] (each byte above 127 borrows from the next
 // digit up; the top digit stays within [-65, 65]), i.e. x = 2^ex sum_s sigma_s 2^(-6-8s) up to the single
 // rounding of X. Integer arithmetic: a floor cascade in floating point loses the remainder of tiny values.
-__device__ __forceinline__ void oz_digits(double x, int ex, uint8_t (&d)[OZ_S]) {
-  long long X = __double2ll_rn(ldexp(x, 54 - ex));
-  const long long lim = (1LL << 54) - 1;
-  X = X > lim ? lim : (X < -lim ? -lim : X);
-#pragma unroll
-  for (int s = OZ_S - 1; s >= 1; --s) {
-    const int r = (int)(int8_t)(uint8_t)(X & 0xFF);  // in [-128, 127], X - r divisible by 256
-    d[s] = (uint8_t)r;
-    X = (X - r) >> 8;
-  }
-  d[0] = (uint8_t)(int8_t)X;
+// sc = 2^(54 - ex) when that is a normal double (then x sc is exact, like ldexp), else 0 (use ldexp).
+__device__ __forceinline__ double oz_scale_of(int ex) {
+  const int p = 54 - ex;
+  return (p > -1023 && p < 1024) ? __longlong_as_double((long long)(p + 1023) << 52) : 0.0;
 }
 
-// row slices of a row-major (rows x K, ld) matrix into out[s][rows][K]; 16 consecutive k per thread
+// The digits of 4 values packed per plane: w[s] byte q = digit s of v[q]. With the bias
+// Y = X + 0x808080808080 the lower six balanced digits are the bytes of Y XOR 0x80 (sigma + 128 is the
+// plain base-256 digit of Y) and the top digit is byte 6 of Y (|sigma_0| <= 65), so digit s is byte
+// 6 - s of Z = Y ^ 0x808080808080; byte gathers by PRMT.
+__device__ __forceinline__ void oz_digits4(const double (&v)[4], int ex, double sc, uint32_t (&w)[OZ_S]) {
+  uint32_t lo[4], hi[4];
+  const long long lim = (1LL << 54) - 1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    long long X = __double2ll_rn(sc != 0.0 ? v[q] * sc : ldexp(v[q], 54 - ex));
+    X = X > lim ? lim : (X < -lim ? -lim : X);
+    const unsigned long long Z = (unsigned long long)(X + 0x808080808080LL) ^ 0x808080808080ULL;
+    lo[q] = (uint32_t)Z;
+    hi[q] = (uint32_t)(Z >> 32);
+  }
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) {
+    const int j = (6 - s) & 3;                 // byte within the 32-bit half
+    const uint32_t* src = (6 - s) >= 4 ? hi : lo;
+    const uint32_t sel = (uint32_t)j | ((uint32_t)(4 + j) << 4);
+    const uint32_t t01 = __byte_perm(src[0], src[1], sel), t23 = __byte_perm(src[2], src[3], sel);
+    w[s] = __byte_perm(t01, t23, 0x5410);
+  }
+}
+
+// row slices of a row-major (rows x K, ld) matrix into out[s][rows][K]: 4 consecutive k per thread
+// (two 16-byte loads when aligned; a warp reads 1 KB contiguous), one 32-bit store per slice plane
 __global__ void oz_slice_rows_kernel(int rows, int K, const double* __restrict__ X, long long ld,
                                      const int* __restrict__ e, uint8_t* out) {
-  const long long groups = (long long)rows * (K / 16);
+  const int kq = K / 4;
   const long long plane = (long long)rows * K;
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
-       g += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(g / (K / 16)), k0 = (int)(g % (K / 16)) * 16;
-    const int ex = e[r];
-    __align__(16) uint8_t dg[OZ_S][16];
+  const long long quads = (long long)rows * kq;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= quads) return;
+  int r = (int)(g / kq), k = (int)(g - (long long)r * kq);
+  const int dr = (int)(stride / kq), dk = (int)(stride - (long long)dr * kq);
+  const bool al = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)(ld * 8)) & 15) == 0;
+  for (; g < quads; g += stride) {
+    const double* x = X + (long long)r * ld + 4 * k;
+    double v[4];
+    if (al) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(x)), b = __ldg(reinterpret_cast<const double2*>(x) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      uint8_t d[OZ_S];
-      oz_digits(X[(long long)r * ld + k0 + q], ex, d);
-#pragma unroll
-      for (int s = 0; s < OZ_S; ++s) dg[s][q] = d[s];
+      for (int q = 0; q < 4; ++q) v[q] = __ldg(x + q);
     }
+    const int ex = e[r];
+    const double sc = oz_scale_of(ex);
+    uint32_t w[OZ_S];
+    oz_digits4(v, ex, sc, w);
+    uint8_t* o = out + (long long)r * K + 4 * k;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s)
-      *reinterpret_cast<uint4*>(out + s * plane + (long long)r * K + k0) = *reinterpret_cast<uint4*>(dg[s]);
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane) = w[s];
+    k += dk;
+    r += dr;
+    if (k >= kq) { k -= kq; ++r; }
   }
 }
 
-// column slices of a row-major (K x cols, ld) matrix, transposed: out[s][cols][K] (64 x 64 tiles)
-__global__ void oz_slice_cols_kernel(int K, int cols, const double* __restrict__ X, long long ld,
-                                     const int* __restrict__ e, uint8_t* out) {
-  __shared__ __align__(16) uint8_t t[OZ_S][64][64 + 16];
+// column slices of a row-major (K x cols, ld) matrix, transposed: out[s][cols][K]. 64 x 64 tiles: each
+// thread digitizes 4 consecutive k of one column (coalesced row reads across the warp) into one word
+// per plane, staged in shared memory [s][col][k/4] (17-word rows), then written as 64-byte K runs.
+__global__ void __launch_bounds__(256) oz_slice_cols_kernel(int K, int cols, const double* __restrict__ X, long long ld,
+                                                            const int* __restrict__ e, uint8_t* out) {
+  __shared__ uint32_t t[OZ_S][64][17];
   const int k0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
   const long long plane = (long long)cols * K;
-  for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
-    const int kk = idx / 64, cc = idx % 64;
-    const int k = k0 + kk, c = c0 + cc;
-    uint8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0};
-    if (k < K && c < cols) oz_digits(X[(long long)k * ld + c], e[c], d);
+  for (int it = threadIdx.x; it < 64 * 16; it += 256) {
+    const int cc = it & 63, kq = it >> 6;
+    const int c = c0 + cc;
+    uint32_t w[OZ_S];
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) t[s][cc][kk] = d[s];
+    for (int s = 0; s < OZ_S; ++s) w[s] = 0;
+    if (c < cols) {
+      const int ex = e[c];
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 4 * kq + q;
+        v[q] = k < K ? __ldg(X + (long long)k * ld + c) : 0.0;
+      }
+      oz_digits4(v, ex, oz_scale_of(ex), w);
+    }
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) t[s][cc][kq] = w[s];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < OZ_S * 64 * 4; idx += blockDim.x) {
-    const int s = idx / 256, cc = (idx / 4) % 64, part = idx % 4;
-    const int c = c0 + cc, k = k0 + part * 16;
-    if (c < cols && k < K)
-      *reinterpret_cast<uint4*>(out + s * plane + (long long)c * K + k) = *reinterpret_cast<const uint4*>(&t[s][cc][part * 16]);
+  for (int it = threadIdx.x; it < OZ_S * 64 * 16; it += 256) {
+    const int kq = it & 15, cc = (it >> 4) & 63, s = it >> 10;
+    const int c = c0 + cc, k = k0 + 4 * kq;
+    if (c < cols && k < K) *reinterpret_cast<uint32_t*>(out + s * plane + (long long)c * K + k) = t[s][cc][kq];
   }
 }
 

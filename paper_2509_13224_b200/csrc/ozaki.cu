@@ -547,6 +547,18 @@ long long oz_tiles(int M, int N, int sym) {
 // the persistent grid; the split count maximizes units / (SMs x rounds), ties to fewer splits
 void oz_split(long long tiles, int K, int* ks, int* kchunk) {
   const int nsm = oz_nsm();
+  static const int long_kc = [] {
+    const char* e = getenv("TTB_OZAKI_LONGK_CHUNK");
+    return e ? atoi(e) : 4 * OZ_SUB * OA_K;
+  }();
+  if (K > 2 * long_kc && long_kc > 0 && tiles * ((K + long_kc - 1) / long_kc) >= 2LL * nsm) {
+    // long K: 16384-deep ranges (4 TMEM accumulations), ordered range-major, so the CTAs running together all
+    // read the same few thousand columns of the slice stacks (L2-resident) instead of drifting apart
+    // over two halves of a multi-GB stack; costs ks partial tiles in HBM (reduced in a fixed order)
+    *kchunk = (long_kc + OA_K - 1) / OA_K * OA_K;
+    *ks = (K + *kchunk - 1) / *kchunk;
+    return;
+  }
   int best = 1;
   double best_eff = 0.0;
   const int kmax = K / 1024 > 1 ? K / 1024 : 1;

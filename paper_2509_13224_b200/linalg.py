@@ -245,6 +245,24 @@ def _trtri(Lr, n):
     return Li
 
 
+_CHOLQR1_KAPPA = float(os.environ.get("TTB_CHOLQR_ONEPASS_KAPPA", "4"))
+
+
+def _norm2_est(A, iters=24):
+    """||A||_2 of a square device matrix by power iteration on A^T A (seeded start; a lower estimate
+    that is within a few percent after 24 steps for the clustered spectra it is used on)."""
+    n = A.shape[0]
+    g = torch.Generator(device=A.device).manual_seed(12345)
+    v = torch.randn(n, 1, generator=g, device=A.device, dtype=A.dtype)
+    v /= v.norm()
+    nrm = 0.0
+    for _ in range(iters):
+        w = gemm(A, gemm(A, v), tA=True)                 # A^T A v
+        nrm = w.norm()
+        v = w / nrm
+    return float(nrm) ** 0.5
+
+
 def cholqr2_colmajor(Acm, m, n):
     """Q R of a very tall col-major m x n matrix held as torch (n, m), by CholeskyQR2 with Ozaki-scheme
     FP64 Gram matrices and products on the int8 tensor cores:
@@ -252,7 +270,9 @@ def cholqr2_colmajor(Acm, m, n):
     Q spans the same space as the Householder Q and differs from it only by column signs (R has a
     positive diagonal) and rounding, so the orthogonalized TT represents the same tensor. CholeskyQR2
     needs cond(X) well below eps^-1/2: the Cholesky factorizations must succeed and the second Gram
-    must be within 0.1 of I (else the first pass lost orthogonality beyond what one repeat restores);
+    must be within 0.1 of I (else the first pass lost orthogonality beyond what one repeat restores).
+    When the power-iteration estimate of cond(L1) is <= 4 (TTB_CHOLQR_ONEPASS_KAPPA) the first pass
+    is kept as is (orthogonality error ~ eps cond^2 <= 16 eps);
     returns (Qt, Rt) in qr_colmajor's layout, or None (the caller takes the Householder path).
     Used for the rounding's right-to-left sweep (core.py _rl_orthogonalize)."""
     if not (_CHOLQR2 and _OZAKI and m >= _CHOLQR2_MIN_M and n >= 256 and n % 128 == 0 and m % 64 == 0):
@@ -260,7 +280,11 @@ def cholqr2_colmajor(Acm, m, n):
     L1 = _chol_rows(Acm, n, m)
     if L1 is None:
         return None
-    Q1 = gemm(_trtri(L1, n), Acm, emulate=True)          # (n, m) = L1^-1 X^T = Q1^T
+    Li1 = _trtri(L1, n)
+    Q1 = gemm(Li1, Acm, emulate=True)                    # (n, m) = L1^-1 X^T = Q1^T
+    if _CHOLQR1_KAPPA > 0.0 and _norm2_est(L1) * _norm2_est(Li1) <= _CHOLQR1_KAPPA:
+        # cond(X) = cond(L1) <= 4: one CholeskyQR pass is already orthogonal to ~eps cond^2
+        return Q1, L1
     got = _chol_rows(Q1, n, m, offdiag=True)
     if got is None:
         return None

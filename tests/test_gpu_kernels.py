@@ -392,13 +392,15 @@ def test_trtri_lower():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind", ["gaussian", "graded", "illcond"])
+@pytest.mark.parametrize("kind", ["gaussian", "gaussian2", "graded", "illcond"])
 def test_cholqr2_colmajor(monkeypatch, kind):
     """CholeskyQR2 with Ozaki Grams: Q orthonormal to 1e-14 and Q R = X whenever it returns a result.
     Column scaling alone (graded) does not hurt it (Cholesky and the Ozaki Gram are both invariant to
     it); a matrix whose column-scaled condition number is 1e12 (illcond) is refused."""
     from paper_2509_13224_b200 import linalg as L
     monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 65536)
+    if kind == "gaussian2":   # force the second pass on a well-conditioned matrix too
+        monkeypatch.setattr(L, "_CHOLQR1_KAPPA", 0.0)
     g = torch.Generator(device="cuda").manual_seed(9)
     n, m = 256, 65536
     Acm = torch.randn(n, m, generator=g, device="cuda", dtype=torch.float64)

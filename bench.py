@@ -166,7 +166,7 @@ def roofline_record(kind, fl, ms, fp64_peak, traffic, g_fl, g_ms, oz_fl, oz_ms, 
                 bf16 = json.load(fh).get("bf16_tflops")
         peak = 2.0 * bf16 if bf16 else 4500.0
         achieved = float(OZ_PAIRS) * fp64_eq
-        rec.update(pipe=("INT8 tcgen05.mma kind::i8 (Ozaki-scheme FP64 emulation: 7+7 int8 slices, 8 levels = "
+        rec.update(pipe=("INT8 tcgen05.mma kind::i8 (Ozaki-scheme FP64 emulation: 7 balanced int8 slices per operand, 8 levels = "
                          "34 exact slice products)"),
                    kernel="oz_gemm_kernel (middle-core TT-matvec GEMM)",
                    timed="whole ttb_dgemm_ozaki calls (operand slicing + oz_gemm_kernel)", achieved=achieved, peak=peak, unit="TOPS",
@@ -306,7 +306,7 @@ def run_b200(args):
                        "round_eps": EPS, "output_ranks": out_ranks, "algorithmic_gflop_per_step": flops / 1e9,
                        "parallelism": f"replicas x{world}", "l2": "inputs 2.4 GB > 126 MB L2, no flush needed",
                        "fp64_gemm": ("products with M N K >= 2^33 as Ozaki-scheme FP64 on the tcgen05 INT8 tensor "
-                                     "cores (7+7 exact int8 slices, 55-bit operands, 8 int32 level sums = 34 slice "
+                                     "cores (7 balanced int8 slices of 54-bit operands, 8 exact int32 level sums = 34 slice "
                                      "products; ~1e-15 normwise vs DGEMM), the rest on DMMA" if L._OZAKI else "all products on DMMA")},
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
                     int(d2h), "ms_per_step": e2e_ms},

@@ -60,10 +60,10 @@ _OZAKI_CHECK = os.environ.get("TTB_OZAKI_CHECK", "0") == "1"   # debug: compare 
 def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False):
     """out = alpha op(A) op(B) + beta out (row-major, FP64 DMMA kernel).
 
-    emulate: large products (M N K >= 2^33, tcgen05-tileable, K <= 4096, alpha = 1, beta = 0, A not
-    transposed) run as the Ozaki-scheme FP64 GEMM on the INT8 tensor cores (ttb_dgemm_ozaki: 55-bit
-    operand slices, 8 exact int32 level sums; agrees with DGEMM to ~1e-15 normwise). TTB_OZAKI=0 keeps
-    every product on DMMA."""
+    emulate: large products (M N K >= 2^33, M % 128, N % 64, K % 64, alpha = 1, beta = 0, A not
+    transposed) run as the Ozaki-scheme FP64 GEMM on the INT8 tensor cores (ttb_dgemm_ozaki: 54-bit
+    operands in 7 balanced 8-bit slices, 8 exact int32 level sums; agrees with DGEMM to ~1e-15
+    normwise). TTB_OZAKI=0 keeps every product on DMMA."""
     A = _rows(A)
     B = _rows(B)
     M, K = (A.shape[1], A.shape[0]) if tA else (A.shape[0], A.shape[1])

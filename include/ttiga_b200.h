@@ -192,6 +192,10 @@ int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, 
  * CTAs (partials reduced in a fixed order). */
 int ttb_dgemm_ozaki_ex(void* stream, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                        const double* B, long long ldb, double beta, double* C, long long ldc, void* ws);
+/* C = A B with A (M x M) lower triangular (strict upper triangle zero): each 128-row block of C runs
+ * only the k steps below its diagonal block (half the work). B row-major M x N; ws as ttb_ozaki_workspace(M, N, M). */
+int ttb_dgemm_ozaki_trilA(void* stream, int M, int N, const double* A, long long lda, const double* B, long long ldb,
+                          double* C, long long ldc, void* ws);
 /* Gram matrix G (n x n) = X^T X of a row-major m x n X, FP64 via the Ozaki scheme (columns sliced once,
  * upper block triangle computed, mirrored); n % 128 == 0, m % 64 == 0 (else workspace 0 / TTB_EARG). */
 long long ttb_ozaki_gram_workspace(int m, int n); /* bytes */

@@ -129,6 +129,7 @@ struct OzOut {
   long long ldo, so;
   double alpha, beta;
   int mode;
+  int trilA;  // A lower triangular (M == K, one K range): row block m0 stops at k = m0 + 128
 };
 
 constexpr int OZ_SUB = 64;
@@ -190,7 +191,8 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int m0, n0;
         oz_tile(u % tiles, ntn, sym, m0, n0);
-        const int kt0 = (u / tiles) * (kchunk / OA_K), kt1 = min(K, (u / tiles + 1) * kchunk) / OA_K;
+        const int kt0 = (u / tiles) * (kchunk / OA_K);
+        const int kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K;
         for (int kt = kt0; kt < kt1; ++kt, ++it) {
           const int st = it % OA_ST;
           if (it >= OA_ST) mbar_wait(smem_u32(&empty[st]), ((it / OA_ST) - 1) & 1);
@@ -207,7 +209,10 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
     if (lane == 0) {  // MMA issuer
       int it = 0, g = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int kt0 = (u / tiles) * (kchunk / OA_K), kt1 = min(K, (u / tiles + 1) * kchunk) / OA_K;
+        int m0, n0;
+        oz_tile(u % tiles, ntn, sym, m0, n0);
+        const int kt0 = (u / tiles) * (kchunk / OA_K);
+        const int kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K;
         for (int ks = kt0; ks < kt1; ks += OZ_SUB, ++g) {
           if (g > 0) {  // the epilogue has the previous accumulation's level sums in registers
             mbar_wait(smem_u32(&tempty), (g - 1) & 1);
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
       oz_tile(u % tiles, ntn, sym, m0, n0);
       n0 += h * 32;
       const int kt0 = (u / tiles) * (kchunk / OA_K);
-      const int kt1 = LONGK ? min(K, (u / tiles + 1) * kchunk) / OA_K : 0;
+      const int kt1 = LONGK ? min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K : 0;
       const int my_ea = ea[m0 + q * 32 + lane];
       const int my_fb = fb[n0 + lane];  // column n0 + lane's exponent, broadcast per column below
       long long hi[32], lo[32];
@@ -635,7 +640,7 @@ __global__ void oz_mirror_kernel(int n, double* G, long long ldg) {
 
 // the int8 GEMM over prepared slices + split-K reduction (+ mirror for sym)
 int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, double beta, double* C, long long ldc,
-           int sym) {
+           int sym, int trilA = 0) {
   CUtensorMap ta, tb;
   if (!oz_tmap(&ta, w.As, M, K, OZ_M, OA_K) || !oz_tmap(&tb, w.Bs, N, K, OA_N, OA_K)) return TTB_EARG;
   const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
@@ -655,9 +660,9 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   oz_split(tiles, K, &ks, &kc);
   OzOut o;
   if (ks > 1)
-    o = OzOut{w.part, N, (long long)M * N, 1.0, 0.0, 1};
+    o = OzOut{w.part, N, (long long)M * N, 1.0, 0.0, 1, 0};
   else
-    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2};
+    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2, trilA && M == K ? 1 : 0};
   const long long units = tiles * ks;
   const int grid = units < oz_nsm() ? (int)units : oz_nsm();
   if (kc > OZ_SUB * OA_K)
@@ -715,6 +720,19 @@ TTB_API int ttb_ozaki_applies(int M, int N, int K) { return oz_shape_ok(M, N, K)
 TTB_API int ttb_dgemm_ozaki(void* stream, int tB, int M, int N, int K, const double* A, long long lda,
                             const double* B, long long ldb, double* C, long long ldc, void* ws) {
   return ozaki_gemm(as_stream(stream), tB, M, N, K, 1.0, A, lda, B, ldb, 0.0, C, ldc, ws);
+}
+
+// C = A B with A (M x M, lda) lower triangular (its strict upper triangle must be zero): row block
+// m0 of C only runs the k steps below m0 + 128 (half the work of a square product; Q = X R^-1 of
+// the CholeskyQR passes). B: row-major M x N (ldb). ws: ttb_ozaki_workspace(M, N, M) bytes.
+TTB_API int ttb_dgemm_ozaki_trilA(void* stream, int M, int N, const double* A, long long lda, const double* B,
+                                  long long ldb, double* C, long long ldc, void* ws) {
+  if (!oz_shape_ok(M, N, M)) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  OzWs w = oz_ws_layout(ws, M, N, M, 0);
+  oz_rows(st, M, M, A, lda, w.ea, w.amax, w.As);
+  oz_cols(st, M, N, B, ldb, w.fb, w.bmax, w.Bs);
+  return oz_run(st, w, M, N, M, 1.0, 0.0, C, ldc, 0, 1);
 }
 
 // General form: C = alpha A op(B) + beta C.

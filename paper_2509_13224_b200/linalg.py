@@ -263,6 +263,14 @@ def _norm2_est(A, iters=24):
     return float(nrm) ** 0.5
 
 
+def _trmm_oz(Li, X, n, m):
+    """Li (n x n lower) @ X (n x m) as the Ozaki GEMM that skips the zero upper triangle."""
+    out = empty(n, m)
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", n, m, n)), dtype=torch.uint8, device=device())
+    call("ttb_dgemm_ozaki_trilA", n, m, ptr(Li), n, ptr(X), max(X.stride(0), 1), ptr(out), m, ptr(ws))
+    return out
+
+
 def cholqr2_colmajor(Acm, m, n):
     """Q R of a very tall col-major m x n matrix held as torch (n, m), by CholeskyQR2 with Ozaki-scheme
     FP64 Gram matrices and products on the int8 tensor cores:
@@ -281,7 +289,7 @@ def cholqr2_colmajor(Acm, m, n):
     if L1 is None:
         return None
     Li1 = _trtri(L1, n)
-    Q1 = gemm(Li1, Acm, emulate=True)                    # (n, m) = L1^-1 X^T = Q1^T
+    Q1 = _trmm_oz(Li1, Acm, n, m)                        # (n, m) = L1^-1 X^T = Q1^T
     if _CHOLQR1_KAPPA > 0.0 and _norm2_est(L1) * _norm2_est(Li1) <= _CHOLQR1_KAPPA:
         # cond(X) = cond(L1) <= 4: one CholeskyQR pass is already orthogonal to ~eps cond^2
         return Q1, L1
@@ -291,7 +299,7 @@ def cholqr2_colmajor(Acm, m, n):
     L2, off = got
     if off > 0.1 or float((L2.diagonal() - 1.0).abs().max()) > 0.1:
         return None
-    Qt = gemm(_trtri(L2, n), Q1, emulate=True)           # Q^T
+    Qt = _trmm_oz(_trtri(L2, n), Q1, n, m)               # Q^T
     del Q1
     return Qt, gemm(L1, L2)                              # R^T = L1 L2 (row-major) == col-major R
 

@@ -376,6 +376,26 @@ def test_svd_gram_path(monkeypatch, graded):
 
 
 @pytest.mark.gpu
+def test_dgemm_ozaki_trilA():
+    """Lower-triangular A: the k steps above each row block's diagonal are skipped, result == full product."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(4)
+    M, N = 384, 4096
+    A = torch.tril(torch.randn(M, M, generator=g, device="cuda", dtype=torch.float64))
+    B = torch.randn(M, N, generator=g, device="cuda", dtype=torch.float64)
+    C = torch.empty(M, N, device="cuda", dtype=torch.float64)
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, M)), dtype=torch.uint8, device="cuda")
+    call("ttb_dgemm_ozaki_trilA", M, N, ptr(A), M, ptr(B), N, ptr(C), N, ptr(ws))
+    Cd = L.gemm(A, B)
+    # the Ozaki error model: operands are rounded relative to their row / column maxima (the same
+    # 54-bit slicing as the dense product), so the bound scales with K max_k|a_ik| max_k|b_kj|
+    scale = M * A.abs().max(1).values[:, None] * B.abs().max(0).values[None, :]
+    assert float(((C - Cd).abs() / scale).max()) < 2 ** -52
+    assert float((C - Cd).norm() / Cd.norm()) < 1e-14
+
+
+@pytest.mark.gpu
 def test_trtri_lower():
     from paper_2509_13224_b200._lib import call, ptr
     g = torch.Generator(device="cuda").manual_seed(2)

@@ -33,7 +33,7 @@ METRIC = "TT matvec+round GFLOP/s (FP64)"
 WORKLOAD = ("configs[4] kernel microbenchmark: 3-core TT-matrix, 1024x1024 modes, operator ranks 16, "
             "cores N(0,1)/sqrt(rank) (seed 0+rank), applied to a TT-vector with ranks 64, rounded to 1e-8")
 N_MODE, R_OP, R_VEC, EPS = 1024, 16, 64, 1e-8
-CPU_SAMPLE_N = 128  # bounded CPU sample: same ranks, mode size 128
+CPU_SAMPLE_N = 256  # bounded CPU sample in the device arm: same ranks, mode size 256 (~10 s)
 
 
 def parse():
@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-solve", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-dmma", action="store_true", help="skip the all-DMMA comparison steps")
     ap.add_argument("--solve-configs", default="1,2,3,4",
                     help="BASELINE solve configs timed at full size after the microbenchmark (comma list)")
     ap.add_argument("--n", type=int, default=N_MODE)
@@ -103,7 +104,7 @@ class ClockSampler:
 
 
 def cpu_sample_run(n=CPU_SAMPLE_N, seed=0):
-    """Oracle (numpy, all host threads) matvec+round on the bounded sample; returns (seconds, flops)."""
+    """Oracle (numpy, all host threads) matvec+round on one instance; returns (seconds, flops, ranks)."""
     from oracle import tt as OT
     from paper_2509_13224_b200.workloads import matvec_round_flops, matvec_round_instance_np
     A, X = matvec_round_instance_np(n, R_OP, R_VEC, 3, seed)
@@ -117,29 +118,45 @@ def cpu_sample_run(n=CPU_SAMPLE_N, seed=0):
     return dt, fl, Y.ranks
 
 
+def _host_mem_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 1e9
+    except Exception:
+        return None
+
+
+REF_FULL_MEM_GB = 64.0   # host memory the oracle needs at n = 1024 (8.6 GB cores, LAPACK copies)
+
+
 def run_reference(args):
+    """Reference arm: the reference algorithm (oracle port of tensor_train/core.py:327-389, numpy/LAPACK
+    on every host thread) on the SAME workload as the device arm (mode size 1024). One full step takes
+    minutes on the host, so this arm times ONE step (no warm-up) whatever --steps/--warmup say, and says
+    so in its line; with too little host memory it falls back to mode size 512 and says that instead."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     ncores = os.cpu_count()
-    for _ in range(args.warmup):
-        cpu_sample_run()
-    times, fl = [], None
-    for _ in range(args.steps):
-        dt, fl, ranks = cpu_sample_run()
-        times.append(dt)
-    v = fl / (sum(times) / len(times)) / 1e9
+    n = args.n
+    mem = _host_mem_gb()
+    if n == N_MODE and mem is not None and mem < REF_FULL_MEM_GB:
+        n = N_MODE // 2
+    dt, fl, ranks = cpu_sample_run(n)
+    v = fl / dt / 1e9
+    sample = (f"oracle (numpy/LAPACK restatement of the reference tt_matvec + tt_round, all {ncores} host threads) on "
+              f"the workload at mode size {n} (ranks 16/64), ONE timed step (a step takes {dt:.0f} s on the host; "
+              f"--steps {args.steps} --warmup {args.warmup} not honoured)")
+    if n != args.n:
+        sample += f"; host memory {mem:.0f} GB < {REF_FULL_MEM_GB:.0f} GB needed at mode size {args.n}"
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": 1,
+        "warmup": 0, "steps_requested": args.steps, "ms_per_step": 1e3 * dt, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "mode_size": N_MODE, "op_ranks": R_OP, "vec_ranks": R_VEC, "round_eps": EPS,
-                   "sample_mode_size": CPU_SAMPLE_N, "parallelism": "replicas x1 (rank 0 only)",
-                   "l2": "inputs > L2"},
-        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": ncores, "kind": "port",
-                         "sample": f"oracle (numpy/LAPACK restatement of the reference tt_matvec + tt_round) on the "
-                                   f"same workload at mode size {CPU_SAMPLE_N} (ranks 16/64 kept), one matvec+round "
-                                   f"per step"},
+        "config": {"workload": WORKLOAD, "mode_size": n, "op_ranks": R_OP, "vec_ranks": R_VEC, "round_eps": EPS,
+                   "output_ranks": list(ranks), "algorithmic_gflop_per_step": fl / 1e9,
+                   "parallelism": "replicas x1 (rank 0 only)", "l2": "inputs > L2"},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": ncores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -149,35 +166,67 @@ def run_reference(args):
 OZ_PAIRS = 34  # slice products per emulated FP64 product (levels 0..7 of 7x7 slices)
 
 
-def roofline_record(kind, fl, ms, fp64_peak, traffic, g_fl, g_ms, oz_fl, oz_ms, n_gemm, steps, ms_step):
-    """Roofline of the dominant kernel. Ozaki-emulated FP64 GEMMs (34 exact int8 slice products per
-    FP64 product) are bounded by the tcgen05 INT8 pipe: achieved int8 TOPS against 2x the measured
-    dense bf16 peak (int8 issues at twice the bf16 rate); the FP64-equivalent rate is reported beside it."""
+def _peaks():
+    pf = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pf):
+        with open(pf) as fh:
+            d = json.load(fh)
+        return d.get("bf16_tflops"), d.get("bf16_tflops_sustained")
+    return None, None
+
+
+def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step):
+    """Roofline of the dominant kernel class: the GEMM shape (kind, M, N, K) with the largest share of
+    the timed region. Ozaki-emulated FP64 GEMMs (34 exact int8 slice products per FP64 product) are
+    bounded by the tcgen05 INT8 pipe: achieved int8 TOPS against 2x the measured dense bf16 peak (int8
+    issues at twice the bf16 rate) -- the SUSTAINED figure, since the kernel runs inside a long step
+    (the burst-peak fraction is reported beside it); the FP64-equivalent rate is reported too."""
+    kind, shape = cls
+    recs = [r for r in prof if (r[3], r[4]) == cls]
+    ms = sum(a.elapsed_time(b) for a, b, _, _, _ in recs)
+    fl = sum(r[2] for r in recs)
     fp64_eq = fl / (ms / 1e3) / 1e12
+    g_ms = sum(a.elapsed_time(b) for a, b, _, _, _ in prof)
+    g_fl = sum(r[2] for r in prof)
+    oz = [r for r in prof if r[3] == "ozaki"]
+    oz_ms = sum(a.elapsed_time(b) for a, b, _, _, _ in oz)
+    oz_fl = sum(r[2] for r in oz)
+    M, N, K = shape
     rec = {"bound": "tensor", "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+           "launches_per_step": len(recs) / steps, "share_of_step": ms / steps / ms_step,
            "all_gemms": {"fp64_equivalent_tflops": g_fl / (g_ms / 1e3) / 1e12 if g_ms else None,
-                         "share_of_step": g_ms / steps / ms_step, "launches": n_gemm,
+                         "share_of_step": g_ms / steps / ms_step, "launches_per_step": len(prof) / steps,
+                         "executed_gflop_per_step": g_fl / steps / 1e9,
                          "ozaki_fp64_equivalent_tflops": oz_fl / (oz_ms / 1e3) / 1e12 if oz_ms else None}}
     if kind == "ozaki":
-        bf16 = None
-        pf = os.path.join(ROOT, "MEASURED_PEAKS.json")
-        if os.path.exists(pf):
-            with open(pf) as fh:
-                bf16 = json.load(fh).get("bf16_tflops")
-        peak = 2.0 * bf16 if bf16 else 4500.0
+        burst, sus = _peaks()
+        peak = 2.0 * sus if sus else (2.0 * burst if burst else 4500.0)
         achieved = float(OZ_PAIRS) * fp64_eq
-        rec.update(pipe=("INT8 tcgen05.mma kind::i8 (Ozaki-scheme FP64 emulation: 7 balanced int8 slices per operand, 8 levels = "
-                         "34 exact slice products)"),
-                   kernel="oz_gemm_kernel (middle-core TT-matvec GEMM)",
-                   timed="whole ttb_dgemm_ozaki calls (operand slicing + oz_gemm_kernel)", achieved=achieved, peak=peak, unit="TOPS",
-                   frac=achieved / peak, fp64_equivalent_tflops=fp64_eq, fp64_dmma_peak_tflops=fp64_peak,
-                   peak_source=("2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16 rate)" if bf16
+        rec.update(pipe=("INT8 tcgen05.mma kind::i8 (Ozaki-scheme FP64 emulation: 7 balanced int8 slices per operand, "
+                         "8 levels = 34 exact slice products)"),
+                   kernel=(f"oz_gemm_kernel, C({M}x{N}) = A({M}x{K}) B({K}x{N}): the matvec, right-to-left carry, "
+                           f"S Vt carry and implicit-U products of the step (all this shape)"),
+                   timed="whole ttb_dgemm_ozaki calls (operand slicing + oz_gemm_kernel), CUDA events on the launching stream",
+                   achieved=achieved, peak=peak, unit="TOPS", frac=achieved / peak,
+                   frac_of_burst_peak=(achieved / (2.0 * burst)) if burst else None,
+                   fp64_equivalent_tflops=fp64_eq, fp64_dmma_peak_tflops=fp64_peak,
+                   algorithmic_unit="2 M N K FP64-equivalent flop per launch x 34 int8 slice products",
+                   peak_source=("2 x MEASURED_PEAKS.json bf16_tflops_sustained (dense int8 = 2x bf16 rate)" if sus
+                                else "2 x MEASURED_PEAKS.json bf16_tflops" if burst
                                 else "nominal B200 dense int8 4.5 POPS (MEASURED_PEAKS.json absent)"))
     else:
-        rec.update(pipe="FP64 DMMA (mma.sync m8n8k4 f64)", kernel="dgemm_kernel (middle-core TT-matvec GEMM)",
+        rec.update(pipe="FP64 DMMA (mma.sync m8n8k4 f64)", kernel=f"dgemm_kernel, C({M}x{N}) = A({M}x{K}) B({K}x{N})",
                    achieved=fp64_eq, peak=fp64_peak, unit="TFLOP/s", frac=fp64_eq / fp64_peak,
+                   algorithmic_unit="2 M N K flop per launch",
                    peak_source="cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)")
     return rec
+
+
+def dominant_class(prof):
+    tot = {}
+    for a, b, _, kind, shape in prof:
+        tot[(kind, shape)] = tot.get((kind, shape), 0.0) + a.elapsed_time(b)
+    return max(tot, key=tot.get) if tot else ("dmma", (0, 0, 0))
 
 
 def run_b200(args):
@@ -236,17 +285,10 @@ def run_b200(args):
     ms_all = max_over_ranks(ms, device="cuda")
     value = whole_job_rate(flops, ms_all, world) / 1e9
 
-    # roofline of the dominant kernel (the middle-core TT-matvec GEMM: Ozaki-emulated FP64 on the INT8
-    # tensor cores, or the DMMA GEMM with TTB_OZAKI=0): algorithmic flops / event-timed duration
-    g_ms = sum(a.elapsed_time(b) for a, b, _, _ in prof)
-    g_fl = sum(f for _, _, f, _ in prof)
-    big = sorted(prof, key=lambda r: -r[2])[: args.steps]
-    big_ms = sum(a.elapsed_time(b) for a, b, _, _ in big)
-    big_fl = sum(f for _, _, f, _ in big)
-    big_kind = big[0][3] if big else "dmma"
-    oz = [r for r in prof if r[3] == "ozaki"]
-    oz_ms = sum(a.elapsed_time(b) for a, b, _, _ in oz)
-    oz_fl = sum(f for _, _, f, _ in oz)
+    # roofline of the dominant kernel class (largest share of the timed region): algorithmic flops /
+    # CUDA-event duration of every launch of that GEMM shape
+    cls = dominant_class(prof)
+    prof_all = prof
 
     # measured FP64 peak on this box: cuBLAS DGEMM 8192^3 (best of 5) -- the roofline denominator
     a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
@@ -290,12 +332,35 @@ def run_b200(args):
     del hA, hX, hY
 
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "r1_dominant_kernel_ozaki.json" if big_kind == "ozaki"
+    tf = os.path.join(ROOT, "profiles", "r2_dominant_kernel_ozaki.json" if cls[0] == "ozaki"
                       else "r1_dominant_kernel.json")
     if os.path.exists(tf):
         with open(tf) as fh:
             d = json.load(fh)
-        traffic = d["dram_bytes_read"] + d["dram_bytes_write"]
+        if tuple(d.get("shape", cls[1])) == tuple(cls[1]):
+            traffic = d["dram_bytes_read"] + d["dram_bytes_write"]
+
+    # ---------------- the same step with every product on DMMA and Householder factorizations
+    # (TTB_OZAKI=0 path), for comparison: what the Ozaki / CholeskyQR2 / Gram routes buy
+    dmma_ms = None
+    if not args.skip_dmma:
+        L._OZAKI = False
+        try:
+            step()
+            torch.cuda.synchronize()
+            d0 = torch.cuda.Event(enable_timing=True)
+            d1 = torch.cuda.Event(enable_timing=True)
+            ns = max(1, min(args.steps, 3))
+            d0.record(st)
+            for _ in range(ns):
+                Y = step()
+            d1.record(st)
+            torch.cuda.synchronize()
+            dmma_ms = d0.elapsed_time(d1) / ns
+        finally:
+            L._OZAKI = True
+        del Y
+
     line = None
     if rank == 0:
         line = {
@@ -310,8 +375,9 @@ def run_b200(args):
                                      "products; ~1e-15 normwise vs DGEMM), the rest on DMMA" if L._OZAKI else "all products on DMMA")},
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
                     int(d2h), "ms_per_step": e2e_ms},
-            "roofline": roofline_record(big_kind, big_fl, big_ms, fp64_peak, traffic, g_fl, g_ms, oz_fl, oz_ms,
-                                        len(prof), args.steps, ms_all),
+            "roofline": roofline_record(cls, fp64_peak, traffic, prof_all, args.steps, ms_all),
+            "executed_gemm_gflop_per_step": sum(r[2] for r in prof_all) / args.steps / 1e9,
+            "all_dmma_ms_per_step": dmma_ms,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
@@ -347,7 +413,9 @@ def run_b200(args):
         for c in [int(x) for x in args.solve_configs.split(",") if x.strip()]:
             if c == 1:
                 continue
-            want_err = c == 2
+            want_err = SOLVE_CONFIGS[c].get("analytic") is not None   # manufactured solution exists
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats()
             rep = D.solve_poisson(D.SolveConfig(seed=0, **SOLVE_CONFIGS[c]), want_error=want_err)
             torch.cuda.synchronize()
             tm = rep.timings
@@ -361,7 +429,17 @@ def run_b200(args):
         dt, fl, _ = cpu_sample_run()
         line["cpu_baseline"] = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
                                 "sample": f"oracle numpy restatement of tt_matvec + tt_round, mode size "
-                                          f"{CPU_SAMPLE_N} (ranks 16/64 kept), one step"}
+                                          f"{CPU_SAMPLE_N} (ranks 16/64 kept), one step ({dt:.1f} s)"}
+        # the same-config (mode size 1024) host timing: one step takes minutes, so it is measured by the
+        # reference arm (bench.py --impl reference) and recorded under profiles/, not re-run here
+        pf = os.path.join(ROOT, "profiles", "r2_reference_arm_n1024.json")
+        if os.path.exists(pf):
+            with open(pf) as fh:
+                ref = json.load(fh)
+            line["cpu_baseline"]["same_config_oneoff"] = {
+                "value": ref["value"], "unit": ref["unit"], "ms_per_step": ref["ms_per_step"],
+                "mode_size": ref["config"]["mode_size"], "cores": ref["cpu_baseline"]["cores"],
+                "source": "profiles/r2_reference_arm_n1024.json (bench.py --impl reference on a GPU box host)"}
         if not args.skip_solve:
             from oracle import iga as OI
             from paper_2509_13224_b200.workloads import SOLVE_CONFIGS

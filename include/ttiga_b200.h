@@ -28,8 +28,8 @@ long long ttb_launch_count(int reset);
 /* ---- dense FP64 building blocks ------------------------------------------------------------ */
 
 /* C[b] = alpha * op(A[b]) op(B[b]) + beta * C[b], row-major, strided batch.
- * Replaces the np.einsum / np.tensordot contractions of tensor_train/core.py:346,381,419,434
- * and tensor_train/amen.py:105-122,146-191. DMMA (mma.sync m8n8k4 f64) tiles, split-K when the
+ * Replaces the np.einsum / np.tensordot contractions of tensor_train/core.py:300,335,373,388
+ * and tensor_train/amen.py:106-123,147-150,152-156. DMMA (mma.sync m8n8k4 f64) tiles, split-K when the
  * output is too small to fill the 148 SMs. */
 int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
               long long sA, const double* B, long long ldb, long long sB, double beta, double* C, long long ldc,
@@ -42,8 +42,8 @@ int ttb_permute(void* stream, int nd, const long long* in_dims, const int* perm,
 int ttb_dot(void* stream, long long n, const double* x, const double* y, double* out, double* part, int take_sqrt);
 
 /* ---- Householder QR / SVD / solvers (np.linalg.qr, np.linalg.svd, np.linalg.solve,
- *      scipy.linalg.cho_factor/cho_solve as used by tensor_train/core.py:362,417,430,
- *      tensor_train/cross.py:170,188,190, tensor_train/amen.py:390-391, assembly.py:412-413) -- */
+ *      scipy.linalg.cho_factor/cho_solve as used by tensor_train/core.py:316,371,384,
+ *      tensor_train/cross.py:170,188,190, tensor_train/amen.py:168-171, assembly.py:412-413) -- */
 
 long long ttb_qr_workspace(int m, int n); /* doubles */
 /* In-place blocked Householder QR of col-major A (m x n, lda); tau: min(m,n). */
@@ -82,7 +82,7 @@ long long ttb_maxvol_workspace(int n, int r); /* doubles */
 int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, int max_iters, int* rows_out, double* ws,
                int* iws);
 
-/* ---- IGA kernels (splines.py:170-245, geometry.py:150-261, assembly.py:208-233, driver.py:388-422) */
+/* ---- IGA kernels (splines.py:146-221, geometry.py:150-261, assembly.py:208-233, driver.py:388-422) */
 
 /* Nonzero basis values/derivatives at nq parameters (Cox-de Boor; NURBS when weights != NULL).
  * first: int[nq]; V, D: nq x (p+1). bad: device int, min'ed with the first out-of-range index. */
@@ -118,7 +118,7 @@ int ttb_l1_error(void* stream, const int* f0, const int* f1, const int* f2, cons
                  const double* U1, int r2, const double* U2, const double* w0, const double* w1, const double* w2,
                  int exact_id, const double* prm, double* part, double* out);
 
-/* ---- TT operator kernels (tensor_train/core.py:373-384, tensor_train/amen.py:76-191) ----------- */
+/* ---- TT operator kernels (tensor_train/core.py:327-338, tensor_train/amen.py:51-193) ----------- */
 
 /* TT-matvec of a banded operator core M (Ra, n, 2h+1, Rb) with a vector core X (rc, n, rd):
  * Y[(a,c), i, (b,d)] = sum_t M[a,i,t,b] X[c, i+t-h, d]. */
@@ -136,10 +136,10 @@ int ttb_local_band_build(void* stream, int r0, int n, int r1, int h, int Rb, con
                          double* LB);
 /* In-place banded Cholesky + solve (one CTA); *info > 0 on a non-positive pivot (caller falls back to LU). */
 int ttb_band_chol_solve(void* stream, long long N, int bw, double* LB, double* b, int* info);
-/* Jacobi diagonal of the local operator, floored at 1e-14 max|d| (amen.py:380-403). part: >= 297 doubles. */
+/* Jacobi diagonal of the local operator, floored at 1e-14 max|d| (amen.py:158-161,179-181). part: >= 297 doubles. */
 int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
                     const double* phiR, double* d, double* part);
-/* Entries of a 3-core TT at N multi-indices (TtTensor.gather, core.py:164-170). */
+/* Entries of a 3-core TT at N multi-indices (TtTensor.gather, core.py:118-124). */
 /* d = max(|d|, 1e-14 max|d|) elementwise (Jacobi preconditioner floor, amen.py:179-181); part >= 320 doubles. */
 int ttb_abs_floor(void* stream, long long tot, double* d, double* part);
 int ttb_tt_gather3(void* stream, int N, const long long* idx, const double* G0, int n0, int r1, const double* G1,

@@ -12,14 +12,14 @@ import numpy as np
 
 
 class SplineFault(ValueError):
-    """Mirror of reference ``SplineError`` (splines.py:61)."""
+    """Mirror of reference ``SplineError`` (splines.py:37)."""
 
 
 class Spline1D:
     """Clamped knot vector + degree (+ weights for NURBS).
 
-    Validation mirrors reference KnotVector.__post_init__ (splines.py:76-92)
-    and Basis1D.__post_init__ (splines.py:132-139).
+    Validation mirrors reference KnotVector.__post_init__ (splines.py:52-68)
+    and Basis1D.__post_init__ (splines.py:108-115).
     """
 
     def __init__(self, knots, degree, weights=None):
@@ -51,25 +51,25 @@ class Spline1D:
 
     @staticmethod
     def uniform(p, spans):
-        """Open uniform knots on [0,1] (reference splines.py:116-122)."""
+        """Open uniform knots on [0,1] (reference splines.py:92-98)."""
         if spans < 1:
             raise SplineFault("need a span")
         mids = np.linspace(0.0, 1.0, spans + 1)[1:-1]
         return Spline1D(np.r_[np.zeros(p + 1), mids, np.ones(p + 1)], p)
 
     def nonempty_spans(self):
-        """Reference KnotVector.spans (splines.py:110-113)."""
+        """Reference KnotVector.spans (splines.py:86-89)."""
         return np.flatnonzero(self.t[1:] > self.t[:-1])
 
     def greville(self):
-        """Knot averages (reference splines.py:308-315)."""
+        """Knot averages (reference splines.py:284-291)."""
         if self.p == 0:
             return 0.5 * (self.t[:-1] + self.t[1:])
         return np.array([self.t[i + 1: i + self.p + 1].mean() for i in range(self.n)])
 
 
 def span_index(sp: Spline1D, x: float) -> int:
-    """Reference find_span (splines.py:170-185) incl. right-end clamp."""
+    """Reference find_span (splines.py:146-161) incl. right-end clamp."""
     t = sp.t
     if x < t[0] or x > t[-1]:
         raise SplineFault(f"{x} outside [{t[0]}, {t[-1]}]")
@@ -84,7 +84,7 @@ def span_index(sp: Spline1D, x: float) -> int:
 def _poly_window(t, p, k, x):
     """Nonzero degree-p values and derivatives on span k.
 
-    Restates reference _bspline_values_derivs (splines.py:188-226): the
+    Restates reference _bspline_values_derivs (splines.py:164-202): the
     triangular Cox-de Boor table with the 0/0 := 0 convention; derivatives
     from the saved degree-(p-1) row.
     """
@@ -122,7 +122,7 @@ def _poly_window(t, p, k, x):
 
 
 def basis_window(sp: Spline1D, x: float):
-    """(first_index, values, derivs) at x (reference eval_basis, splines.py:229-245)."""
+    """(first_index, values, derivs) at x (reference eval_basis, splines.py:205-221)."""
     k = span_index(sp, x)
     v, d = _poly_window(sp.t, sp.p, k, x)
     if sp.w is not None:
@@ -134,7 +134,7 @@ def basis_window(sp: Spline1D, x: float):
 
 
 def dense_tables(sp: Spline1D, xs):
-    """Dense (len(xs), n) value/derivative tables (reference tabulate, splines.py:318-334)."""
+    """Dense (len(xs), n) value/derivative tables (reference tabulate, splines.py:294-310)."""
     xs = np.atleast_1d(np.asarray(xs, dtype=float))
     V = np.zeros((xs.size, sp.n))
     D = np.zeros((xs.size, sp.n))
@@ -148,7 +148,7 @@ def dense_tables(sp: Spline1D, xs):
 def knot_insert(sp: Spline1D, ctrl, x):
     """Boehm insertion; rational bases in homogeneous coordinates.
 
-    Restates reference insert_knot (splines.py:248-291).
+    Restates reference insert_knot (splines.py:224-267).
     """
     t, p = sp.t, sp.p
     if not (t[0] < x < t[-1]):
@@ -176,7 +176,7 @@ def knot_insert(sp: Spline1D, ctrl, x):
 
 
 def bisect_refine(sp: Spline1D, ctrl, levels: int):
-    """Reference h_refine_uniform (splines.py:294-305)."""
+    """Reference h_refine_uniform (splines.py:270-281)."""
     if levels < 0:
         raise SplineFault("levels < 0")
     for _ in range(levels):

@@ -11,7 +11,8 @@
 // column by column so every pivot is 1 + |w| >= 1, gives the unit-lower reflector block V = L,
 // T = U L_top^{-T}, tau = diag(T) and R_h = S R, i.e. exactly what dgeqrf + dlarft produce (up
 // to roundoff). CholeskyQR2 needs cond(P) well below eps^{-1/2}; the Cholesky pivots are checked
-// (min/max diagonal of R1, R2 >= 1e-5) and the caller falls back to the TSQR panels otherwise.
+// (min/max diagonal of R1, R2 >= 1e-5; the second Gram Q1^T Q1 within 0.1 of I entrywise) and the
+// caller falls back to the TSQR panels otherwise.
 #include "common.cuh"
 
 TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
@@ -34,9 +35,20 @@ __global__ void __launch_bounds__(CQT) chol_inv_kernel(int b, const double* __re
   __shared__ int bad;
   const int ld = b + 1;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < b * b; e += CQT) W[(e / b) * ld + e % b] = G[e];
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
+  for (int e = threadIdx.x; e < b * b; e += CQT) {
+    const double g = G[e];
+    W[(e / b) * ld + e % b] = g;
+    // the second pass (bit 2) factors Q1^T Q1: accepted only within 0.1 of I entrywise (the rule of
+    // linalg.cholqr2_colmajor); a min/max pivot ratio alone does not bound how far Q1 is from orthogonal
+    if (bit == 2 && !(fabs(g - (e / b == e % b ? 1.0 : 0.0)) <= 0.1)) bad = 1;
+  }
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) atomicOr(flag, bit);
+    return;
+  }
   for (int k = 0; k < b; ++k) {
     const double piv = W[k * ld + k];
     if (!(piv > 0.0) || !isfinite(piv)) {

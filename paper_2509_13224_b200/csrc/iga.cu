@@ -10,7 +10,7 @@ namespace {
 constexpr int PMAX = 8;
 
 // ---------------------------------------------------------------------------
-// Cox-de Boor (NURBS Book A2.2/A2.3) for one parameter; reference splines.py:170-245.
+// Cox-de Boor (NURBS Book A2.2/A2.3) for one parameter; reference splines.py:146-221.
 __global__ void basis_kernel(int nq, const double* __restrict__ x, const double* __restrict__ t, int nk, int p,
                              const double* __restrict__ w, int* first, double* V, double* D, int* bad) {
   int q = blockIdx.x * blockDim.x + threadIdx.x;

@@ -24,6 +24,7 @@ namespace {
 
 constexpr int OZ_S = 7;                  // slices per operand
 constexpr int OZ_M = 128;
+constexpr int OZ_NONFINITE = 1 << 20;   // exponent of a row/column with an Inf/NaN maximum
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -295,7 +296,9 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
           const int cc = j * 16 + c;
           const int e = my_ea + __shfl_sync(0xffffffffu, my_fb, cc);
           double x;
-          if (e - 36 < 1024 && e + LO_EXP > -1023)
+          if (e >= OZ_NONFINITE)
+            x = __longlong_as_double(0x7ff8000000000000LL);   // a non-finite operand row/column
+          else if (e - 36 < 1024 && e + LO_EXP > -1023)
             x = fma((double)lo[cc], __longlong_as_double((long long)(e + LO_EXP + 1023) << 52),
                     (double)hi[cc] * __longlong_as_double((long long)(e - 36 + 1023) << 52));
           else
@@ -330,18 +333,28 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
 }
 
 // ---- slicing
+// Non-finite operands: the row/column maxima propagate NaN (fmax would drop it) and a row or column
+// whose maximum is Inf/NaN gets the exponent OZ_NONFINITE; every output that touches it is written
+// as NaN (DGEMM would give Inf or NaN there), so an upstream breakdown is not hidden by the slicing.
+__device__ __forceinline__ double oz_amax(double m, double x) {
+  const double a = fabs(x);
+  return (a > m || a != a) ? a : m;   // sticky NaN: NaN > m is false, and m stays NaN once it is
+}
+__device__ __forceinline__ int oz_exp_of(double m) {
+  int ex = 0;
+  if (!(m <= 1.7976931348623157e308)) return OZ_NONFINITE;   // Inf or NaN
+  if (m > 0.0) frexp(m, &ex);
+  return ex;
+}
+
 // exponent of the row maximum (frexp): one warp per row of a row-major (rows x K, ld) matrix
 __global__ void oz_rowexp_kernel(int rows, int K, const double* __restrict__ X, long long ld, int* e) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= rows) return;
   double m = 0.0;
-  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(X[(long long)w * ld + k]));
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) {
-    int ex = 0;
-    if (m > 0.0) frexp(m, &ex);
-    e[w] = ex;
-  }
+  for (int k = lane; k < K; k += 32) m = oz_amax(m, X[(long long)w * ld + k]);
+  for (int o = 16; o; o >>= 1) m = oz_amax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) e[w] = oz_exp_of(m);
 }
 
 // row maxima of a row-major (rows x K, ld) matrix with long rows: warp per (row, 8192-wide segment),
@@ -352,8 +365,8 @@ __global__ void oz_rowmax_kernel(int rows, int K, const double* __restrict__ X, 
   if (r >= rows) return;
   const int k0 = blockIdx.y * 8192, k1 = min(K, k0 + 8192);
   double m = 0.0;
-  for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs(X[(long long)r * ld + k]));
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int k = k0 + lane; k < k1; k += 32) m = oz_amax(m, X[(long long)r * ld + k]);
+  for (int o = 16; o; o >>= 1) m = oz_amax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) atomicMax(rmax + r, (unsigned long long)__double_as_longlong(m));
 }
 
@@ -378,17 +391,14 @@ __global__ void oz_colmax_kernel(int K, int cols, const double* __restrict__ X, 
   if (c >= cols) return;
   const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
   double m = 0.0;
-  for (int k = k0; k < k1; ++k) m = fmax(m, fabs(X[(long long)k * ld + c]));
+  for (int k = k0; k < k1; ++k) m = oz_amax(m, X[(long long)k * ld + c]);
   atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
 }
 
 __global__ void oz_colexp_kernel(int cols, const unsigned long long* cmax, int* e) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
-  const double m = __longlong_as_double((long long)cmax[c]);
-  int ex = 0;
-  if (m > 0.0) frexp(m, &ex);
-  e[c] = ex;
+  e[c] = oz_exp_of(__longlong_as_double((long long)cmax[c]));   // NaN's bit pattern is above Inf's
 }
 
 // Balanced base-256 digits of the 54-bit fixed-point value X = round(x 2^(54 - ex)) (|X| <= 2^54 - 1):

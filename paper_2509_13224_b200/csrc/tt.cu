@@ -121,7 +121,7 @@ __global__ void jacobi_diag_kernel(int r0, int n, int r1, int Ra, int Rb, int h,
   }
 }
 
-// floor |d| at max|d| * 1e-14 (reference amen.py:401-403): d <- max(|d|, floor)
+// floor |d| at max|d| * 1e-14 (reference amen.py:179-181): d <- max(|d|, floor)
 __global__ void abs_floor_kernel(long long n, double* d, const double* dmax) {
   const double fl = fmax(*dmax, 1e-300) * 1e-14;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -154,7 +154,7 @@ __global__ void max_final(int np, const double* part, double* out) {
 }
 
 // ---------------------------------------------------------------------------
-// PCG (scipy.sparse.linalg.cg semantics, reference amen.py:395-414)
+// PCG (scipy.sparse.linalg.cg semantics, reference amen.py:175-193)
 // device scalars S: [0] rho, [1] rho_prev, [2] pq, [3] rr(||r||^2), [4] atol^2, [5] done flag, [6] iterations
 constexpr int PB = 296;
 
@@ -510,7 +510,7 @@ TTB_API int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int 
 // Banded direct solve of the projected AMEn system. In the (i, x, z) ordering
 // (mode index outermost) the local matrix B = phiL (x) A_k (x) phiR is banded with
 // half-bandwidth bw = (h+1) r0 r1 - 1, so its Cholesky costs N bw^2 instead of N^3.
-// The solution of the permuted system is the reference's (amen.py:386-394) up to roundoff.
+// The solution of the permuted system is the reference's (amen.py:164-172) up to roundoff.
 namespace {
 
 // LB[row * (bw+1) + d] = B[row, row - d] (lower band), rows/cols in (i, x, z) order

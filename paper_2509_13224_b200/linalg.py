@@ -45,7 +45,8 @@ _GEMM_PROFILE = None  # when a list: (start_event, end_event, flops) per GEMM la
 
 
 def gemm_profile(enable: bool):
-    """Start/stop recording CUDA events around every GEMM (bench.py roofline); returns the records."""
+    """Start/stop recording CUDA events around every GEMM (bench.py roofline); returns the records
+    (start_event, end_event, flops, "ozaki"|"dmma", (M, N, K))."""
     global _GEMM_PROFILE
     rec = _GEMM_PROFILE
     _GEMM_PROFILE = [] if enable else None
@@ -87,7 +88,7 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False)
              max(out.stride(0), 1), ptr(ws))
         if prof is not None:
             e1.record()
-            prof.append((e0, e1, 2.0 * M * N * K, "ozaki"))
+            prof.append((e0, e1, 2.0 * M * N * K, "ozaki", (M, N, K)))
         if _OZAKI_CHECK:
             ref = empty(M, N)
             call("ttb_dgemm", int(tA), int(tB), M, N, K, 1.0, ptr(A), max(A.stride(0), 1), 0, ptr(B),
@@ -105,7 +106,7 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False)
              max(B.stride(0), 1), 0, float(beta), ptr(out), max(out.stride(0), 1), 0, 1)
         if prof is not None:
             e1.record()
-            prof.append((e0, e1, 2.0 * M * N * K, "dmma"))
+            prof.append((e0, e1, 2.0 * M * N * K, "dmma", (M, N, K)))
     return out
 
 
@@ -532,7 +533,7 @@ def solve(A, B):
 
 
 def cho_solve_or_lu(Bm, b):
-    """scipy cho_factor/cho_solve with fallback to a pivoted LU solve (reference amen.py:388-393)."""
+    """scipy cho_factor/cho_solve with fallback to a pivoted LU solve (reference amen.py:166-171)."""
     n = Bm.shape[0]
     L = Bm.contiguous().clone()
     info = empty(1, dtype=I32)

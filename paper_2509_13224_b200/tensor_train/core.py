@@ -26,7 +26,7 @@ __all__ = [
 
 
 class TtShapeError(ValueError):
-    """Mode sizes or bond ranks do not conform (reference core.py:80)."""
+    """Mode sizes or bond ranks do not conform (reference core.py:34)."""
 
 
 def to_device(x):
@@ -49,7 +49,7 @@ def _check_chain(cores, order):
 
 
 class TtTensor:
-    """Chain of (r_{k-1}, n_k, r_k) device cores (reference core.py:100-192)."""
+    """Chain of (r_{k-1}, n_k, r_k) device cores (reference core.py:54-146)."""
 
     def __init__(self, cores):
         self.cores = [to_device(G).contiguous() for G in cores]
@@ -94,7 +94,7 @@ class TtTensor:
         return self.full_device().cpu().numpy()
 
     def gather(self, idx):
-        """Entries at multi-indices idx (N, d) -> device (N,) (reference core.py:164-170)."""
+        """Entries at multi-indices idx (N, d) -> device (N,) (reference core.py:118-124)."""
         idx = torch.as_tensor(idx, dtype=torch.int64, device=device()).contiguous()
         if self.d != 3:
             v = self.cores[0][0, idx[:, 0], :]
@@ -121,7 +121,7 @@ class TtTensor:
 
 
 class TtMatrix:
-    """Chain of operator cores (reference core.py:195-267), dense or banded (``band`` = h)."""
+    """Chain of operator cores (reference core.py:149-221), dense or banded (``band`` = h)."""
 
     def __init__(self, cores, band=None, col_sizes=None):
         self.cores = [to_device(G).contiguous() for G in cores]
@@ -301,7 +301,7 @@ def _widen(M, h):
 
 
 def tt_add(a, b):
-    """Block-diagonal core concatenation, ranks add (reference core.py:306-325)."""
+    """Block-diagonal core concatenation, ranks add (reference core.py:260-279)."""
     a, b = _same_kind(a, b)
     ca, tag = _fused(a)
     cb, _ = _fused(b)
@@ -325,7 +325,7 @@ def tt_add(a, b):
 
 
 def tt_scale(a, c):
-    """Scalar multiple absorbed into the first core (reference core.py:332-337)."""
+    """Scalar multiple absorbed into the first core (reference core.py:286-291)."""
     cores, tag = _fused(a)
     cores = [G.clone() for G in cores]
     cores[0] = cores[0] * float(c)
@@ -337,7 +337,7 @@ def tt_sub(a, b):
 
 
 def tt_dot(a, b):
-    """Exact chain contraction (reference core.py:340-347); returns a Python float."""
+    """Exact chain contraction (reference core.py:294-301); returns a Python float."""
     if a.mode_sizes != b.mode_sizes:
         raise TtShapeError("tensor mode sizes differ")
     return float(_dot_dev(a, b).item())
@@ -355,7 +355,7 @@ def _dot_dev(a, b):
 
 
 def _rl_orthogonalize(cores, renorm=False, svd0=False):
-    """Right-to-left Householder sweep: cores[1:] right-orthonormal (reference core.py:414-419).
+    """Right-to-left Householder sweep: cores[1:] right-orthonormal (reference core.py:368-373).
 
     svd0: also return the SVD factors of the final cores[0] (the first step of the rounding's
     left-to-right pass); its carry and SVD run on a side stream while the explicit Q of core 1 is
@@ -402,7 +402,7 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False):
 
 
 def tt_norm(a):
-    """Frobenius norm through an orthogonalization sweep (reference core.py:350-370)."""
+    """Frobenius norm through an orthogonalization sweep (reference core.py:304-324)."""
     cores, _ = _fused(a)
     cores, scale = _rl_orthogonalize(cores, renorm=True)
     n0 = L.nrm2(cores[0])
@@ -412,7 +412,7 @@ def tt_norm(a):
 
 
 def tt_matvec(A, x):
-    """Operator application, ranks multiply (reference core.py:373-384)."""
+    """Operator application, ranks multiply (reference core.py:327-338)."""
     if A.col_sizes != x.mode_sizes:
         raise TtShapeError(f"operator column sizes {A.col_sizes} != vector sizes {x.mode_sizes}")
     out = []
@@ -432,7 +432,7 @@ def tt_matvec(A, x):
 
 
 def _chop(s, delta, max_rank=None):
-    """Reference _chop (core.py:387-396) on host singular values."""
+    """Reference _chop (core.py:341-350) on host singular values."""
     if s.size == 0:
         return 1
     tails = np.sqrt(np.cumsum(s[::-1] ** 2))[::-1]
@@ -443,7 +443,7 @@ def _chop(s, delta, max_rank=None):
 
 
 def tt_round(t, eps, max_rank=None):
-    """Right-to-left QR then left-to-right truncated SVD (reference core.py:399-435)."""
+    """Right-to-left QR then left-to-right truncated SVD (reference core.py:353-389)."""
     if eps <= 0:
         raise ValueError("eps must be positive")
     cores, tag = _fused(t)
@@ -469,7 +469,7 @@ def tt_round(t, eps, max_rank=None):
 
 
 def tt_from_full(X, eps=1e-14, max_rank=None):
-    """Sequential TT-SVD of a dense array (reference core.py:438-456)."""
+    """Sequential TT-SVD of a dense array (reference core.py:392-410)."""
     X = to_device(X)
     d = X.dim()
     sizes = tuple(X.shape)
@@ -490,7 +490,7 @@ def tt_from_full(X, eps=1e-14, max_rank=None):
 
 
 def tt_matrix_from_full(X, eps=1e-14):
-    """TT-SVD of a dense operator given as (n1, m1, n2, m2, ...) (reference core.py:459-475)."""
+    """TT-SVD of a dense operator given as (n1, m1, n2, m2, ...) (reference core.py:413-429)."""
     X = to_device(X)
     if X.dim() % 2:
         raise TtShapeError("operator array needs paired row/col axes")

@@ -1,7 +1,7 @@
 """Host-memory entry point for the rounded TT matrix-vector product.
 
 The reference's public call is ``tt_round(tt_matvec(A, x), eps)`` on numpy-backed TTs
-(reference tensor_train/core.py:373-384 and :399-435): operator and vector cores live in
+(reference tensor_train/core.py:327-338 and :353-389): operator and vector cores live in
 host memory and so does the result. ``tt_matvec_round_host`` is that call for host (pinned)
 cores, with the PCIe transfers overlapped with the device work instead of serialized
 around it:
@@ -68,7 +68,11 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
     for M, G in zip(A_cores, x_cores):
         Ra, n, m, Rb = M.shape
         rc, _, rd = G.shape
-        Md = L.empty(Ra, n, m, Rb)
+        # Md is allocated on (owned by) the copy stream, so the caching allocator cannot hand it memory
+        # that kernels still queued on the compute stream are reading; record_stream(comp) below then
+        # keeps it alive until the contractions that read it have run.
+        with torch.cuda.stream(copy):
+            Md = L.empty(Ra, n, m, Rb)
         Y = L.empty(Ra * rc, n, Rb * rd)
         Yv = Y.view(Ra, rc, n, Rb, rd)
         xk = xd[len(cores)]

@@ -294,8 +294,12 @@ def test_dgemm_ozaki_fp64_accuracy(tB, graded):
     call("ttb_dgemm_ozaki", tB, M, N, K, ptr(A), K, ptr(B), K if tB else N, ptr(C), N, ptr(ws))
     Cd = L.gemm(A, B, tB=bool(tB))
     scale = A.abs() @ (B.abs().t() if tB else B.abs())
-    assert float(((C - Cd).abs() / scale).max()) < (2e-12 if graded else 1e-14)
-    assert float((C - Cd).norm() / Cd.norm()) < (1e-12 if graded else 1e-14)
+    e_elem = float(((C - Cd).abs() / scale).max())
+    e_norm = float((C - Cd).norm() / Cd.norm())
+    print(f"ozaki tB={tB} graded={graded}: elementwise {e_elem:.2e} normwise {e_norm:.2e}")
+    # measured: ~1.1e-15 Gaussian, 2.9-3.8e-15 graded; bounds ~10x the measured error
+    assert e_elem < (3e-14 if graded else 1e-14), e_elem
+    assert e_norm < (3e-14 if graded else 1e-14), e_norm
     # operands reproduce exactly through the slices (I x B, incl. tiny negatives next to large entries)
     I = torch.eye(K, dtype=torch.float64, device="cuda")
     Bk = (B.t().contiguous() if tB else B).clone()
@@ -462,3 +466,38 @@ def test_round_with_emulated_gemms_matches_dmma(monkeypatch):
     Y2 = tt_round(tt_matvec(A, X), 1e-8)
     assert Y1.ranks == Y2.ranks
     assert tt_norm(tt_sub(Y1, Y2)) <= 1e-12 * tt_norm(Y2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tB", [0, 1])
+def test_dgemm_ozaki_nonfinite_propagates(tB):
+    """A NaN or Inf operand entry makes its whole output row / column NaN (as a DGEMM would make it
+    non-finite) instead of being saturated into finite slices; the other outputs are unaffected."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, N, K = 512, 256, 1024
+    A = torch.randn(M, K, generator=g, device="cuda", dtype=torch.float64)
+    B = torch.randn((N, K) if tB else (K, N), generator=g, device="cuda", dtype=torch.float64)
+    A[3, 5] = float("nan")
+    A[9, 0] = float("inf")
+    if tB:
+        B[7, 2] = float("-inf")
+    else:
+        B[2, 7] = float("-inf")
+    C = torch.empty(M, N, device="cuda", dtype=torch.float64)
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, K)), dtype=torch.uint8, device="cuda")
+    call("ttb_dgemm_ozaki", tB, M, N, K, ptr(A), K, ptr(B), K if tB else N, ptr(C), N, ptr(ws))
+    bad_r = torch.zeros(M, dtype=torch.bool, device="cuda")
+    bad_r[[3, 9]] = True
+    bad_c = torch.zeros(N, dtype=torch.bool, device="cuda")
+    bad_c[7] = True
+    nan = torch.isnan(C)
+    assert bool(nan[bad_r].all()) and bool(nan[:, bad_c].all())
+    ok = ~(bad_r[:, None] | bad_c[None, :])
+    assert not bool(nan[ok].any())
+    Af, Bf = A.clone(), B.clone()
+    Af[~torch.isfinite(Af)] = 0.0
+    Bf[~torch.isfinite(Bf)] = 0.0
+    Cd = L.gemm(Af, Bf, tB=bool(tB))
+    assert float(((C - Cd).abs()[ok]).max() / Cd.abs().max()) < 1e-14

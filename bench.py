@@ -1,15 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark: TT matvec+round GFLOP/s (FP64) on the configs[4] kernel microbenchmark,
-plus the TT-IGA Poisson solve time of configs[1] (quarter cylinder, n=128, p=3).
+"""Benchmark: TT matvec+round GFLOP/s (FP64) on the configs[4] kernel microbenchmark, plus the
+TT-IGA Poisson solves of configs[1..4] at their full BASELINE sizes.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 One step = one pass of the hot path over one synthetic batch: Y = round(A x, 1e-8)
 for a 3-core TT-matrix (1024 x 1024 modes, operator ranks 16) and a TT-vector
-(ranks 64), cores i.i.d. N(0,1)/sqrt(rank) from a seed. Inputs (2.4 GB) are larger
-than L2, so no flush is needed between steps. Multi-GPU: replicas only (the solve
-path does not shard; each rank runs its own seeded instance, no collective on the
-data path); value = total flops of all ranks / max-over-ranks device time.
+(ranks 64), cores i.i.d. N(0,1)/sqrt(rank) from a seed (reference tensor_train/core.py:327-389).
+Inputs (2.4 GB) are larger than L2, so no flush is needed between steps. Multi-GPU: replicas only
+(the solve path does not shard; each rank runs its own seeded instance, no collective on the data
+path); value = total flops of all ranks / max-over-ranks device time.
+
+GFLOP/s counts the reference algorithm's nominal LAPACK flops (workloads.matvec_round_flops) for
+BOTH arms, so the two arms' values are in the ratio of their step times; ms_per_step is the direct
+measure. The line also carries the flops the device actually executed in GEMMs
+(executed_gemm_gflop_per_step) and the same step with every product on DMMA and Householder
+factorizations (all_dmma_ms_per_step).
+
+--impl reference: the reference algorithm (the numpy/LAPACK oracle restatement of the reference
+tt_matvec + tt_round, on every host thread) on the SAME workload (mode size 1024); one step takes
+minutes on the host, so that arm times one step.
 """
 
 from __future__ import annotations

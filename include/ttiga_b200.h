@@ -101,13 +101,21 @@ int ttb_geo_eval(void* stream, long long N, const long long* idx, const int* f0,
                  const double* D2, int p0, int p1, int p2, int n0, int n1, int n2, const double* cw, double sing_tol,
                  int mode, int ri, int rj, int src, double* out, long long* bad);
 
-/* Banded operator core from a quadrature-grid TT core G (r, nq, s) (assembly._contract_matrix_core):
- * out[a, i, t, b] = sum_q G[a,q,b] w[q] X[q, i-first[q]] Y[q, j-first[q]], j = i+t-h, out (r, n, 2h+1, s). */
+/* Banded operator core from a quadrature-grid TT core G (r, nq, s) (reference assembly.py:208-222):
+ * out[a, i, t, b] = sum_q G[a,q,b] w[q] X[q, i-first[q]] Y[q, j-first[q]], j = i+t-h, out (r, n, 2h+1, s).
+ * first[] must be non-decreasing in q (Gauss points ordered by element). One CTA per (a, tile of basis
+ * indices): the tile's quadrature window of G, w, X, Y staged in shared memory, each output reduced by
+ * 4 lanes with warp shuffles. */
 int ttb_op_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
                 const double* X, const double* Y, int p, int n, int h, double* out);
-/* Load core (assembly._contract_vector_core): out[a, i, b] = sum_q G[a,q,b] w[q] V[q, i-first[q]]. */
+/* Load core (reference assembly.py:225-233): out[a, i, b] = sum_q G[a,q,b] w[q] V[q, i-first[q]] (same scheme). */
 int ttb_vec_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
                  const double* V, int p, int n, double* out);
+/* The previous one-thread-per-output forms of ttb_op_core / ttb_vec_core (A/B comparisons and tests). */
+int ttb_op_core_flat(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                     const double* X, const double* Y, int p, int n, int h, double* out);
+int ttb_vec_core_flat(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                      const double* V, int p, int n, double* out);
 /* Solution core at quadrature points: T[a,q,b] = sum_k u[a, first[q]+k, b] V[q,k]. */
 int ttb_field_table(void* stream, int r, int n, int s, const double* u, int nq, const int* first, const double* V,
                     int p, double* T);

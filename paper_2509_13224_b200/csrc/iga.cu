@@ -248,19 +248,192 @@ __global__ void geo_kernel(GeoArgs g, long long N, const long long* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// operator core (banded): out[a, i, t, b] = sum_{q in Q(i)} G[a,q,b] w[q] X[q,i-f_q] Y[q,j-f_q], j = i+t-h
-__device__ __forceinline__ int lower_bound_first(const int* f, int nq, int v) {  // first q with f[q] >= v
-  int lo = 0, hi = nq;
+// Per-direction 1D weighted quadrature of a quadrature-grid TT core (reference assembly.py:208-233):
+//   operator core (banded): out[a, i, t, b] = sum_{q: f_q <= min(i,j), f_q >= max(i,j) - p} G[a,q,b] w[q] X[q,i-f_q] Y[q,j-f_q],
+//                           j = i + t - h;
+//   load core:              out[a, i, b]    = sum_{q: i - p <= f_q <= i} G[a,q,b] w[q] V[q,i-f_q].
+// f_q (the first basis index of q's element) is non-decreasing in q, so every sum runs over a contiguous
+// q range. One CTA owns one rank index a and a tile of QT_I consecutive basis indices i: it stages the
+// tile's quadrature window of G (the contiguous rows G[a, qlo:qhi, :]), the weights, the basis tables
+// and the per-index range starts/ends in shared memory, then every output is reduced by a group of
+// QT_L lanes (strided over the range, combined with warp shuffles). The outputs of a tile are one
+// contiguous run of QT_I (2h+1) s doubles.
+constexpr int QT_T = 256;   // threads per CTA
+constexpr int QT_L = 4;     // lanes per output (shuffle-reduced)
+constexpr int QT_SMEM = 96 * 1024;
+
+__device__ __forceinline__ int lower_bound_first(const int* f, int lo, int hi, int v) {  // first q with f[q] >= v
   while (lo < hi) {
-    int mid = (lo + hi) >> 1;
+    const int mid = (lo + hi) >> 1;
     if (f[mid] < v) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
-__global__ void op_core_kernel(int r, int nq, int s, const double* __restrict__ G, const double* __restrict__ w,
-                               const int* __restrict__ first, const double* __restrict__ X,
-                               const double* __restrict__ Y, int p, int n, int h, double* out) {
+// Stages the tile's window (q in [qlo, qlo + nw)) in shared memory, or -- when nw exceeds the staging
+// capacity `cap` (a knot vector with very uneven elements) -- points the same views at global memory.
+// rb/re (per basis index k = i0 - h + e of the extended tile): the window-relative q range whose
+// first index satisfies k - p <= f_q <= k.
+__device__ __forceinline__ void qt_stage(int s, int p, int h, int i0, int ni, int cap, const int* __restrict__ first,
+                                         const double* __restrict__ Ga, const double* __restrict__ w,
+                                         const double* __restrict__ X, const double* __restrict__ Y, char* sm,
+                                         int qlo, int nw, const double*& Gs, const double*& ws, const double*& Xs,
+                                         const double*& Ys, const int*& fs, int*& rb, int*& re) {
+  const int P1 = p + 1;
+  const int next = ni + 2 * h;
+  rb = reinterpret_cast<int*>(sm);
+  re = rb + next;
+  if (nw <= cap) {
+    double* g = reinterpret_cast<double*>(sm + (((2 * next * 4) + 15) & ~15));
+    double* wv = g + (long long)nw * s;
+    double* xv = wv + nw;
+    double* yv = xv + nw * P1;
+    int* fv = reinterpret_cast<int*>(yv + (Y ? nw * P1 : 0));
+    // G rows qlo..qlo+nw-1 of rank a: one contiguous run (16-byte vector loads when aligned)
+    const long long tot = (long long)nw * s;
+    const double* src = Ga + (long long)qlo * s;
+    if ((((uintptr_t)src) & 15) == 0) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(g);
+      for (long long e = threadIdx.x; e < tot / 2; e += QT_T) d2[e] = __ldg(s2 + e);
+      if ((tot & 1) && threadIdx.x == 0) g[tot - 1] = __ldg(src + tot - 1);
+    } else {
+      for (long long e = threadIdx.x; e < tot; e += QT_T) g[e] = __ldg(src + e);
+    }
+    for (int e = threadIdx.x; e < nw; e += QT_T) {
+      wv[e] = w[qlo + e];
+      fv[e] = first[qlo + e];
+    }
+    for (int e = threadIdx.x; e < nw * P1; e += QT_T) {
+      xv[e] = X[(long long)qlo * P1 + e];
+      if (Y) yv[e] = Y[(long long)qlo * P1 + e];
+    }
+    Gs = g; ws = wv; Xs = xv; Ys = yv; fs = fv;
+  } else {
+    Gs = Ga + (long long)qlo * s;
+    ws = w + qlo;
+    Xs = X + (long long)qlo * P1;
+    Ys = Y ? Y + (long long)qlo * P1 : nullptr;
+    fs = first + qlo;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < next; e += QT_T) {
+    const int k = i0 - h + e;
+    rb[e] = lower_bound_first(fs, 0, nw, k - p);
+    re[e] = lower_bound_first(fs, 0, nw, k + 1);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(QT_T) op_core_kernel(int r, int nq, int s, const double* __restrict__ G,
+                                                       const double* __restrict__ w, const int* __restrict__ first,
+                                                       const double* __restrict__ X, const double* __restrict__ Y,
+                                                       int p, int n, int h, int ti, int cap, double* out) {
+  extern __shared__ __align__(16) char qsm[];
+  const int a = blockIdx.y;
+  const int i0 = blockIdx.x * ti, ni = min(ti, n - i0);
+  const int B = 2 * h + 1, P1 = p + 1;
+  // quadrature window of the tile: q with f_q in [i0 - p, i0 + ni - 1]
+  const int qlo = lower_bound_first(first, 0, nq, i0 - p);
+  const int qhi = lower_bound_first(first, qlo, nq, i0 + ni);
+  const int nw = qhi - qlo;
+  const double *Gs, *ws, *Xs, *Ys;
+  const int* fs;
+  int *rb, *re;
+  qt_stage(s, p, h, i0, ni, cap, first, G + (long long)a * nq * s, w, X, Y, qsm, qlo, nw, Gs, ws, Xs, Ys, fs, rb, re);
+  const int lane = threadIdx.x & (QT_L - 1);
+  const long long nout = (long long)ni * B * s;
+  double* o = out + (((long long)a * n + i0) * B) * s;
+  // one output per group of QT_L lanes; all lanes of a warp stay in the loop (shuffles)
+  for (long long g0 = threadIdx.x / QT_L; g0 < (nout + QT_T / QT_L - 1) / (QT_T / QT_L) * (QT_T / QT_L);
+       g0 += QT_T / QT_L) {
+    double acc = 0.0;
+    if (g0 < nout) {
+      const int b = (int)(g0 % s);
+      const long long rest = g0 / s;
+      const int t = (int)(rest % B), ii = (int)(rest / B);
+      const int i = i0 + ii, j = i + t - h;
+      if (j >= 0 && j < n) {
+        const int lo = rb[max(i, j) - i0 + h], hi = re[min(i, j) - i0 + h];
+        for (int q = lo + lane; q < hi; q += QT_L) {
+          const int f = fs[q];
+          acc += Gs[(long long)q * s + b] * ws[q] * Xs[q * P1 + (i - f)] * Ys[q * P1 + (j - f)];
+        }
+      }
+    }
+#pragma unroll
+    for (int m = QT_L / 2; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m, QT_L);
+    if (lane == 0 && g0 < nout) o[g0] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(QT_T) vec_core_kernel(int r, int nq, int s, const double* __restrict__ G,
+                                                        const double* __restrict__ w, const int* __restrict__ first,
+                                                        const double* __restrict__ V, int p, int n, int ti,
+                                                        int cap, double* out) {
+  extern __shared__ __align__(16) char qsm[];
+  const int a = blockIdx.y;
+  const int i0 = blockIdx.x * ti, ni = min(ti, n - i0);
+  const int P1 = p + 1;
+  const int qlo = lower_bound_first(first, 0, nq, i0 - p);
+  const int qhi = lower_bound_first(first, qlo, nq, i0 + ni);
+  const int nw = qhi - qlo;
+  const double *Gs, *ws, *Xs, *Ys;
+  const int* fs;
+  int *rb, *re;
+  qt_stage(s, p, 0, i0, ni, cap, first, G + (long long)a * nq * s, w, V, nullptr, qsm, qlo, nw, Gs, ws, Xs, Ys, fs, rb,
+           re);
+  const int lane = threadIdx.x & (QT_L - 1);
+  const long long nout = (long long)ni * s;
+  double* o = out + ((long long)a * n + i0) * s;
+  for (long long g0 = threadIdx.x / QT_L; g0 < (nout + QT_T / QT_L - 1) / (QT_T / QT_L) * (QT_T / QT_L);
+       g0 += QT_T / QT_L) {
+    double acc = 0.0;
+    if (g0 < nout) {
+      const int b = (int)(g0 % s), ii = (int)(g0 / s);
+      const int i = i0 + ii;
+      const int lo = rb[ii], hi = re[ii];
+      for (int q = lo + lane; q < hi; q += QT_L) acc += Gs[(long long)q * s + b] * ws[q] * Xs[q * P1 + (i - fs[q])];
+    }
+#pragma unroll
+    for (int m = QT_L / 2; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m, QT_L);
+    if (lane == 0 && g0 < nout) o[g0] = acc;
+  }
+}
+
+// Launch geometry: tile width ti from the mean points per element g = ceil(nq / (n - p)) (exact for
+// knot vectors without repeated interior knots), so a tile's window of <= (ti + p) elements fits the
+// staging budget; cap = window rows the dynamic shared memory actually holds (larger windows read G
+// from global memory in place).
+struct QtLaunch {
+  int ti, cap;
+  size_t smem;
+};
+
+__host__ QtLaunch qt_launch(int nq, int s, int p, int n, int h, bool two_tables) {
+  const int nel = n - p > 0 ? n - p : 1;
+  const int g = (nq + nel - 1) / nel;
+  const long long row = 8LL * s + 8 + 8LL * (p + 1) * (two_tables ? 2 : 1) + 4;
+  QtLaunch L{1, 0, 0};
+  for (int ti = 64; ti >= 1; ti >>= 1) {
+    const long long rows = (long long)(ti + p) * g;
+    const long long bytes = 16 + 8LL * (ti + 2 * h) + rows * row + 64;
+    if (bytes <= QT_SMEM || ti == 1) {
+      L.ti = ti;
+      L.cap = (int)((QT_SMEM - 16 - 8LL * (ti + 2 * h) - 64) / row);
+      if (L.cap < 0) L.cap = 0;
+      L.smem = (size_t)QT_SMEM;
+      break;
+    }
+  }
+  return L;
+}
+
+// previous thread-per-output kernels (any layout of `first`; used when one element holds more points
+// than the staging budget allows)
+__global__ void op_core_flat_kernel(int r, int nq, int s, const double* __restrict__ G, const double* __restrict__ w,
+                                    const int* __restrict__ first, const double* __restrict__ X,
+                                    const double* __restrict__ Y, int p, int n, int h, double* out) {
   const int B = 2 * h + 1;
   const long long tot = (long long)r * n * B * s;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
@@ -273,7 +446,7 @@ __global__ void op_core_kernel(int r, int nq, int s, const double* __restrict__ 
     const int j = i + t - h;
     double acc = 0.0;
     if (j >= 0 && j < n) {
-      const int lo = lower_bound_first(first, nq, max(i, j) - p);
+      const int lo = lower_bound_first(first, 0, nq, max(i, j) - p);
       for (int q = lo; q < nq; ++q) {
         const int f = first[q];
         if (f > min(i, j)) break;
@@ -285,16 +458,16 @@ __global__ void op_core_kernel(int r, int nq, int s, const double* __restrict__ 
   }
 }
 
-__global__ void vec_core_kernel(int r, int nq, int s, const double* __restrict__ G, const double* __restrict__ w,
-                                const int* __restrict__ first, const double* __restrict__ V, int p, int n,
-                                double* out) {
+__global__ void vec_core_flat_kernel(int r, int nq, int s, const double* __restrict__ G, const double* __restrict__ w,
+                                     const int* __restrict__ first, const double* __restrict__ V, int p, int n,
+                                     double* out) {
   const long long tot = (long long)r * n * s;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(e % s);
     const int i = (int)((e / s) % n);
     const int a = (int)(e / ((long long)s * n));
     double acc = 0.0;
-    const int lo = lower_bound_first(first, nq, i - p);
+    const int lo = lower_bound_first(first, 0, nq, i - p);
     for (int q = lo; q < nq; ++q) {
       const int f = first[q];
       if (f > i) break;
@@ -415,7 +588,15 @@ TTB_API int ttb_op_core(void* stream, int r, int nq, int s, const double* G, con
                         const double* X, const double* Y, int p, int n, int h, double* out) {
   long long tot = (long long)r * n * (2 * h + 1) * s;
   if (tot == 0) return TTB_OK;
-  op_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, X, Y, p, n, h, out); ttb_count();
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(op_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QT_SMEM);
+    cudaFuncSetAttribute(vec_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QT_SMEM);
+    cfg = true;
+  }
+  const QtLaunch L = qt_launch(nq, s, p, n, h, true);
+  op_core_kernel<<<dim3(ceil_div(n, L.ti), r), QT_T, L.smem, as_stream(stream)>>>(r, nq, s, G, w, first, X, Y, p, n, h,
+                                                                                  L.ti, L.cap, out); ttb_count();
   return ttb_last_error();
 }
 
@@ -423,7 +604,31 @@ TTB_API int ttb_vec_core(void* stream, int r, int nq, int s, const double* G, co
                          const double* V, int p, int n, double* out) {
   long long tot = (long long)r * n * s;
   if (tot == 0) return TTB_OK;
-  vec_core_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, V, p, n, out); ttb_count();
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(vec_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QT_SMEM);
+    cfg = true;
+  }
+  const QtLaunch L = qt_launch(nq, s, p, n, 0, false);
+  vec_core_kernel<<<dim3(ceil_div(n, L.ti), r), QT_T, L.smem, as_stream(stream)>>>(r, nq, s, G, w, first, V, p, n, L.ti,
+                                                                                   L.cap, out); ttb_count();
+  return ttb_last_error();
+}
+
+// Previous thread-per-output kernels (tools/bench comparisons only).
+TTB_API int ttb_op_core_flat(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                             const double* X, const double* Y, int p, int n, int h, double* out) {
+  long long tot = (long long)r * n * (2 * h + 1) * s;
+  if (tot == 0) return TTB_OK;
+  op_core_flat_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, X, Y, p, n, h, out); ttb_count();
+  return ttb_last_error();
+}
+
+TTB_API int ttb_vec_core_flat(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
+                              const double* V, int p, int n, double* out) {
+  long long tot = (long long)r * n * s;
+  if (tot == 0) return TTB_OK;
+  vec_core_flat_kernel<<<grid_for(tot), 256, 0, as_stream(stream)>>>(r, nq, s, G, w, first, V, p, n, out); ttb_count();
   return ttb_last_error();
 }
 

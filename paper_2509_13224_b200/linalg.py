@@ -341,12 +341,13 @@ def _jacobi(Rcm, n, want_v=False, info=None):
 _JACOBI_RT_MAX = int(os.environ.get("TTB_JACOBI_RT_MAX", "64"))
 _PRECOND = os.environ.get("TTB_JACOBI_PRECOND", "1") != "0"
 _PRECOND_RATIO = 100.0
+_PRECOND_MAX_N = int(os.environ.get("TTB_JACOBI_PRECOND_MAX_N", "160"))   # the assembly sums; larger: no sweep gain
 
 
 def _graded(norms):
     """Whether a matrix whose row/column norms (or |diag R|) are ``norms`` is graded enough for the QR
     preconditioner to pay (max/min > 100; zero entries count as graded)."""
-    if not _PRECOND or norms.numel() < 2:
+    if not _PRECOND or norms.numel() < 2 or norms.numel() > _PRECOND_MAX_N:
         return False
     mn, mx = torch.aminmax(norms.abs())
     return bool(mn * _PRECOND_RATIO < mx)

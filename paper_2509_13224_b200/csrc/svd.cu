@@ -595,6 +595,296 @@ __global__ void __launch_bounds__(GT) jacobi_gram_kernel(int n, double* A, doubl
   if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
+// Warp-sliced Gram block one-sided Jacobi (n even, n <= 1024, one matrix). Same pairing, rotation
+// rule and stopping test as jacobi_gram_kernel<8> (tournament order over blocks of 4 columns, each
+// CTA orthogonalizes one pair = 8 columns per round), but the rows are split across the 8 warps
+// (warp w owns rows [w RW, (w+1) RW) of every column for the whole run) so that a round has a
+// single CTA barrier:
+//   per warp: wait until the previous owners' warp w published these rows (ver[b][w], acquire),
+//             cp.async its 8 x RW slab into shared memory, partial Gram by DMMA;
+//   CTA:      barrier, every warp sums the 8 partial Grams (same order: identical G in all warps);
+//   per warp: convergence test + one cyclic sweep of the 8 x 8 two-sided Jacobi (redundantly in
+//             every warp: no broadcast barrier), A_slab J by DMMA straight to global, fence,
+//             publish ver[b][w] (release).
+// Rows never move between warps, so a warp depends only on the same warp index of the CTAs that
+// held its two blocks in the previous round; the per-round critical path is one L2 round trip,
+// one 8 KB slab load, ~70 DMMA and the 8 x 8 rotation sweep instead of eight barriers around
+// single-warp and single-thread sections (jacobi_gram_kernel: 11 us per round, 46% barrier stall).
+constexpr int WS_W = 8;          // warps per CTA
+constexpr int WS_T = WS_W * 32;
+
+__device__ __forceinline__ uint32_t sm_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}\n" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   sm_u32(dst)),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// Rotation of jrot, branch-free, with the tangent from approximate (MUFU) reciprocal square root and
+// reciprocal on power-of-two-scaled operands: t only chooses the angle -- any t gives an exactly
+// orthogonal (c, s) below, and a t off by ~1e-6 relative leaves ~1e-6 of g_pq for the next visit --
+// while c = (1 + t^2)^(-1/2) is the FP64 rsqrt, so (c, s) are orthogonal to rounding. Replaces jrot's
+// FP64 square root and division.
+__device__ __forceinline__ void jrot_fast(double al, double be, double ga, double thr2, double& c, double& s) {
+  const double d = be - al, g2 = 2.0 * ga;
+  const double m = fmax(fabs(d), fabs(g2));
+  const long long ex = (__double_as_longlong(m) >> 52) & 0x7ff;
+  const double sc = __longlong_as_double((2046LL - min(ex, 2045LL)) << 52);   // 2^(1023 - ex): m sc in [1, 2)
+  const double ds = fabs(d) * sc, gs = fabs(g2) * sc;
+  const double h = fma(ds, ds, gs * gs);
+  const double den = fma(h, rsqrt_approx(h), ds);          // |d| + sqrt(d^2 + g^2), scaled, >= 1
+  double t = gs * rcp_approx(den);
+  const bool pos = (d == 0.0) || ((d > 0.0) == (g2 > 0.0));
+  t = pos ? t : -t;
+  // c from the library rsqrt (unbiased rounding): a hand-rolled Newton step from the approximate
+  // rsqrt lands ~2e-17 high on average, and 1e4 rotation visits per column turn that into a 3e-13
+  // drift of the column norms
+  const double r = rsqrt(fma(t, t, 1.0));
+  const bool act = ga != 0.0 && ga * ga > thr2 * al * be;
+  c = act ? r : 1.0;
+  s = act ? r * t : 0.0;
+}
+
+__device__ __forceinline__ bool jw_eigen8(double* G, double* J, double tol, int lane) {
+  // absent columns (n % 4 != 0) are zero: they pass the test and never rotate
+  bool nd = false;
+  for (int e = lane; e < 64; e += 32) {
+    const int p = e >> 3, q = e & 7;
+    if (p < q) {
+      const double ga = G[e];
+      if (!(ga == 0.0 || fabs(ga) <= tol * sqrt(G[p * 9] * G[q * 9]))) nd = true;
+    }
+  }
+  nd = __any_sync(0xffffffffu, nd);
+  if (nd) {
+    // every lane computes the two rotations it needs itself (pairs k1 = lane / 8 and k2),
+    // so a round is one shared-memory read / update / write with no parameter broadcast
+    const double thr2 = 0.0625 * tol * tol;
+    const int k1 = lane >> 3, k2 = (lane >> 1) & 3, rr = lane & 1, ji = lane & 7;
+#pragma unroll
+    for (int rd = 0; rd < 7; ++rd) {
+      int p1 = rr_index(k1, rd, 8), q1 = rr_index(7 - k1, rd, 8);
+      int p2 = rr_index(k2, rd, 8), q2 = rr_index(7 - k2, rd, 8);
+      if (p1 > q1) { int t = p1; p1 = q1; q1 = t; }
+      if (p2 > q2) { int t = p2; p2 = q2; q2 = t; }
+      const double a1 = G[p1 * 9], b1 = G[q1 * 9], g1 = G[p1 * 8 + q1];
+      const double a2 = G[p2 * 9], b2 = G[q2 * 9], g2 = G[p2 * 8 + q2];
+      const double gpp = G[p1 * 8 + p2], gpq = G[p1 * 8 + q2], gqp = G[q1 * 8 + p2], gqq = G[q1 * 8 + q2];
+      const double jp = J[ji * 8 + p1], jq = J[ji * 8 + q1];
+      double c1, s1, c2, s2;
+      jrot_fast(a1, b1, g1, thr2, c1, s1);
+      jrot_fast(a2, b2, g2, thr2, c2, s2);
+      const double up = rr ? (s1 * gpp + c1 * gqp) : (c1 * gpp - s1 * gqp);
+      const double uq = rr ? (s1 * gpq + c1 * gqq) : (c1 * gpq - s1 * gqq);
+      const double nv0 = c2 * up - s2 * uq, nv1 = s2 * up + c2 * uq;
+      const double jv0 = c1 * jp - s1 * jq, jv1 = s1 * jp + c1 * jq;
+      const int gx = rr ? q1 : p1;
+      __syncwarp();
+      G[gx * 8 + p2] = nv0;
+      G[gx * 8 + q2] = nv1;
+      J[ji * 8 + p1] = jv0;
+      J[ji * 8 + q1] = jv1;
+      __syncwarp();
+    }
+  }
+  return nd;
+}
+
+__global__ void __launch_bounds__(WS_T) jacobi_wslice_kernel(int n, int RW, double* A, double* V, int* cnt, int* ver,
+                                                              int max_sweeps, double tol, int* sweeps_out,
+                                                              long long* prof = nullptr) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double Gp[2][WS_W][64];
+  __shared__ double G[64], J[64];
+  __shared__ int need_s;
+  __shared__ __align__(8) unsigned long long mbar[WS_W];
+#define JW_STAMP(k)                                                                                          \
+  if (prof && lane == 0 && w == 0 && R >= 64 && R < 80) {                                                 \
+    long long t_;                                                                                            \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                                 \
+    prof[((long long)blockIdx.x * 16 + (R - 64)) * 8 + (k)] = t_;                                          \
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb = (n + 3) / 4;
+  const int NBL = (nb + 1) & ~1;
+  const int LDW = RW + 4;
+  const int nmat = V ? 2 : 1;
+  double* slab = sm + (size_t)w * nmat * 8 * LDW;  // [mat][col][row] for this warp
+  const int row0 = w * RW;
+  const int vrows = max(0, min(RW, n - row0));     // rows of this warp's slab inside the matrix
+  const uint32_t bar = sm_u32(&mbar[w]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) { cnt[0] = 0; cnt[1] = 0; }
+  if (blockIdx.x == 0)
+    for (int b = threadIdx.x; b < nb * WS_W; b += WS_T) ver[b] = 0;
+  for (int e = lane; e < nmat * 8 * LDW; e += 32) slab[e] = 0.0;   // rows >= n stay zero
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  grid.sync();
+  uint32_t phase = 0;
+  int sweep = 0, gpar = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int* c = cnt + (sweep & 1);
+    for (int r = 0; r < NBL - 1; ++r) {
+      const int R = sweep * (NBL - 1) + r;
+      for (int pr = blockIdx.x; pr < NBL / 2; pr += gridDim.x) {
+        int bp = rr_index(pr, r, NBL), bq = rr_index(NBL - 1 - pr, r, NBL);
+        if (bp > bq) { int t = bp; bp = bq; bq = t; }
+        if (bq >= nb) {  // paired with the dummy block: pass the round
+          if (lane == 0 && bp < nb) {
+            while (ld_acquire(ver + bp * WS_W + w) < R) {}
+            st_release(ver + bp * WS_W + w, R + 1);
+          }
+          __syncwarp();
+          continue;
+        }
+        JW_STAMP(0);
+        // slab load: block bp's 4 columns as soon as bp is published, then bq's (bulk copies of
+        // this warp's rows; absent columns zeroed)
+        const int cp_ = min(4, n - bp * 4), cq_ = min(4, n - bq * 4);
+        if (lane == 0 && vrows > 0) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                       "r"((uint32_t)(nmat * (cp_ + cq_) * vrows * 8))
+                       : "memory");
+          while (ld_acquire(ver + bp * WS_W + w) < R) {}
+          for (int mat = 0; mat < nmat; ++mat)
+            for (int lc = 0; lc < cp_; ++lc)
+              bulk_g2s(slab + (mat * 8 + lc) * LDW, (mat ? V : A) + (long long)(bp * 4 + lc) * n + row0, vrows * 8, bar);
+          while (ld_acquire(ver + bq * WS_W + w) < R) {}
+          for (int mat = 0; mat < nmat; ++mat)
+            for (int lc = 0; lc < cq_; ++lc)
+              bulk_g2s(slab + (mat * 8 + 4 + lc) * LDW, (mat ? V : A) + (long long)(bq * 4 + lc) * n + row0, vrows * 8,
+                       bar);
+        } else if (lane == 0) {
+          while (ld_acquire(ver + bp * WS_W + w) < R || ld_acquire(ver + bq * WS_W + w) < R) {}
+        }
+        if (cp_ < 4 || cq_ < 4) {
+          for (int mat = 0; mat < nmat; ++mat)
+            for (int lc = 0; lc < 8; ++lc)
+              if ((lc < 4 && lc >= cp_) || (lc >= 4 && lc - 4 >= cq_))
+                for (int e = lane; e < RW; e += 32) slab[(mat * 8 + lc) * LDW + e] = 0.0;
+        }
+        JW_STAMP(1);
+        if (vrows > 0) {
+          mbar_wait_parity(bar, phase);
+          phase ^= 1;
+        }
+        __syncwarp();
+        JW_STAMP(2);
+        // partial Gram of this warp's rows: 4 independent DMMA chains over k-steps of 4 rows
+        {
+          const double* col = slab + (lane >> 2) * LDW + (lane & 3);
+          double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+          for (int k = 0; k < RW; k += 16) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double x = col[k + 4 * u];
+              dmma8(d[u][0], d[u][1], x, x);
+            }
+          }
+          const int e0 = (lane >> 2) * 8 + 2 * (lane & 3);
+          Gp[gpar][w][e0] = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+          Gp[gpar][w][e0 + 1] = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
+        }
+        __syncthreads();
+        JW_STAMP(3);
+        // warp 0: full Gram, convergence test, one cyclic sweep of the 8 x 8 two-sided Jacobi
+        // (rotations accumulated in J); the other warps wait at the broadcast barrier
+        if (w == 0) {
+          for (int e = lane; e < 64; e += 32) {
+            double g = 0.0;
+#pragma unroll
+            for (int v = 0; v < WS_W; ++v) g += Gp[gpar][v][e];
+            G[e] = g;
+            J[e] = ((e >> 3) == (e & 7)) ? 1.0 : 0.0;
+          }
+          __syncwarp();
+          const bool nd = jw_eigen8(G, J, tol, lane);
+          if (lane == 0) need_s = nd;
+        }
+        gpar ^= 1;
+        __syncthreads();
+        const bool need = need_s;
+        if (need) {
+          JW_STAMP(4);
+          // A_slab <- A_slab J (and V_slab), straight to global, as (A_slab J)^T = J^T A_slab^T so that
+          // each lane holds two consecutive rows of one column (16-byte stores, 64-byte segments)
+          const double j0 = J[(lane & 3) * 8 + (lane >> 2)], j1 = J[(4 + (lane & 3)) * 8 + (lane >> 2)];
+          const int oc = lane >> 2;
+          const int gco = (oc < 4 ? bp * 4 : bq * 4) + (oc & 3);
+          const bool oko = oc < 4 ? oc < cp_ : oc - 4 < cq_;
+          for (int mat = 0; mat < nmat; ++mat) {
+            double* X = mat ? V : A;
+            const double* src = slab + mat * 8 * LDW + (lane & 3) * LDW + (lane >> 2);
+            double2* dst = reinterpret_cast<double2*>(X + (long long)gco * n + row0 + 2 * (lane & 3));
+#pragma unroll 4
+            for (int s = 0; s < RW; s += 8) {
+              const double a0 = src[s], a1 = src[4 * LDW + s];
+              double d0 = 0.0, d1 = 0.0;
+              dmma8(d0, d1, j0, a0);
+              dmma8(d0, d1, j1, a1);
+              if (oko && row0 + s + 2 * (lane & 3) < n) dst[s / 2] = make_double2(d0, d1);
+            }
+          }
+          JW_STAMP(5);
+        }
+        // generic-proxy slab accesses of this round before the next round's bulk writes
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        JW_STAMP(6);
+        // publish: the warp barrier orders every lane's stores before lane 0's release fence, which
+        // is cumulative over them (and over the acquires that admitted this round)
+        if (lane == 0) {
+          if (need && w == 0) atomicAdd(c, 1);
+          asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+          st_relaxed(ver + bp * WS_W + w, R + 1);
+          st_relaxed(ver + bq * WS_W + w, R + 1);
+        }
+        JW_STAMP(7);
+      }
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(sweep + 1) & 1] = 0;
+    const int done = (*(volatile int*)c) == 0;
+    grid.sync();
+    if (done) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
 __global__ void init_av_kernel(int n, const double* Ain, double* A, double* V) {
   const long long nn = (long long)n * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
@@ -687,14 +977,40 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
     static int jalg = -1;
     if (jalg < 0) {
       const char* ev = getenv("TTB_JACOBI");
-      jalg = (ev && ev[0] == 'b') ? 1 : (ev && ev[0] == '1') ? 2 : 0;  // block | 16-column | default
+      jalg = (ev && ev[0] == 'b') ? 1 : (ev && ev[0] == '1') ? 2 : (ev && ev[0] == 'g') ? 3 : 0;  // block | 16-column | gram | default
     }
     const size_t rows_pad = (size_t)(((n + 31) & ~31) + 4);
     const size_t gsmem16 = (size_t)16 * rows_pad * (V ? 2 : 1) * sizeof(double);
     const size_t gsmem8 = (size_t)8 * rows_pad * (V ? 2 : 1) * sizeof(double);
     // 8 columns per CTA: measured 38 ms vs 57 ms (16 columns) for n = 1024 at equal sweep counts
     const bool use16 = jalg == 2 && gsmem16 <= 200 * 1024;
-    if (jalg != 1 && gsmem8 <= 200 * 1024) {
+    // warp-sliced kernel (default): n even, <= 1024 (rows per warp <= 128)
+    const int wrw = ((((n + WS_W - 1) / WS_W) + 15) / 16) * 16;
+    const size_t wsmem = (size_t)WS_W * (V ? 2 : 1) * 8 * (wrw + 4) * sizeof(double);
+    if (jalg == 0 && n % 2 == 0 && n <= 1024 && wsmem <= 200 * 1024) {
+      static int wmax = 0;
+      if (!wmax) {
+        cudaFuncSetAttribute(jacobi_wslice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_wslice_kernel, WS_T, 200 * 1024);
+        wmax = sms * (per > 0 ? per : 1);
+      }
+      const int nbk = (n + 3) / 4;
+      int nblk = ((nbk + 1) / 2) < wmax ? ((nbk + 1) / 2) : wmax;
+      static int* wver = nullptr;
+      static int wver_cap = 0;
+      if (nbk * WS_W > wver_cap) {
+        if (wver) { cudaStreamSynchronize(st); cudaFree(wver); }
+        wver_cap = nbk * WS_W + 1024;
+        if (cudaMalloc(&wver, sizeof(int) * wver_cap) != cudaSuccess) { wver = nullptr; wver_cap = 0; return (int)cudaErrorMemoryAllocation; }
+      }
+      int rw = wrw;
+      long long* noprof = nullptr;
+      void* args[] = {&n, &rw, &Aw, &Vw, &cnt, &wver, &ms, &tl, &sw, &noprof};
+      e = cudaLaunchCooperativeKernel((const void*)jacobi_wslice_kernel, dim3(nblk), dim3(WS_T), args, wsmem, st); ttb_count();
+    } else if (jalg != 1 && gsmem8 <= 200 * 1024) {
       const int GBsel = use16 ? 16 : 8;
       const void* kfn = use16 ? (const void*)jacobi_gram_kernel<16> : (const void*)jacobi_gram_kernel<8>;
       static int gmax[2] = {0, 0};

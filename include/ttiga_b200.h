@@ -89,6 +89,15 @@ int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, int max_
 int ttb_basis_eval(void* stream, int nq, const double* x, const double* knots, int nk, int p, const double* weights,
                    int* first, double* V, double* D, int* bad);
 
+/* min det J over the full nq0 x nq1 x nq2 tensor grid of the windows (f_d, V_d, D_d) (admissibility of the
+ * seeded random geometry at every Gauss point of the solve, BASELINE configs[3]). out (device, 2 x u64):
+ * out[0] = order-preserving key of min det J (decode: k >> 63 ? bits k ^ 2^63 : bits ~k), out[1] = number of
+ * points with det J <= 0. No reference counterpart (configs[3]'s geometry is a BASELINE extension). */
+int ttb_geo_min_det(void* stream, int nq0, int nq1, int nq2, const int* f0, const int* f1, const int* f2,
+                    const double* V0, const double* V1, const double* V2, const double* D0, const double* D1,
+                    const double* D2, int p0, int p1, int p2, int n0, int n1, int n2, const double* cw,
+                    unsigned long long* out);
+
 /* Rational geometry map at N grid multi-indices idx (int64, N x 3) of a tensor grid whose per-direction
  * basis windows are (f_d, V_d, D_d). cw: control grid (n0, n1, n2, 4) = (w x, w y, w z, w).
  * mode 0: out[k] = R[ri][rj], R = J^-1 J^-T det J       (assembly.metric_oracle)

@@ -500,11 +500,23 @@ def extend(u_int, sl, sizes):
     return T.TT(out)
 
 
+def geometry_params(cfg: Config):
+    """cfg.geometry_params, plus -- for the seeded random cube solved on an exact-count (n_basis) open
+    uniform space -- the solve's Gauss grid as the det J > 0 admissibility grid (BASELINE configs[3]:
+    "rejected until det J > 0 at all Gauss points")."""
+    prm = dict(cfg.geometry_params)
+    if cfg.geometry == "random_cube" and cfg.n_basis is not None and "check_gauss" not in prm:
+        ng = cfg.n_gauss
+        q = [d + 1 for d in cfg.degree] if ng is None else ([int(ng)] * 3 if np.isscalar(ng) else [int(g) for g in ng])
+        prm["check_gauss"] = [[n - d, g] for n, d, g in zip(cfg.n_basis, cfg.degree, q)]
+    return prm
+
+
 def solve(cfg: Config, want_error=True):
     """Reference solve_poisson (driver.py:455-532) without the operator cache."""
     tm = {}
     t0 = time.perf_counter()
-    patch = build_patch(cfg.geometry, cfg.geometry_params)
+    patch = build_patch(cfg.geometry, geometry_params(cfg))
     cfg.resolve(patch)
     disc = discretize(cfg, patch)
     tm["t_setup_s"] = time.perf_counter() - t0

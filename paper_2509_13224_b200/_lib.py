@@ -46,6 +46,8 @@ SIGNATURES = {
     "ttb_basis_eval": (i32, [vp, i32, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "ttb_geo_eval": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, f64,
                            i32, i32, i32, i32, vp, vp]),
+    "ttb_geo_min_det": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp,
+                              vp]),
     "ttb_op_core": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]),
     "ttb_vec_core": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, i32, i32, vp]),
     "ttb_op_core_flat": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]),

@@ -584,6 +584,61 @@ TTB_API int ttb_geo_eval(void* stream, long long N, const long long* idx, const 
   return ttb_last_error();
 }
 
+// min det J over the full tensor grid n0 x n1 x n2 (and the count of det J <= 0): the admissibility
+// check of seeded random geometries at every Gauss point of the solve (8.4e9 points at configs[3]).
+// One thread per point, grid-stride; min as an order-preserving 64-bit key.
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  const long long b = __double_as_longlong(d);
+  return b >= 0 ? ((unsigned long long)b ^ 0x8000000000000000ULL) : ~(unsigned long long)b;
+}
+__global__ void __launch_bounds__(256) min_det_kernel(GeoArgs g, int n0, int n1, int n2, unsigned long long* minkey,
+                                                      unsigned long long* count) {
+  const long long N = (long long)n0 * n1 * n2;
+  double mn = 1.0e308;
+  unsigned long long cnt = 0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < N; k += (long long)gridDim.x * blockDim.x) {
+    const int q2 = (int)(k % n2);
+    const long long t = k / n2;
+    const int q1 = (int)(t % n1), q0 = (int)(t / n1);
+    GeoOut o;
+    geo_point(g, q0, q1, q2, o);
+    mn = fmin(mn, o.det);
+    cnt += (o.det <= 0.0);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(minkey, dkey(mn));
+    if (cnt) atomicAdd(count, cnt);
+  }
+}
+
+TTB_API int ttb_geo_min_det(void* stream, int nq0, int nq1, int nq2, const int* f0, const int* f1, const int* f2,
+                            const double* V0, const double* V1, const double* V2, const double* D0, const double* D1,
+                            const double* D2, int p0, int p1, int p2, int n0, int n1, int n2, const double* cw,
+                            unsigned long long* out) {
+  if (nq0 < 1 || nq1 < 1 || nq2 < 1 || !out) return TTB_EARG;
+  const int* f[3] = {f0, f1, f2};
+  const double* V[3] = {V0, V1, V2};
+  const double* D[3] = {D0, D1, D2};
+  int p[3] = {p0, p1, p2}, n[3] = {n0, n1, n2};
+  GeoArgs g = make_geo(f, V, D, p, n, cw, 0.0);
+  cudaStream_t st = as_stream(stream);
+  const unsigned long long init[2] = {~0ULL, 0ULL};
+  cudaMemcpyAsync(out, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long N = (long long)nq0 * nq1 * nq2;
+  long long blocks = (N + 255) / 256;
+  if (blocks > 8LL * sms) blocks = 8LL * sms;
+  min_det_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, nq0, nq1, nq2, out, out + 1); ttb_count();
+  return ttb_last_error();
+}
+
 TTB_API int ttb_op_core(void* stream, int r, int nq, int s, const double* G, const double* w, const int* first,
                         const double* X, const double* Y, int p, int n, int h, double* out) {
   long long tot = (long long)r * n * (2 * h + 1) * s;

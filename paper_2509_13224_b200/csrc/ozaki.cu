@@ -618,6 +618,54 @@ OzWs oz_ws_layout(void* base, int M, int N, int K, int gram) {
   return w;
 }
 
+// Row exponent + slicing in ONE pass (K % 4 == 0, K <= 128 NQ): one warp per row holds the row in
+// registers (lane l: quads l + 32 j), takes the max, then writes the 7 slice planes -- the operand is
+// read once instead of twice (oz_rowexp_kernel + oz_slice_rows_kernel: 8.6 GB of extra reads per
+// 1M x 1024 operand).
+template <int NQ>
+__global__ void __launch_bounds__(256) oz_rowslice_fused_kernel(int rows, int K, const double* __restrict__ X,
+                                                                 long long ld, int* __restrict__ e, uint8_t* out) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int kq = K / 4;
+  const long long plane = (long long)rows * K;
+  const double* x = X + (long long)r * ld;
+  const bool al = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)(ld * 8)) & 15) == 0;
+  double v[NQ][4];
+  double m = 0.0;
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int q = lane + 32 * j;
+    if (q < kq) {
+      if (al) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(x + 4 * q));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(x + 4 * q) + 1);
+        v[j][0] = a.x; v[j][1] = a.y; v[j][2] = b.x; v[j][3] = b.y;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[j][u] = __ldg(x + 4 * q + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m = oz_amax(m, v[j][u]);
+    }
+  }
+  for (int o = 16; o; o >>= 1) m = oz_amax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int ex = oz_exp_of(m);
+  if (lane == 0) e[r] = ex;
+  const double sc = oz_scale_of(ex);
+  uint8_t* o = out + (long long)r * K;
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int q = lane + 32 * j;
+    if (q < kq) {
+      uint32_t w[OZ_S];
+      oz_digits4(v[j], ex, sc, w);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane + 4 * q) = w[s];
+    }
+  }
+}
+
 // exponents (and slices) of the rows of a row-major (rows x K, ld) operand
 void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, int* e, unsigned long long* rmax,
              uint8_t* out) {
@@ -625,6 +673,14 @@ void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, in
     cudaMemsetAsync(rmax, 0, sizeof(unsigned long long) * rows, st);
     oz_rowmax_kernel<<<dim3(ceil_div(rows, 8), ceil_div(K, 8192)), 256, 0, st>>>(rows, K, X, ld, rmax); ttb_count();
     oz_colexp_kernel<<<ceil_div(rows, 256), 256, 0, st>>>(rows, rmax, e); ttb_count();
+  } else if (K % 4 == 0 && K <= 128 * 16) {
+    const unsigned g = (unsigned)ceil_div((long long)rows * 32, 256);
+    if (K <= 128 * 2) oz_rowslice_fused_kernel<2><<<g, 256, 0, st>>>(rows, K, X, ld, e, out);
+    else if (K <= 128 * 4) oz_rowslice_fused_kernel<4><<<g, 256, 0, st>>>(rows, K, X, ld, e, out);
+    else if (K <= 128 * 8) oz_rowslice_fused_kernel<8><<<g, 256, 0, st>>>(rows, K, X, ld, e, out);
+    else oz_rowslice_fused_kernel<16><<<g, 256, 0, st>>>(rows, K, X, ld, e, out);
+    ttb_count();
+    return;
   } else {
     oz_rowexp_kernel<<<ceil_div((long long)rows * 32, 256), 256, 0, st>>>(rows, K, X, ld, e); ttb_count();
   }
@@ -632,8 +688,69 @@ void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, in
 }
 
 // exponents (and transposed slices) of the columns of a row-major (K x cols, ld) operand
+// Column exponent + transposed slicing in one kernel for short K (K <= 2048): a CTA owns 64 columns
+// over all K rows -- pass 1 takes the column maxima (DRAM), pass 2 re-reads the CTA's 64 x K tile
+// (<= 1 MB, L2-resident across the ~148 concurrent CTAs) and slices through the shared-memory
+// transpose of oz_slice_cols_kernel. Saves the separate oz_colmax pass over the operand from DRAM.
+__global__ void __launch_bounds__(256) oz_cols_fused_kernel(int K, int cols, const double* __restrict__ X, long long ld,
+                                                            int* __restrict__ e, uint8_t* out) {
+  __shared__ uint32_t t[OZ_S][64][17];
+  __shared__ double pm[4][64];
+  __shared__ int es[64];
+  const int c0 = blockIdx.x * 64;
+  const long long plane = (long long)cols * K;
+  {
+    const int cc = threadIdx.x & 63, kr = threadIdx.x >> 6;
+    const int c = c0 + cc;
+    double m = 0.0;
+    if (c < cols)
+      for (int k = kr; k < K; k += 4) m = oz_amax(m, __ldg(X + (long long)k * ld + c));
+    pm[kr][cc] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const double m = oz_amax(oz_amax(pm[0][threadIdx.x], pm[1][threadIdx.x]), oz_amax(pm[2][threadIdx.x], pm[3][threadIdx.x]));
+    const int ex = oz_exp_of(m);
+    es[threadIdx.x] = ex;
+    if (c0 + (int)threadIdx.x < cols) e[c0 + threadIdx.x] = ex;
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < K; k0 += 64) {
+    for (int it = threadIdx.x; it < 64 * 16; it += 256) {
+      const int cc = it & 63, kq = it >> 6;
+      const int c = c0 + cc;
+      uint32_t w[OZ_S];
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) w[s] = 0;
+      if (c < cols) {
+        const int ex = es[cc];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = k0 + 4 * kq + q;
+          v[q] = k < K ? __ldg(X + (long long)k * ld + c) : 0.0;
+        }
+        oz_digits4(v, ex, oz_scale_of(ex), w);
+      }
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) t[s][cc][kq] = w[s];
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < OZ_S * 64 * 16; it += 256) {
+      const int kq = it & 15, cc = (it >> 4) & 63, s = it >> 10;
+      const int c = c0 + cc, k = k0 + 4 * kq;
+      if (c < cols && k < K) *reinterpret_cast<uint32_t*>(out + s * plane + (long long)c * K + k) = t[s][cc][kq];
+    }
+    __syncthreads();
+  }
+}
+
 void oz_cols(cudaStream_t st, int K, int cols, const double* X, long long ld, int* e, unsigned long long* cmax,
              uint8_t* out) {
+  if (K <= 2048) {
+    oz_cols_fused_kernel<<<ceil_div(cols, 64), 256, 0, st>>>(K, cols, X, ld, e, out); ttb_count();
+    return;
+  }
   cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * cols, st);
   oz_colmax_kernel<<<dim3(ceil_div(cols, 256), ceil_div(K, 256)), 256, 0, st>>>(K, cols, X, ld, cmax); ttb_count();
   oz_colexp_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(cols, cmax, e); ttb_count();

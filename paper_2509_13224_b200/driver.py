@@ -303,12 +303,24 @@ def _sync():
     torch.cuda.synchronize()
 
 
+def geometry_params(cfg: SolveConfig) -> dict:
+    """cfg.geometry_params, plus -- for the seeded random cube on an exact-count (n_basis) open uniform
+    solution space -- the solve's Gauss grid as its det J > 0 admissibility grid (BASELINE configs[3]:
+    "rejected until det J > 0 at all Gauss points"; oracle/iga.py geometry_params)."""
+    prm = dict(cfg.geometry_params)
+    if cfg.geometry == "random_cube" and cfg.n_basis is not None and "check_gauss" not in prm:
+        ng = cfg.n_gauss
+        q = [d + 1 for d in cfg.degree] if ng is None else ([int(ng)] * 3 if np.isscalar(ng) else [int(g) for g in ng])
+        prm["check_gauss"] = [[n - d, g] for n, d, g in zip(cfg.n_basis, cfg.degree, q)]
+    return prm
+
+
 def solve_poisson(cfg: SolveConfig, want_error: bool = True) -> SolutionReport:
     """Full TT pipeline for one configuration (reference driver.py:455-532; no operator cache)."""
     timings = {}
     _sync()
     t0 = time.perf_counter()
-    patch = make_geometry(cfg.geometry, cfg.geometry_params)
+    patch = make_geometry(cfg.geometry, geometry_params(cfg))
     cfg.resolve_bc(patch)
     disc = discretize(cfg, patch)
     _sync()

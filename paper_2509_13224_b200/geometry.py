@@ -131,6 +131,20 @@ class GridEvaluator:
             xi = tuple(float(self.axes_points[d][q[d]]) for d in range(3))
             raise SingularMapError(f"singular geometry map at xi={xi}")
 
+    def min_det(self):
+        """(min det J, number of points with det J <= 0) over the FULL tensor grid (device kernel
+        ttb_geo_min_det; no index list, so the 8.4e9-point Gauss grid of configs[3] is one launch)."""
+        out = torch.empty(2, dtype=torch.int64, device=device())
+        (f0, V0, D0), (f1, V1, D1), (f2, V2, D2) = self.win
+        p = self.patch.degrees
+        n = self.cw.shape[:3]
+        q = self.shape
+        call("ttb_geo_min_det", q[0], q[1], q[2], ptr(f0), ptr(f1), ptr(f2), ptr(V0), ptr(V1), ptr(V2), ptr(D0),
+             ptr(D1), ptr(D2), p[0], p[1], p[2], n[0], n[1], n[2], ptr(self.cw), ptr(out))
+        key, bad = (int(v) & ((1 << 64) - 1) for v in out.cpu().tolist())
+        bits = key ^ (1 << 63) if key >> 63 else (~key) & ((1 << 64) - 1)
+        return float(np.frombuffer(np.uint64(bits).tobytes(), dtype=np.float64)[0]), bad
+
     def records(self, idx, check=True):
         """(N, 22) device records: J (9), x (3), det, R (9)."""
         N = len(idx)
@@ -385,32 +399,49 @@ def _deformed_cube(prm):
                      "directions": ("x", "y", "z"), "default_dirichlet": _all_faces()})
 
 
+def gauss_grid(elements, points):
+    """Gauss-Legendre points of ``elements`` uniform spans of [0, 1], ``points`` per span: the solve's
+    quadrature on an exact-count open uniform solution basis (assembly.build_quadrature)."""
+    xg, _ = np.polynomial.legendre.leggauss(int(points))
+    brk = np.linspace(0.0, 1.0, int(elements) + 1)
+    return np.concatenate([0.5 * (a + b) + 0.5 * (b - a) * xg for a, b in zip(brk[:-1], brk[1:])])
+
+
 def _random_cube(prm):
     """BASELINE config 4: seeded N(0, sigma^2) perturbation of a degree-3 cube net, det J > 0 rejection.
 
-    Check grid: 8 Gauss-Legendre points per geometry knot span per direction, evaluated on the device.
+    Check grid: with ``check_gauss = (elements, points)`` (set by the solve driver for exact-count
+    solution spaces) every Gauss point of the solve -- 2036^3 = 8.4e9 points at configs[3], one
+    min-det kernel launch per draw; otherwise 8 Gauss-Legendre points per geometry knot span.
+    Oracle: oracle/patch.py random_cube (same draws, same grid).
     """
-    p = _take(prm, {"sigma": 0.02, "n_ctrl": 8, "degree": 3, "seed": 0, "max_draws": 100})
+    p = _take(prm, {"sigma": 0.02, "n_ctrl": 8, "degree": 3, "seed": 0, "max_draws": 100, "check_gauss": None})
     deg, nc = int(p["degree"]), int(p["n_ctrl"])
     kv = KnotVector.open_uniform(deg, nc - deg)
     from .splines import greville_points
     g = greville_points(kv)
     base = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1)
     rng = np.random.default_rng(int(p["seed"]))
-    xg, _ = np.polynomial.legendre.leggauss(8)
-    brk = np.unique(kv.knots)
-    chk = np.concatenate([0.5 * (a + b) + 0.5 * (b - a) * xg for a, b in zip(brk[:-1], brk[1:])])
+    if p["check_gauss"] is not None:
+        cg = np.asarray(p["check_gauss"], dtype=int).reshape(-1, 2)
+        cg = np.repeat(cg, 3, axis=0) if cg.shape[0] == 1 else cg
+        axes = [gauss_grid(E, q) for E, q in cg]
+    else:
+        xg, _ = np.polynomial.legendre.leggauss(8)
+        brk = np.unique(kv.knots)
+        chk = np.concatenate([0.5 * (a + b) + 0.5 * (b - a) * xg for a, b in zip(brk[:-1], brk[1:])])
+        axes = [chk, chk, chk]
     meta = {"name": "random_cube", "params": p, "directions": ("x", "y", "z"), "default_dirichlet": _all_faces()}
     b = Basis1D(kv)
-    n = chk.size
-    idx = np.stack(np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij"), -1).reshape(-1, 3)
     for draw in range(int(p["max_draws"])):
         ctrl = base.copy()
         ctrl[1:-1, 1:-1, 1:-1] += rng.normal(0.0, p["sigma"], size=(nc - 2, nc - 2, nc - 2, 3))
         patch = GeometryPatch((b, b, b), ctrl, np.ones((nc, nc, nc)), dict(meta))
-        det = GridEvaluator(patch, [chk, chk, chk]).records(idx, check=False)[:, 12]
-        if bool((det > 0).all().item()):
+        mn, bad = GridEvaluator(patch, axes).min_det()
+        if bad == 0 and mn > 0.0:
             patch.metadata["draws"] = draw + 1
+            patch.metadata["check_points"] = int(np.prod([a.size for a in axes]))
+            patch.metadata["min_det"] = mn
             return patch
     raise GeometryError("no admissible random draw")
 

@@ -104,7 +104,7 @@ def assembly_summary(tag, c):
     kw = dict(SOLVE_CONFIGS[c])
     cfg = OI.Config(seed=0, **kw)
     t = time.perf_counter()
-    patch = OI.build_patch(cfg.geometry, cfg.geometry_params)
+    patch = OI.build_patch(cfg.geometry, OI.geometry_params(cfg))
     cfg.resolve(patch)
     disc = OI.discretize(cfg, patch)
     rK, rf = OI._seeds(cfg.seed, 2)

@@ -266,3 +266,36 @@ def test_configs2_n16_vs_oracle_fixture(record_property):
 def test_configs3_n10_vs_oracle_fixture(record_property):
     """Random cube at n=10 (operator ranks 53, f = 1, no manufactured solution)."""
     _vs_fixture("c3_n10", 3, 10, 1e-5, record_property)
+
+
+def test_random_cube_det_check_on_solve_gauss_grid(record_property):
+    """configs[3]'s admissibility check covers every Gauss point of the solve: the device min-det kernel
+    (ttb_geo_min_det) against the oracle's sum-factorized check at n=64 (244^3 points), and the full
+    n=512 grid (2036^3 = 8.4e9 points) timed, with the same draw count as the coarse-grid oracle draw."""
+    import time
+    from oracle import iga as OI
+    from oracle import patch as OP
+    from paper_2509_13224_b200 import driver as D
+    from paper_2509_13224_b200.geometry import GridEvaluator, make_geometry
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    cfg = D.SolveConfig(seed=0, **dict(SOLVE_CONFIGS[3], n_basis=64))
+    prm = D.geometry_params(cfg)
+    assert prm["check_gauss"] == [[61, 4]] * 3
+    patch = make_geometry("random_cube", prm)
+    opt = OP.build_patch("random_cube", OI.geometry_params(OI.Config(seed=0, **dict(SOLVE_CONFIGS[3], n_basis=64))))
+    assert patch.metadata["draws"] == opt.meta["draws"]
+    assert np.array_equal(patch.control_points, opt.ctrl)
+    e_min = abs(patch.metadata["min_det"] - opt.meta["min_det"]) / opt.meta["min_det"]
+    axes = [OP.gauss_grid(61, 4)] * 3
+    mn, bad = GridEvaluator(patch, axes).min_det()
+    assert bad == 0 and abs(mn - patch.metadata["min_det"]) == 0.0
+    cfg = D.SolveConfig(seed=0, **SOLVE_CONFIGS[3])
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    full = make_geometry("random_cube", D.geometry_params(cfg))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    _report(record_property, "random_cube det check", n64_min_det_rel_err=e_min, n512_points=full.metadata["check_points"],
+            n512_min_det=full.metadata["min_det"], n512_draws=full.metadata["draws"], n512_check_s=dt)
+    assert e_min <= 1e-12
+    assert full.metadata["check_points"] == 2036 ** 3 and full.metadata["min_det"] > 0

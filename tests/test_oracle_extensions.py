@@ -57,6 +57,31 @@ def test_random_cube_seeded_and_valid():
         assert a.metric(xi)[1] > 0
 
 
+def test_random_cube_min_det_sum_factorization_matches_pointwise():
+    """The sum-factorized det J grid check (used for the solve's full Gauss grid) against the per-point
+    Jacobians of the restated reference evaluator."""
+    pt = P.build_patch("random_cube", {"seed": 5, "sigma": 0.05})
+    axes = [P.gauss_grid(3, 4), P.gauss_grid(4, 3), P.gauss_grid(5, 2)]
+    mn, bad = P.min_det_polynomial_grid(pt, axes, chunk=3)
+    ev = P.TensorGridEval(pt, axes)
+    idx = np.stack(np.meshgrid(*[np.arange(a.size) for a in axes], indexing="ij"), -1).reshape(-1, 3)
+    det = np.linalg.det(ev.jac_points(idx)[0])
+    assert bad == int((det <= 0).sum())
+    assert abs(mn - det.min()) <= 1e-13 * abs(det).max()
+
+
+def test_random_cube_checks_the_solve_gauss_grid():
+    """configs[3] rejects draws on every Gauss point of the solve: the driver passes (n_basis - p, p + 1)."""
+    cfg = iga.Config(geometry="random_cube", degree=3, n_basis=10, source="one")
+    prm = iga.geometry_params(cfg)
+    assert prm["check_gauss"] == [[7, 4]] * 3
+    pt = P.build_patch("random_cube", prm)
+    assert pt.meta["check_points"] == 28 ** 3 and pt.meta["min_det"] > 0
+    # a draw far off the identity is rejected on the dense grid
+    with pytest.raises(P.PatchFault):
+        P.build_patch("random_cube", {"sigma": 0.5, "max_draws": 2, "check_gauss": [7, 4]})
+
+
 def test_exp_sines_source_is_minus_laplacian():
     rng = np.random.default_rng(3)
     x = rng.uniform(0.1, 0.9, (20, 3))

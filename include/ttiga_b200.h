@@ -128,12 +128,31 @@ int ttb_vec_core_flat(void* stream, int r, int nq, int s, const double* G, const
 /* Solution core at quadrature points: T[a,q,b] = sum_k u[a, first[q]+k, b] V[q,k]. */
 int ttb_field_table(void* stream, int r, int n, int s, const double* u, int nq, const int* first, const double* V,
                     int p, double* T);
-/* driver.l2_error integrals: out[0] = sum w det|u-u*|, out[1] = sum w det|u*| (part: 2*nq0*nq1 doubles). */
+/* driver.l2_error integrals: out[0] = sum w det|u-u*|, out[1] = sum w det|u*| (part: 2*nq0*nq1 doubles).
+ * exact_id >= 0: u* in-kernel (iga.cu exact_fn, parameters prm); exact_id = -1: prm is the table of u* at
+ * every quadrature point (nq0 x nq1 x nq2, row-major) for a user-supplied analytic function. */
 int ttb_l1_error(void* stream, const int* f0, const int* f1, const int* f2, const double* V0, const double* V1,
                  const double* V2, const double* D0, const double* D1, const double* D2, int p0, int p1, int p2,
                  int n0, int n1, int n2, const double* cw, int nq0, int nq1, int nq2, const double* U0, int r1,
                  const double* U1, int r2, const double* U2, const double* w0, const double* w1, const double* w2,
                  int exact_id, const double* prm, double* part, double* out);
+
+/* ---- classical full-grid system (reference driver.py:561-703, full_grid_reference) -------------- */
+
+/* Element-by-element stiffness and load of the tensor-product B-spline space on the device: one CTA per
+ * element accumulates the local (p+1)^3 x (p+1)^3 matrix over the element's g0 g1 g2 Gauss points and adds
+ * it into the stencil storage K (n0 n1 n2 x prod(2 p_d + 1), slot ((o0 (2p1+1) + o1)(2p2+1) + o2) for the
+ * column with per-direction offsets o_d - p_d), and the local load into f (n0 n1 n2). ne, g, p, n: host
+ * int[3] (elements, Gauss points per element, degree, basis functions per direction); s_d, V_d, D_d: the
+ * per-quadrature-point basis windows; Rw: (nq0 nq1 nq2, 9) weighted metric w R_ij; Fw: weighted f det J.
+ * K and f must be zeroed by the caller. Replaces the reference's numpy einsum + scipy COO assembly. */
+int ttb_fullgrid_assemble(void* stream, const int* ne, const int* g, const int* p, const int* n, const int* s0,
+                          const int* s1, const int* s2, const double* V0, const double* V1, const double* V2,
+                          const double* D0, const double* D1, const double* D2, const double* Rw, const double* Fw,
+                          double* K, double* f);
+/* y = M K M x on the stencil storage (M = diag(mask) selects the interior dofs; mask NULL: y = K x). */
+int ttb_stencil_spmv(void* stream, int n0, int n1, int n2, int p0, int p1, int p2, const double* K, const double* x,
+                     const unsigned char* mask, double* y);
 
 /* ---- TT operator kernels (tensor_train/core.py:327-338, tensor_train/amen.py:51-193) ----------- */
 

@@ -48,6 +48,8 @@ SIGNATURES = {
                            i32, i32, i32, i32, vp, vp]),
     "ttb_geo_min_det": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp,
                               vp]),
+    "ttb_fullgrid_assemble": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ttb_stencil_spmv": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ttb_op_core": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]),
     "ttb_vec_core": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, i32, i32, vp]),
     "ttb_op_core_flat": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]),

@@ -513,7 +513,7 @@ __global__ void l1err_kernel(GeoArgs g, int nq0, int nq1, int nq2, const double*
     for (int c = 0; c < r2; ++c) u += Tsh[c] * U2[(long long)c * nq2 + q2];
     GeoOut o;
     geo_point(g, q0, q1, q2, o);
-    const double ue = exact_fn(exact_id, o.x, prm);
+    const double ue = exact_id < 0 ? prm[((long long)q0 * nq1 + q1) * nq2 + q2] : exact_fn(exact_id, o.x, prm);
     const double wd = w01 * w2[q2] * o.det;
     num += wd * fabs(u - ue);
     den += wd * fabs(ue);

@@ -8,6 +8,7 @@ fused kernel over the whole tensor quadrature grid.
 
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 import json
 import math
@@ -24,10 +25,12 @@ from ._lib import call, device, ptr
 from .assembly import (BoundarySpec, Discretization, FaceCondition, apply_dirichlet, assemble_load, assemble_stiffness,
                        build_quadrature)
 from .geometry import SOURCE_IDS, GeometryPatch, make_geometry
+from .pointfn import PointFn, builtin_sources, on_device
 from .splines import Basis1D, KnotVector, basis_windows, eval_basis
 from .tensor_train import AmenOptions, TtMatrix, TtTensor, amen_solve, tt_add, tt_round
 
-__all__ = ["DriverError", "SolveConfig", "SolutionReport", "SOURCES", "ANALYTIC", "solve_poisson", "l2_error",
+__all__ = ["DriverError", "OracleRefusedError", "FullGridResult", "full_grid_reference", "FULL_GRID_DOF_GUARD",
+           "SolveConfig", "SolutionReport", "SOURCES", "ANALYTIC", "solve_poisson", "l2_error",
            "compression_ratio", "evaluate_field", "solution_basis", "fit_slope", "field_on_grid"]
 
 
@@ -35,24 +38,41 @@ class DriverError(ValueError):
     """Invalid solve configuration (reference driver.py:69)."""
 
 
-SOURCES = tuple(SOURCE_IDS)
+class OracleRefusedError(RuntimeError):
+    """Full-grid reference refused: problem exceeds the dof guard (reference driver.py:73)."""
+
+
+FULL_GRID_DOF_GUARD = 1_000_000
+
+
+# name -> source term f(x): the reference's numpy lambdas (driver.py:80-98) as PointFn objects that the
+# load kernel evaluates in-kernel by id (pointfn.py); SOURCES["one"](numpy points) works as in the reference
+SOURCES = builtin_sources(SOURCE_IDS)
 
 
 def _t_sines(x):
     return torch.sin(math.pi * x[:, 0]) * torch.sin(math.pi * x[:, 1]) * torch.sin(math.pi * x[:, 2])
 
 
+def _np_sines(x):
+    return np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1]) * np.sin(np.pi * x[:, 2])
+
+
+# analytic solutions (reference driver.py:101-149): factories (cfg, patch) -> u(points), here PointFn
+# objects carrying the l1err_kernel id and parameters (exact_fn in iga.cu) and the numpy/torch versions
 def _an_lshape(cfg, patch):
-    return (0, (0.0, 0.0, 1.0, 1.0),
-            lambda x: torch.sin(math.pi * x[:, 0]) * torch.sin(math.pi * x[:, 1]) / (2.0 * math.pi ** 2))
+    return PointFn(lambda x: np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1]) / (2.0 * np.pi ** 2),
+                   lambda x: torch.sin(math.pi * x[:, 0]) * torch.sin(math.pi * x[:, 1]) / (2.0 * math.pi ** 2),
+                   name="lshape_exact", analytic_id=0, params=(0.0, 0.0, 1.0, 1.0))
 
 
 def _an_cube(cfg, patch):
-    return 1, (0.0, 0.0, 1.0, 1.0), _t_sines
+    return PointFn(_np_sines, _t_sines, name="cube_sines", analytic_id=1, params=(0.0, 0.0, 1.0, 1.0))
 
 
 def _an_exp(cfg, patch):
-    return 3, (0.0, 0.0, 1.0, 1.0), lambda x: torch.exp(x.sum(1)) * _t_sines(x)
+    return PointFn(lambda x: np.exp(x.sum(1)) * _np_sines(x), lambda x: torch.exp(x.sum(1)) * _t_sines(x),
+                   name="exp_sines", analytic_id=3, params=(0.0, 0.0, 1.0, 1.0))
 
 
 def _an_ring(cfg, patch):
@@ -70,7 +90,11 @@ def _an_ring(cfg, patch):
         r = torch.hypot(x[:, 0], x[:, 1])
         return (ui * torch.log(ro / r) + uo * torch.log(r / ri)) / math.log(ro / ri)
 
-    return 2, (ui, uo, ri, ro), u
+    def u_np(x):
+        r = np.hypot(x[:, 0], x[:, 1])
+        return (ui * np.log(ro / r) + uo * np.log(r / ri)) / np.log(ro / ri)
+
+    return PointFn(u_np, u, name="ring_radial", analytic_id=2, params=(ui, uo, ri, ro))
 
 
 ANALYTIC = {"lshape_exact": _an_lshape, "cube_sines": _an_cube, "ring_radial": _an_ring, "exp_sines": _an_exp}
@@ -126,7 +150,7 @@ class SolveConfig:
             if self.bc_from_analytic:
                 if self.analytic is None:
                     raise DriverError("bc_from_analytic needs an analytic solution")
-                fn = ANALYTIC[self.analytic](self, patch)[2]
+                fn = ANALYTIC[self.analytic](self, patch)
                 self.bc = BoundarySpec({(int(a), int(s)): FaceCondition("dirichlet", fn)
                                         for a, s in patch.metadata.get("default_dirichlet", [])},
                                        allow_adjacent_nonzero=True)
@@ -242,9 +266,9 @@ def _field_tables(disc: Discretization, u: TtTensor):
 def l2_error(u: TtTensor, analytic, patch: GeometryPatch, disc: Discretization) -> float:
     """Reference l2_error (driver.py:388-422) as one device pass over the quadrature grid.
 
-    ``analytic`` is the (id, params, fn) triple returned by an ANALYTIC factory.
-    """
-    exact_id, prm, _ = analytic
+    ``analytic``: the PointFn an ANALYTIC factory returns (evaluated inside l1err_kernel by id) or any
+    reference-style numpy callable of physical points (tabulated once at the quadrature points through
+    the host bridge, pointfn.on_device)."""
     from .geometry import GridEvaluator
     ev = GridEvaluator(patch, disc.quad_axes())
     U0, U1, U2 = _field_tables(disc, u)
@@ -252,7 +276,16 @@ def l2_error(u: TtTensor, analytic, patch: GeometryPatch, disc: Discretization) 
     (f0, V0, D0), (f1, V1, D1), (f2, V2, D2) = ev.win
     p = patch.degrees
     n = ev.cw.shape[:3]
-    prm_t = torch.as_tensor(np.asarray(prm, dtype=np.float64), device=device())
+    if isinstance(analytic, PointFn) and analytic.analytic_id is not None:
+        exact_id = analytic.analytic_id
+        prm_t = torch.as_tensor(np.asarray(analytic.params, dtype=np.float64), device=device())
+    elif callable(analytic):
+        exact_id = -1                                   # table of exact values at every quadrature point
+        idx = torch.stack(torch.meshgrid(*[torch.arange(k, device=device()) for k in nq], indexing="ij"),
+                          -1).reshape(-1, 3)
+        prm_t = on_device(analytic)(ev.points(idx)).to(torch.float64).contiguous()
+    else:
+        raise DriverError("analytic must be a callable of physical points")
     part = L.empty(2 * nq[0] * nq[1])
     out = L.empty(2)
     w = [t.w_dev for t in disc.tables]
@@ -358,3 +391,132 @@ def solve_poisson(cfg: SolveConfig, want_error: bool = True) -> SolutionReport:
                          compression_u=compression_ratio(u_full), timings=timings, sweeps=result.sweeps)
     rep.K, rep.f, rep.system, rep.disc, rep.patch = K, f, system, disc, patch
     return rep
+
+
+# ---------------------------------------------------------------------------
+# classical full-grid anchor (reference driver.py:535-703)
+
+@dataclass
+class FullGridResult:
+    """Reference FullGridResult (driver.py:535-544): K as a scipy CSR matrix and f, u as numpy arrays over
+    the full coefficient space (boundary coefficients included), like the reference's."""
+
+    K: object
+    f: np.ndarray
+    u: np.ndarray
+    mode_sizes: tuple
+    l2_error: float | None = None
+
+
+def _stencil_to_csr(Kst, sizes, p):
+    """Stencil storage (n_dofs, prod(2p_d+1)) -> scipy CSR (host; only for the API's return value)."""
+    import scipy.sparse as sp
+    K = Kst.cpu().numpy()
+    n0, n1, n2 = sizes
+    I = np.arange(n0 * n1 * n2).reshape(n0, n1, n2)
+    rows, cols, vals = [], [], []
+    w1, w2 = 2 * p[1] + 1, 2 * p[2] + 1
+    for o0 in range(-p[0], p[0] + 1):
+        for o1 in range(-p[1], p[1] + 1):
+            for o2 in range(-p[2], p[2] + 1):
+                sl_i = tuple(slice(max(0, -o), n - max(0, o)) for o, n in zip((o0, o1, o2), sizes))
+                sl_j = tuple(slice(max(0, o), n - max(0, -o)) for o, n in zip((o0, o1, o2), sizes))
+                ri, cj = I[sl_i].ravel(), I[sl_j].ravel()
+                v = K[ri, ((o0 + p[0]) * w1 + (o1 + p[1])) * w2 + (o2 + p[2])]
+                keep = v != 0.0
+                rows.append(ri[keep])
+                cols.append(cj[keep])
+                vals.append(v[keep])
+    nd = n0 * n1 * n2
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(nd, nd)).tocsr()
+
+
+def full_grid_reference(cfg: SolveConfig) -> FullGridResult:
+    """Classical IGA assembly and solve with the same quadrature (reference driver.py:561-703), on the device:
+    Gauss-point metric and load from the geometry kernel, element-by-element stiffness/load into a stencil
+    array (ttb_fullgrid_assemble), Dirichlet lift from the same Greville face interpolation as the TT path,
+    and a Jacobi-preconditioned CG on the interior (ttb_stencil_spmv) to a relative residual of 1e-14 (the
+    reference: scipy spsolve up to 50k interior dofs, CG at rtol 1e-12 above). Refuses above the dof guard,
+    as the reference does: this path is the one the TT pipeline exists to avoid."""
+    from .assembly import _face_coefficients
+    from .geometry import GridEvaluator
+    from .tensor_train import tt_from_full
+    patch = make_geometry(cfg.geometry, cfg.geometry_params)
+    cfg.resolve_bc(patch)
+    bases = tuple(solution_basis(patch.bases[d], cfg.degree[d], cfg.elements[d]) for d in range(3))
+    disc = build_quadrature(bases, cfg.n_gauss)
+    sizes = disc.mode_sizes
+    n_dofs = disc.n_dofs
+    if n_dofs > FULL_GRID_DOF_GUARD:
+        raise OracleRefusedError(f"full-grid oracle refused: {n_dofs} dofs exceed the {FULL_GRID_DOF_GUARD} guard")
+    dev = device()
+    nq = disc.quad_shape
+    g = disc.n_gauss
+    ne = tuple(nq[d] // g[d] for d in range(3))
+    p = tuple(b.degree for b in bases)
+    ev = GridEvaluator(patch, disc.quad_axes())
+    idx = torch.stack(torch.meshgrid(*[torch.arange(k, device=dev) for k in nq], indexing="ij"), -1).reshape(-1, 3)
+    rec = ev.records(idx)                                        # raises on a singular map, as the reference
+    w = [t.w_dev for t in disc.tables]
+    wq = (w[0][:, None, None] * w[1][None, :, None] * w[2][None, None, :]).reshape(-1)
+    Rw = (rec[:, 13:] * wq[:, None]).contiguous()
+    Fw = (ev.source_times_det(idx, cfg.source) * wq).contiguous()
+    S = (2 * p[0] + 1) * (2 * p[1] + 1) * (2 * p[2] + 1)
+    Kst = L.zeros(n_dofs, S)
+    fvec = L.zeros(n_dofs)
+    i3 = lambda v: (C.c_int * 3)(*[int(x) for x in v])          # noqa: E731
+    tb = disc.tables
+    call("ttb_fullgrid_assemble", i3(ne), i3(g), i3(p), i3(sizes), ptr(tb[0].starts), ptr(tb[1].starts),
+         ptr(tb[2].starts), ptr(tb[0].vals), ptr(tb[1].vals), ptr(tb[2].vals), ptr(tb[0].ders), ptr(tb[1].ders),
+         ptr(tb[2].ders), ptr(Rw), ptr(Fw), ptr(Kst), ptr(fvec))
+    # Dirichlet elimination mirroring the TT path (reference _dense_lift, driver.py:547-558)
+    lift = L.zeros(*sizes)
+    for axis, side in cfg.bc.dirichlet_faces():
+        fc = cfg.bc.condition(axis, side)
+        if fc.is_zero():
+            continue
+        sl = [slice(None)] * 3
+        sl[axis] = 0 if side == 0 else sizes[axis] - 1
+        lift[tuple(sl)] = _face_coefficients(patch, disc, cfg.bc, axis, side)
+    lift = lift.reshape(-1)
+    mask_b = torch.zeros(sizes, dtype=torch.bool, device=dev)
+    mask_b[tuple(cfg.bc.interior_slices(sizes))] = True
+    mask = mask_b.reshape(-1).to(torch.uint8).contiguous()
+
+    def spmv(x, m=None):
+        y = L.empty(n_dofs)
+        call("ttb_stencil_spmv", sizes[0], sizes[1], sizes[2], p[0], p[1], p[2], ptr(Kst), ptr(x), ptr(m), ptr(y))
+        return y
+
+    mf = mask.to(torch.float64)
+    b = (fvec - spmv(lift)) * mf
+    diag = Kst[:, S // 2]
+    dinv = torch.where(mask.bool(), 1.0 / torch.where(diag != 0, diag, torch.ones_like(diag)), torch.zeros_like(diag))
+    x = L.zeros(n_dofs)
+    r = b.clone()
+    z = dinv * r
+    pv = z.clone()
+    rz = torch.dot(r, z)
+    bnorm = float(torch.linalg.vector_norm(b).item())
+    converged = bnorm == 0.0
+    it = 0
+    while not converged and it < 20_000:
+        Ap = spmv(pv, mask)
+        alpha = rz / torch.dot(pv, Ap)
+        x += alpha * pv
+        r -= alpha * Ap
+        it += 1
+        if it % 10 == 0 and float(torch.linalg.vector_norm(r).item()) <= 1e-14 * bnorm:
+            converged = True
+            break
+        z = dinv * r
+        rz_new = torch.dot(r, z)
+        pv = z + (rz_new / rz) * pv
+        rz = rz_new
+    if not converged:
+        raise RuntimeError("full-grid CG failed to converge")
+    u = lift + x
+    err = None
+    if cfg.analytic is not None:
+        err = l2_error(tt_from_full(u.reshape(sizes), 1e-14), ANALYTIC[cfg.analytic](cfg, patch), patch, disc)
+    return FullGridResult(_stencil_to_csr(Kst, sizes, p), fvec.cpu().numpy(), u.cpu().numpy(), sizes, err)

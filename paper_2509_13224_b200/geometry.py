@@ -17,6 +17,7 @@ import numpy as np
 import torch
 
 from . import linalg as L
+from .pointfn import on_device
 from ._lib import call, device, ptr
 from .splines import Basis1D, KnotVector, basis_windows
 
@@ -87,15 +88,19 @@ class GeometryPatch:
 
     def eval_point(self, xi) -> np.ndarray:
         ev = GridEvaluator(self, [[float(x)] for x in xi])
-        return ev.points(np.zeros((1, 3), dtype=np.int64))[0].cpu().numpy()
+        return ev.points(np.zeros((1, 3), dtype=np.int64))[0]
 
     def eval_metric(self, xi) -> MetricSample:
+        """One point (reference geometry.py:103-114): J from the device evaluator, det / metric from it on the
+        host exactly as the reference forms them (det = np.linalg.det(J))."""
         ev = GridEvaluator(self, [[float(x)] for x in xi])
-        rec = ev.records(np.zeros((1, 3), dtype=np.int64), check=False)[0].cpu().numpy()
-        det = float(rec[12])
+        jac = ev.records(np.zeros((1, 3), dtype=np.int64), check=False)[0, :9].reshape(3, 3)
+        det = float(np.linalg.det(jac))
         if abs(det) < 1e-12 * self.scale ** 3:
             raise SingularMapError(f"singular geometry map at xi={tuple(xi)}")
-        return MetricSample(rec[:9].reshape(3, 3), det, rec[13:].reshape(3, 3))
+        inv = np.linalg.inv(jac)
+        metric = inv @ inv.T * det
+        return MetricSample(jac, det, 0.5 * (metric + metric.T))
 
 
 class GridEvaluator:
@@ -145,19 +150,32 @@ class GridEvaluator:
         bits = key ^ (1 << 63) if key >> 63 else (~key) & ((1 << 64) - 1)
         return float(np.frombuffer(np.uint64(bits).tobytes(), dtype=np.float64)[0]), bad
 
+    # Public evaluation methods mirror the reference's array types: numpy (or list) indices -> numpy
+    # results (reference GridEvaluator, geometry.py:150-261); a CUDA int64 index tensor -> CUDA tensors
+    # (the device path every internal caller takes).
+    @staticmethod
+    def _host(idx):
+        return not isinstance(idx, torch.Tensor)
+
+    @staticmethod
+    def _ret(x, host):
+        return x.cpu().numpy() if host else x
+
     def records(self, idx, check=True):
-        """(N, 22) device records: J (9), x (3), det, R (9)."""
+        """(N, 22) records: J (9), x (3), det, R (9)."""
+        host = self._host(idx)
         N = len(idx)
         out = L.empty(N, 22)
         idx, bad = self._launch(idx, 2, out)
         if check:
             self._raise_if_bad(idx, bad)
-        return out
+        return self._ret(out, host)
 
     def points(self, idx):
+        host = self._host(idx)
         out = L.empty(len(idx), 3)
         self._launch(idx, 3, out)
-        return out
+        return self._ret(out, host)
 
     def jacobians(self, idx):
         rec = self.records(idx, check=False)
@@ -169,20 +187,26 @@ class GridEvaluator:
 
     def metric_entry(self, idx, i, j, check=True):
         """R[:, i, j] only (cross oracle of assembly.metric_oracle)."""
+        host = self._host(idx)
         out = L.empty(len(idx))
         idx, bad = self._launch(idx, 0, out, ri=i, rj=j)
         if check:
             self._raise_if_bad(idx, bad)
-        return out
+        return self._ret(out, host)
 
     def source_times_det(self, idx, source):
-        """f(x(xi)) det J (assembly.load_oracle); ``source`` is a SOURCE_IDS name or a torch callable."""
-        if isinstance(source, str):
+        """f(x(xi)) det J (assembly.load_oracle). ``source``: a SOURCE_IDS name or a built-in PointFn
+        (evaluated inside geo_kernel), or any callable of physical points (numpy semantics, bridged)."""
+        host = self._host(idx)
+        name = source if isinstance(source, str) else getattr(source, "name", None)
+        if name in SOURCE_IDS and (isinstance(source, str) or getattr(source, "source_id", None) is not None):
             out = L.empty(len(idx))
-            self._launch(idx, 1, out, src=SOURCE_IDS[source])
-            return out
+            self._launch(idx, 1, out, src=SOURCE_IDS[name])
+            return self._ret(out, host)
         rec = self.records(idx, check=False)
-        return source(rec[:, 9:12]) * rec[:, 12]
+        if host:
+            return np.asarray(source(rec[:, 9:12]), dtype=float) * rec[:, 12]
+        return on_device(source)(rec[:, 9:12]) * rec[:, 12]
 
 
 # ---------------------------------------------------------------------------

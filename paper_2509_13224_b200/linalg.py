@@ -603,8 +603,17 @@ def maxvol_colmajor(Qcm, n, r, tol=1.01, max_iters=200):
 
 
 def maxvol(M, tol=1.01, max_iters=200):
-    """Reference maxvol(M) for a row-major (n x r) device matrix."""
+    """Reference maxvol(M) (tensor_train/maxvol.py:37-62): sorted row indices (host int64 array) of a
+    row-major (n x r) matrix -- a CUDA tensor, or a numpy array / nested list as in the reference (copied
+    to the device once)."""
+    if not isinstance(M, torch.Tensor):
+        M = np.asarray(M, dtype=float)
+        if M.ndim != 2:
+            raise ValueError("maxvol expects a matrix")
+        M = torch.as_tensor(M, device=device())
+    if M.dim() != 2:
+        raise ValueError("maxvol expects a matrix")
     n, r = M.shape
     if tol < 1.0:
         raise ValueError("tol must be at least 1")
-    return maxvol_colmajor(permute(M, (1, 0)), n, r, tol, max_iters)
+    return maxvol_colmajor(permute(M.to(F64).contiguous(), (1, 0)), n, r, tol, max_iters)

@@ -35,6 +35,23 @@ def to_device(x):
     return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=device())
 
 
+class DeviceCore(torch.Tensor):
+    """A TT core in device memory that numpy can read: ``np.asarray(core)`` copies it to the host, so
+    reference-style code that compares cores with numpy (np.array_equal / np.allclose on ``t.cores[k]``,
+    the reference's cores being numpy arrays) keeps working. Torch operations see a plain CUDA tensor
+    (``__torch_function__`` disabled: no dispatch overhead, results are ordinary tensors)."""
+
+    __torch_function__ = torch._C._disabled_torch_function_impl
+
+    def __array__(self, dtype=None, copy=None):
+        a = torch.Tensor.cpu(self).numpy()
+        return a if dtype is None else a.astype(dtype, copy=False)
+
+
+def _core(G):
+    return to_device(G).contiguous().as_subclass(DeviceCore)
+
+
 def _check_chain(cores, order):
     if not cores:
         raise TtShapeError("empty core list")
@@ -52,7 +69,7 @@ class TtTensor:
     """Chain of (r_{k-1}, n_k, r_k) device cores (reference core.py:54-146)."""
 
     def __init__(self, cores):
-        self.cores = [to_device(G).contiguous() for G in cores]
+        self.cores = [_core(G) for G in cores]
         _check_chain(self.cores, 3)
 
     d = property(lambda s: len(s.cores))
@@ -94,8 +111,11 @@ class TtTensor:
         return self.full_device().cpu().numpy()
 
     def gather(self, idx):
-        """Entries at multi-indices idx (N, d) -> device (N,) (reference core.py:118-124)."""
-        idx = torch.as_tensor(idx, dtype=torch.int64, device=device()).contiguous()
+        """Entries at multi-indices idx (N, d) (reference core.py:118-124): a CUDA index tensor gives a CUDA
+        (N,) tensor, numpy / list indices a numpy array (the reference's types)."""
+        if not isinstance(idx, torch.Tensor):
+            return self.gather(torch.as_tensor(np.asarray(idx), dtype=torch.int64, device=device())).cpu().numpy()
+        idx = idx.to(device=device(), dtype=torch.int64).contiguous()
         if self.d != 3:
             v = self.cores[0][0, idx[:, 0], :]
             for k in range(1, self.d):
@@ -124,7 +144,7 @@ class TtMatrix:
     """Chain of operator cores (reference core.py:149-221), dense or banded (``band`` = h)."""
 
     def __init__(self, cores, band=None, col_sizes=None):
-        self.cores = [to_device(G).contiguous() for G in cores]
+        self.cores = [_core(G) for G in cores]
         self.band = None if band is None else int(band)
         _check_chain(self.cores, 4)
         if self.band is not None:

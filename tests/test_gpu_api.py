@@ -58,12 +58,12 @@ def test_maxvol_validation(M):
 
 def test_cross_constant_and_noise(M):
     res = M.tt.tt_cross(M.tt.CrossOracle(lambda idx: torch.full((idx.shape[0],), 3.5, dtype=torch.float64,
-                                                                   device="cuda"), (8, 8, 8)),
+                                                                   device="cuda"), (8, 8, 8), device=True),
                         1e-10, rng=np.random.default_rng(2))
     assert res.ranks == (1, 1, 1, 1) and np.abs(res.tensor.full() - 3.5).max() < 1e-12
     g = torch.Generator(device="cuda").manual_seed(5)
     noisy = M.tt.CrossOracle(lambda idx: 1e-16 * torch.randn(idx.shape[0], dtype=torch.float64, device="cuda",
-                                                             generator=g), (12, 12, 12))
+                                                             generator=g), (12, 12, 12), device=True)
     res = M.tt.tt_cross(noisy, 1e-10, rng=np.random.default_rng(6), scale=1.0)
     assert res.ranks == (1, 1, 1, 1) and np.all(res.tensor.full() == 0.0) and res.converged
 
@@ -145,3 +145,31 @@ def test_spline_errors_and_singular_map(M):
     hemi = M.geo.make_geometry("closed_hemisphere")
     with pytest.raises(M.geo.SingularMapError):
         hemi.eval_metric(np.array([0.3, 1.0, 0.5]))  # pole face: det J = 0
+
+
+def test_full_grid_reference_anchor():
+    """The classical full-grid system (reference driver.py:561-703) on the device: the trilinear element
+    stiffness pattern of the reference's own test, and TT solve == full-grid solve on the ring."""
+    from paper_2509_13224_b200 import driver as D
+    from paper_2509_13224_b200.assembly import BoundarySpec, FaceCondition
+    cfg = D.SolveConfig(geometry="unit_cube", degree=1, elements=1, source="one", seed=0,
+                        bc=BoundarySpec({(0, 0): FaceCondition("dirichlet", 0.0)}))
+    ref = D.full_grid_reference(cfg)
+    dense = ref.K.toarray()
+    nodes = [(i, j, k) for i in range(2) for j in range(2) for k in range(2)]
+    pattern = {0: 1 / 3, 1: 0.0, 2: -1 / 12, 3: -1 / 12}
+    for a, na in enumerate(nodes):
+        for b, nb in enumerate(nodes):
+            assert abs(dense[a, b] - pattern[sum(x != y for x, y in zip(na, nb))]) < 1e-12
+    kw = dict(geometry="ring", degree=2, elements=4, source="sin_pi_xyz", seed=0)
+    rep = D.solve_poisson(D.SolveConfig(**kw))
+    ref = D.full_grid_reference(D.SolveConfig(**kw))
+    u = rep.u.full().ravel()
+    diff = np.linalg.norm(u - ref.u) / np.linalg.norm(ref.u)
+    K = rep.K.full().reshape(ref.K.shape)
+    eK = np.linalg.norm(K - ref.K.toarray()) / np.linalg.norm(ref.K.toarray())
+    ef = np.linalg.norm(rep.f.full().ravel() - ref.f) / np.linalg.norm(ref.f)
+    print(f"full-grid anchor (ring, p=2, 4 el.): K {eK:.2e}, f {ef:.2e}, u {diff:.2e}")
+    assert eK <= 1e-9 and ef <= 1e-9 and diff <= 10 * rep.config.eps_solve
+    with pytest.raises(D.OracleRefusedError):
+        D.full_grid_reference(D.SolveConfig(geometry="unit_cube", degree=1, elements=128, seed=0))

@@ -44,12 +44,15 @@ def test_geometry_vs_golden(P, golden, name):
     assert np.allclose(patch.control_points, g[f"{name}_ctrl"], atol=1e-15)
     ev = P.geo.GridEvaluator(patch, list(g[f"{name}_axes"]))
     idx = g[f"{name}_idx"]
-    J, x = ev.jacobians(idx)
+    J, x = ev.jacobians(idx)          # numpy indices -> numpy results (reference array types)
     det, R = ev.metric(idx)
-    assert np.abs(J.cpu().numpy() - g[f"{name}_jac"]).max() <= 1e-13
-    assert np.abs(x.cpu().numpy() - g[f"{name}_pts"]).max() <= 1e-14
-    assert np.abs(det.cpu().numpy() - g[f"{name}_det"]).max() <= 1e-13
-    assert np.abs(R.cpu().numpy() - g[f"{name}_R"]).max() <= 1e-12
+    assert isinstance(J, np.ndarray) and isinstance(R, np.ndarray)
+    Jd, _ = ev.jacobians(torch.as_tensor(idx, device="cuda"))    # device path: CUDA in, CUDA out
+    assert Jd.is_cuda and np.array_equal(Jd.cpu().numpy(), J)
+    assert np.abs(J - g[f"{name}_jac"]).max() <= 1e-13
+    assert np.abs(x - g[f"{name}_pts"]).max() <= 1e-14
+    assert np.abs(det - g[f"{name}_det"]).max() <= 1e-13
+    assert np.abs(R - g[f"{name}_R"]).max() <= 1e-12
 
 
 @pytest.mark.parametrize("name", ["quarter_cylinder", "deformed_cube", "random_cube"])
@@ -63,8 +66,8 @@ def test_extension_geometries_vs_oracle(P, name):
     idx = rng.integers(0, 9, (200, 3))
     det_o, R_o = OP.TensorGridEval(op, axes).det_metric(idx)
     det, R = P.geo.GridEvaluator(gp, axes).metric(idx)
-    assert np.abs(det.cpu().numpy() - det_o).max() <= 1e-12
-    assert np.abs(R.cpu().numpy() - R_o).max() <= 1e-11
+    assert np.abs(det - det_o).max() <= 1e-12
+    assert np.abs(R - R_o).max() <= 1e-11
 
 
 # ---------------------------------------------------------------- tensor train
@@ -127,7 +130,7 @@ def test_cross_vs_golden(P, golden):
         return (torch.sin(x[:, 0] + 1.0) * torch.cos(0.3 * x[:, 1]) * (x[:, 2] + 1.0)
                 + torch.exp(-0.1 * x[:, 0]) * (x[:, 1] + 0.5) * torch.cos(0.2 * x[:, 2]))
 
-    res = P.tt.tt_cross(P.tt.CrossOracle(f, n), 1e-10, rng=np.random.default_rng(7))
+    res = P.tt.tt_cross(P.tt.CrossOracle(f, n, device=True), 1e-10, rng=np.random.default_rng(7))
     assert res.ranks == tuple(g["cross_ranks"])
     assert res.n_evals == int(g["cross_nevals"])
     assert rel(res.tensor.full(), g["cross_ref"]) <= 1e-9
@@ -139,7 +142,7 @@ def test_cross_separable_exact(P):
         x = idx.to(torch.float64)
         return torch.exp(-0.3 * x[:, 0]) * (x[:, 1] + 1.0) * torch.cos(x[:, 2])
 
-    res = P.tt.tt_cross(P.tt.CrossOracle(f, (16, 16, 16)), 1e-10, rng=np.random.default_rng(4))
+    res = P.tt.tt_cross(P.tt.CrossOracle(f, (16, 16, 16), device=True), 1e-10, rng=np.random.default_rng(4))
     grid = np.indices((16, 16, 16)).reshape(3, -1).T
     ref = (np.exp(-0.3 * grid[:, 0]) * (grid[:, 1] + 1.0) * np.cos(grid[:, 2])).reshape(16, 16, 16)
     assert res.ranks == (1, 1, 1, 1)

@@ -616,6 +616,95 @@ __global__ void __launch_bounds__(256) min_det_kernel(GeoArgs g, int n0, int n1,
   }
 }
 
+// Sum-factorized variant (n2 <= 64 control points in the last direction): one warp per (q0, q1) line
+// contracts the first two directions once -- W_v[c][comp] = sum_{a,b} X0_a X1_b cw[f0+a][f1+b][c][comp]
+// for (X0, X1) = (N0, N1), (D0, N1), (N0, D1) over every c -- and then every point of the line needs
+// only (p2 + 1) terms per quantity: ~90 FMA per point instead of the ~1000 FMA and 2 KB of window loads
+// of geo_point (1.47 s -> ~0.1 s for the 8.4e9-point configs[3] grid).
+constexpr int MD_MAXC = 64;
+__global__ void __launch_bounds__(256) min_det_sf_kernel(GeoArgs g, int n0q, int n1q, int n2q, unsigned long long* minkey,
+                                                         unsigned long long* count) {
+  __shared__ double Wsh[8][3][MD_MAXC * 4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long lines = (long long)n0q * n1q;
+  const int nc = g.n[2];
+  const int p0 = g.p[0] + 1, p1 = g.p[1] + 1, p2 = g.p[2] + 1;
+  double mn = 1.0e308;
+  unsigned long long cnt = 0;
+  double (*W)[MD_MAXC * 4] = Wsh[w];
+  for (long long line = blockIdx.x * 8LL + w; line < lines; line += (long long)gridDim.x * 8) {
+    const int q0 = (int)(line / n1q), q1 = (int)(line % n1q);
+    const int f0 = g.first[0][q0], f1 = g.first[1][q1];
+    const double* V0 = g.V[0] + (long long)q0 * p0;
+    const double* D0 = g.D[0] + (long long)q0 * p0;
+    const double* V1 = g.V[1] + (long long)q1 * p1;
+    const double* D1 = g.D[1] + (long long)q1 * p1;
+    for (int e = lane; e < nc * 4; e += 32) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int a = 0; a < p0; ++a) {
+        const double va = V0[a], da = D0[a];
+        double t0 = 0.0, t1 = 0.0;
+        for (int b = 0; b < p1; ++b) {
+          const double x = g.cw[((long long)(f0 + a) * g.n[1] + (f1 + b)) * nc * 4 + e];
+          t0 += V1[b] * x;
+          t1 += D1[b] * x;
+        }
+        s0 += va * t0;
+        s1 += da * t0;
+        s2 += va * t1;
+      }
+      W[0][e] = s0;
+      W[1][e] = s1;
+      W[2][e] = s2;
+    }
+    __syncwarp();
+    for (int q2 = lane; q2 < n2q; q2 += 32) {
+      const int f2 = g.first[2][q2];
+      const double* V2 = g.V[2] + (long long)q2 * p2;
+      const double* D2 = g.D[2] + (long long)q2 * p2;
+      double S[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) S[u][cc] = 0.0;
+      for (int c = 0; c < p2; ++c) {
+        const double vc = V2[c], dc = D2[c];
+        const double* w0 = W[0] + (f2 + c) * 4;
+        const double* w1 = W[1] + (f2 + c) * 4;
+        const double* w2 = W[2] + (f2 + c) * 4;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          S[0][cc] += vc * w0[cc];
+          S[1][cc] += vc * w1[cc];
+          S[2][cc] += vc * w2[cc];
+          S[3][cc] += dc * w0[cc];
+        }
+      }
+      const double den = S[0][3];
+      const double inv2 = 1.0 / (den * den);
+      double J[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) J[c][e] = (S[1 + e][c] * den - S[0][c] * S[1 + e][3]) * inv2;
+      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      mn = fmin(mn, det);
+      cnt += (det <= 0.0);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  }
+  if (lane == 0) {
+    atomicMin(minkey, dkey(mn));
+    if (cnt) atomicAdd(count, cnt);
+  }
+}
+
 TTB_API int ttb_geo_min_det(void* stream, int nq0, int nq1, int nq2, const int* f0, const int* f1, const int* f2,
                             const double* V0, const double* V1, const double* V2, const double* D0, const double* D1,
                             const double* D2, int p0, int p1, int p2, int n0, int n1, int n2, const double* cw,
@@ -633,6 +722,12 @@ TTB_API int ttb_geo_min_det(void* stream, int nq0, int nq1, int nq2, const int* 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long N = (long long)nq0 * nq1 * nq2;
+  if (n2 <= MD_MAXC) {
+    long long blocks = ((long long)nq0 * nq1 + 7) / 8;
+    if (blocks > 16LL * sms) blocks = 16LL * sms;
+    min_det_sf_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, nq0, nq1, nq2, out, out + 1); ttb_count();
+    return ttb_last_error();
+  }
   long long blocks = (N + 255) / 256;
   if (blocks > 8LL * sms) blocks = 8LL * sms;
   min_det_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, nq0, nq1, nq2, out, out + 1); ttb_count();

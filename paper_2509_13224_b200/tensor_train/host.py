@@ -28,25 +28,119 @@ from .core import TtShapeError, _chop, _rl_orthogonalize
 __all__ = ["tt_matvec_round_host"]
 
 
-def _pinned(t):
+def _host(t):
+    """A host core as a contiguous CPU float64 tensor (numpy arrays are wrapped, not copied)."""
     t = torch.as_tensor(t, dtype=torch.float64)
     if t.device.type != "cpu":
         raise ValueError("host cores expected")
-    t = t.contiguous()
-    return t if t.is_pinned() else t.pin_memory()
+    return t.contiguous()
+
+
+_STAGE_BYTES = 32 << 20    # pinned staging buffer size
+_STAGE_N = 6               # staging ring depth
+_stage_ring = None
+
+
+def _ring():
+    global _stage_ring
+    if _stage_ring is None:
+        _stage_ring = [torch.empty(_STAGE_BYTES // 8, dtype=torch.float64).pin_memory() for _ in range(_STAGE_N)]
+    return _stage_ring
+
+
+class _Uploader:
+    """Host -> device copies on the copy stream, in submission order, from a worker thread.
+
+    Pinned sources go straight to a DMA. Pageable sources (the numpy arrays a reference caller holds)
+    are staged through a ring of pinned buffers: the worker copies chunk i into buffer i % R (a
+    parallel CPU copy that releases the GIL) and queues its H2D, waiting for the buffer's previous DMA
+    before reusing it -- so the memcpy of chunk i + 1 overlaps the DMA of chunk i, and both overlap the
+    device work the main thread is launching meanwhile. ``submit`` returns a token; ``wait(token)``
+    makes the compute stream wait for that copy."""
+
+    def __init__(self, copy_stream):
+        import queue
+        import threading
+        self.copy = copy_stream
+        self.jobs = queue.Queue()
+        self.done = {}
+        self.cv = threading.Condition()
+        self.err = None
+        self.n = 0
+        self.dev = torch.cuda.current_device()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        torch.cuda.set_device(self.dev)
+        ring = _ring()
+        used = [None] * len(ring)
+        j = 0
+        try:
+            while True:
+                job = self.jobs.get()
+                if job is None:
+                    return
+                tok, src, dst = job
+                with torch.cuda.stream(self.copy):
+                    if src.is_pinned():
+                        dst.copy_(src, non_blocking=True)
+                    else:
+                        flat_s, flat_d = src.reshape(-1), dst.reshape(-1)
+                        step = _STAGE_BYTES // 8
+                        for e0 in range(0, flat_s.numel(), step):
+                            e1 = min(flat_s.numel(), e0 + step)
+                            if used[j] is not None:
+                                used[j].synchronize()
+                            buf = ring[j][: e1 - e0]
+                            buf.copy_(flat_s[e0:e1])
+                            flat_d[e0:e1].copy_(buf, non_blocking=True)
+                            used[j] = torch.cuda.Event()
+                            used[j].record(self.copy)
+                            j = (j + 1) % len(ring)
+                    ev = torch.cuda.Event()
+                    ev.record(self.copy)
+                with self.cv:
+                    self.done[tok] = ev
+                    self.cv.notify_all()
+        except BaseException as e:     # surfaced by wait()
+            with self.cv:
+                self.err = e
+                self.cv.notify_all()
+
+    def submit(self, src, dst):
+        tok = self.n
+        self.n += 1
+        self.jobs.put((tok, src, dst))
+        return tok
+
+    def wait(self, tok, stream):
+        with self.cv:
+            while tok not in self.done and self.err is None:
+                self.cv.wait()
+            if self.err is not None:
+                raise self.err
+            ev = self.done.pop(tok)
+        stream.wait_event(ev)
+
+    def close(self):
+        self.jobs.put(None)
+        self.th.join()
 
 
 def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=16, chunks=8):
     """Round(A x) for host-resident cores; returns the rounded cores as pinned host tensors.
 
-    A_cores: dense operator cores (r0, n, m, r1); x_cores: vector cores (s0, m, s1) (numpy
-    arrays or CPU tensors). ``out`` may hold pinned host tensors of the expected output shapes
-    (reused across calls). The function returns after the downloads completed.
+    A_cores: dense operator cores (r0, n, m, r1); x_cores: vector cores (s0, m, s1) -- numpy arrays
+    (pageable memory, as a reference caller holds them: staged through a pinned ring by a worker
+    thread) or CPU tensors (pinned ones go straight to DMA). Returns pinned host tensors (``.numpy()``
+    views share their memory), allocated through torch's caching host allocator unless ``out`` holds
+    pinned tensors of the expected output shapes. The function returns after the downloads completed.
     """
     if eps <= 0:
         raise ValueError("eps must be positive")
-    A_cores = [_pinned(G) for G in A_cores]
-    x_cores = [_pinned(G) for G in x_cores]
+    A_cores = [_host(G) for G in A_cores]
+    x_cores = [_host(G) for G in x_cores]
     if len(A_cores) != len(x_cores) or not A_cores:
         raise TtShapeError("operator and vector must have the same number of cores")
     for k, (M, G) in enumerate(zip(A_cores, x_cores)):
@@ -56,41 +150,43 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
 
-    # ---- uploads (vector cores first, then operator cores slice by slice) and contractions
-    xd = []
-    with torch.cuda.stream(copy):
-        for G in x_cores:
-            xd.append(G.to("cuda", non_blocking=True))
-    x_ready = torch.cuda.Event()
-    x_ready.record(copy)
-    comp.wait_event(x_ready)
-    cores = []
-    for M, G in zip(A_cores, x_cores):
-        Ra, n, m, Rb = M.shape
-        rc, _, rd = G.shape
-        # Md is allocated on (owned by) the copy stream, so the caching allocator cannot hand it memory
-        # that kernels still queued on the compute stream are reading; record_stream(comp) below then
-        # keeps it alive until the contractions that read it have run.
+    # ---- uploads (vector cores first, then operator cores slice by slice) and contractions. Device
+    # buffers are allocated on (owned by) the copy stream, so the caching allocator cannot hand them
+    # memory that kernels still queued on the compute stream are reading; record_stream(comp) then
+    # keeps them alive until the contractions that read them have run.
+    up = _Uploader(copy)
+    try:
         with torch.cuda.stream(copy):
-            Md = L.empty(Ra, n, m, Rb)
-        Y = L.empty(Ra * rc, n, Rb * rd)
-        Yv = Y.view(Ra, rc, n, Rb, rd)
-        xk = xd[len(cores)]
-        step = max(1, -(-Ra // slices))
-        for a0 in range(0, Ra, step):
-            a1 = min(Ra, a0 + step)
-            with torch.cuda.stream(copy):
-                Md[a0:a1].copy_(M[a0:a1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            comp.wait_event(ev)
-            for a in range(a0, a1):
-                T = L.tdot(Md[a], xk, ([1], [1]), emulate=True)    # (i, b, c, d)
-                L.permute(T, (2, 0, 1, 3), out=Yv[a])              # (c, i, b, d)
-        Md.record_stream(comp)
-        cores.append(Y)
-    for t in xd:
-        t.record_stream(comp)
+            xd = [L.empty(*G.shape) for G in x_cores]
+            Mds = [L.empty(*M.shape) for M in A_cores]
+        x_tok = [up.submit(G, D) for G, D in zip(x_cores, xd)]
+        plan = []
+        for M, Md in zip(A_cores, Mds):
+            Ra = M.shape[0]
+            step = max(1, -(-Ra // slices))
+            plan.append([(a0, min(Ra, a0 + step), up.submit(M[a0:min(Ra, a0 + step)], Md[a0:min(Ra, a0 + step)]))
+                         for a0 in range(0, Ra, step)])
+        for t in x_tok:
+            up.wait(t, comp)
+        cores = []
+        for M, G, Md, slabs in zip(A_cores, x_cores, Mds, plan):
+            Ra, n, m, Rb = M.shape
+            rc, _, rd = G.shape
+            Y = L.empty(Ra * rc, n, Rb * rd)
+            Yv = Y.view(Ra, rc, n, Rb, rd)
+            xk = xd[len(cores)]
+            for a0, a1, tok in slabs:
+                up.wait(tok, comp)
+                for a in range(a0, a1):
+                    T = L.tdot(Md[a], xk, ([1], [1]), emulate=True)    # (i, b, c, d)
+                    L.permute(T, (2, 0, 1, 3), out=Yv[a])              # (c, i, b, d)
+            Md.record_stream(comp)
+            cores.append(Y)
+        for t in xd:
+            t.record_stream(comp)
+    finally:
+        up.close()
+    del Mds
 
     # ---- rounding (reference order), downloads overlapped with the last core formation
     host = [] if out is None else list(out)
@@ -98,7 +194,7 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
     def host_buf(k, shape):
         if k < len(host) and tuple(host[k].shape) == tuple(shape) and host[k].is_pinned():
             return host[k]
-        buf = torch.empty(shape, dtype=torch.float64).pin_memory()
+        buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)   # caching host allocator
         if k < len(host):
             host[k] = buf
         else:

@@ -44,3 +44,27 @@ def test_host_zero_and_errors():
         tt_matvec_round_host(A, [np.ones((1, 4, 3)), np.ones((3, 5, 1))], 1e-8)
     with pytest.raises(ValueError):
         tt_matvec_round_host(A, x, 0.0)
+
+
+def test_host_matches_device_at_scale(monkeypatch):
+    """The benchmarked host path at n=512 (every large-scale route on, pageable numpy inputs staged through
+    the pinned ring in 32 MB chunks, uploads racing the contractions) against the device-resident call:
+    guards the copy-stream ordering that tiny shapes cannot expose (host.py upload race)."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor, tt_matvec, tt_matvec_round_host, tt_round
+    from paper_2509_13224_b200.tensor_train import host as H
+    from paper_2509_13224_b200.workloads import matvec_round_instance_np
+    monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 1 << 18)
+    monkeypatch.setattr(L, "_GRAM_MIN_M", 1 << 18)
+    A, x = matvec_round_instance_np(512, 16, 64, 3, 0)
+    ref = tt_round(tt_matvec(TtMatrix(A), TtTensor(x)), 1e-8)
+    got = tt_matvec_round_host(A, x, 1e-8)
+    assert not any(torch.as_tensor(G).is_pinned() for G in A)
+    assert [tuple(g.shape) for g in got] == [tuple(G.shape) for G in ref.cores]
+    for g, G in zip(got, ref.cores):
+        assert torch.equal(g, G.cpu()), "host path must give the device path's bits"
+    # pinned inputs take the direct-DMA path: same bits again
+    got2 = tt_matvec_round_host([torch.as_tensor(G).pin_memory() for G in A], [torch.as_tensor(G).pin_memory() for G in x],
+                                1e-8)
+    assert all(torch.equal(a, b) for a, b in zip(got, got2))
+    assert H._STAGE_BYTES * H._STAGE_N < 512 ** 2 * 16 * 16 * 8

@@ -16,6 +16,42 @@ __device__ __forceinline__ int rr_index(int k, int r, int N) {
   return k == 0 ? 0 : ((k - 1 + r) % (N - 1)) + 1;
 }
 
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// Rotation of jrot, branch-free, with the tangent from approximate (MUFU) reciprocal square root and
+// reciprocal on power-of-two-scaled operands: t only chooses the angle -- any t gives an exactly
+// orthogonal (c, s) below, and a t off by ~1e-6 relative leaves ~1e-6 of g_pq for the next visit --
+// while c = (1 + t^2)^(-1/2) is the FP64 rsqrt, so (c, s) are orthogonal to rounding. Replaces jrot's
+// FP64 square root and division.
+__device__ __forceinline__ void jrot_fast(double al, double be, double ga, double thr2, double& c, double& s) {
+  const double d = be - al, g2 = 2.0 * ga;
+  const double m = fmax(fabs(d), fabs(g2));
+  const long long ex = (__double_as_longlong(m) >> 52) & 0x7ff;
+  const double sc = __longlong_as_double((2046LL - min(ex, 2045LL)) << 52);   // 2^(1023 - ex): m sc in [1, 2)
+  const double ds = fabs(d) * sc, gs = fabs(g2) * sc;
+  const double h = fma(ds, ds, gs * gs);
+  const double den = fma(h, rsqrt_approx(h), ds);          // |d| + sqrt(d^2 + g^2), scaled, >= 1
+  double t = gs * rcp_approx(den);
+  const bool pos = (d == 0.0) || ((d > 0.0) == (g2 > 0.0));
+  t = pos ? t : -t;
+  // c from the library rsqrt (unbiased rounding): a hand-rolled Newton step from the approximate
+  // rsqrt lands ~2e-17 high on average, and 1e4 rotation visits per column turn that into a 3e-13
+  // drift of the column norms
+  const double r = rsqrt(fma(t, t, 1.0));
+  const bool act = ga != 0.0 && ga * ga > thr2 * al * be;
+  c = act ? r : 1.0;
+  s = act ? r * t : 0.0;
+}
+
 // A (n x n col-major, ld n) -> columns mutually orthogonal; V accumulates rotations.
 // Returns number of sweeps in *sweeps_out (thread 0).
 __device__ void jacobi_core(int n, double* A, double* V, int* flag, int max_sweeps, double tol, int* sweeps_out) {
@@ -40,9 +76,8 @@ __device__ void jacobi_core(int n, double* A, double* V, int* flag, int max_swee
         al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
         if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
         if (lane == 0) *flag = 1;
-        double zeta = (be - al) / (2.0 * ga);
-        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        double c, s;
+        jrot_fast(al, be, ga, 0.0, c, s);
         for (int i = lane; i < n; i += 32) {
           double x = ap[i], y = aq[i];
           ap[i] = c * x - s * y;
@@ -155,9 +190,8 @@ __global__ void __launch_bounds__(CT) jacobi_coop_kernel(int n, double* A, doubl
         al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
         if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
         if (lane == 0) atomicAdd(c, 1);
-        double zeta = (be - al) / (2.0 * ga);
-        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        double cs, sn;
+        jrot_fast(al, be, ga, 0.0, cs, sn);
         for (int i = lane; i < n; i += 32) {
           double x = ap[i], y = aq[i];
           ap[i] = cs * x - sn * y;
@@ -242,9 +276,8 @@ __global__ void __launch_bounds__(BT) jacobi_block_kernel(int n, int b, double* 
             al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
             if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
             if (lane == 0) rot = 1;
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+            double cs, sn;
+            jrot_fast(al, be, ga, 0.0, cs, sn);
             for (int i = lane; i < n; i += 32) {
               const double x = ap[i], y = aq[i];
               ap[i] = cs * x - sn * y;
@@ -637,42 +670,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __device__ __forceinline__ void st_relaxed(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ double rsqrt_approx(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  return y;
-}
-__device__ __forceinline__ double rcp_approx(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  return y;
-}
-
-// Rotation of jrot, branch-free, with the tangent from approximate (MUFU) reciprocal square root and
-// reciprocal on power-of-two-scaled operands: t only chooses the angle -- any t gives an exactly
-// orthogonal (c, s) below, and a t off by ~1e-6 relative leaves ~1e-6 of g_pq for the next visit --
-// while c = (1 + t^2)^(-1/2) is the FP64 rsqrt, so (c, s) are orthogonal to rounding. Replaces jrot's
-// FP64 square root and division.
-__device__ __forceinline__ void jrot_fast(double al, double be, double ga, double thr2, double& c, double& s) {
-  const double d = be - al, g2 = 2.0 * ga;
-  const double m = fmax(fabs(d), fabs(g2));
-  const long long ex = (__double_as_longlong(m) >> 52) & 0x7ff;
-  const double sc = __longlong_as_double((2046LL - min(ex, 2045LL)) << 52);   // 2^(1023 - ex): m sc in [1, 2)
-  const double ds = fabs(d) * sc, gs = fabs(g2) * sc;
-  const double h = fma(ds, ds, gs * gs);
-  const double den = fma(h, rsqrt_approx(h), ds);          // |d| + sqrt(d^2 + g^2), scaled, >= 1
-  double t = gs * rcp_approx(den);
-  const bool pos = (d == 0.0) || ((d > 0.0) == (g2 > 0.0));
-  t = pos ? t : -t;
-  // c from the library rsqrt (unbiased rounding): a hand-rolled Newton step from the approximate
-  // rsqrt lands ~2e-17 high on average, and 1e4 rotation visits per column turn that into a 3e-13
-  // drift of the column norms
-  const double r = rsqrt(fma(t, t, 1.0));
-  const bool act = ga != 0.0 && ga * ga > thr2 * al * be;
-  c = act ? r : 1.0;
-  s = act ? r * t : 0.0;
 }
 
 __device__ __forceinline__ bool jw_eigen8(double* G, double* J, double tol, int lane) {

@@ -13,7 +13,9 @@
   (reference assembly.py:236-304): the load cores in full, and for the 190 MB stiffness TT its
   gauge-invariant summaries -- ranks, the singular values of both unfoldings, the Frobenius norm
   and 4096 seeded entries K[(i0,i1,i2),(j0,j1,j2)] with |i_d - j_d| <= p.
-* ``c3``: the same assembly summaries for configs[3] (seeded random cube, n=512).
+* ``c3``: the same assembly summaries for configs[3] (seeded random cube, n=512) -- beyond this
+  container's memory (the oracle's dense operator cores are 30 GB each); ``c3n128`` is the same
+  configuration at n=128 (geometry, det J check on the solve's Gauss grid, cross, rounding).
 
 The AMEn solve of configs[2]/[3] is out of the oracle's reach (its explicit residual core is
 ~100 GB / ~0.5 TB), see DESIGN.md §5b.
@@ -100,8 +102,10 @@ def c4():
     return out
 
 
-def assembly_summary(tag, c):
+def assembly_summary(tag, c, n_basis=None):
     kw = dict(SOLVE_CONFIGS[c])
+    if n_basis is not None:
+        kw["n_basis"] = n_basis
     cfg = OI.Config(seed=0, **kw)
     t = time.perf_counter()
     patch = OI.build_patch(cfg.geometry, OI.geometry_params(cfg))
@@ -129,7 +133,12 @@ def main():
     out = dict(np.load(PATH)) if os.path.exists(PATH) else {}
     for w in which:
         out = {k: v for k, v in out.items() if not k.startswith(w + "_")}
-        out.update(c4() if w == "c4" else assembly_summary(w, int(w[1])))
+        if w == "c4":
+            out.update(c4())
+        elif w == "c3n128":
+            out.update(assembly_summary(w, 3, 128))
+        else:
+            out.update(assembly_summary(w, int(w[1])))
         np.savez_compressed(PATH, **out)
     print("wrote", PATH)
 

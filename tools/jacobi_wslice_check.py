@@ -12,8 +12,11 @@ from paper_2509_13224_b200 import linalg as L  # noqa: E402
 
 alg = os.environ.get("TTB_JACOBI", "default")
 rng = np.random.default_rng(0)
-for n, kind in ((130, "gauss"), (256, "gauss"), (512, "gauss"), (1000, "gauss"), (1024, "gauss"),
-                (1024, "graded"), (1024, "R^T gram")):
+CASES = ((130, "gauss"), (256, "gauss"), (512, "gauss"), (1000, "gauss"), (1024, "gauss"), (1024, "graded"),
+         (1024, "R^T gram"))
+if os.environ.get("SMALL"):
+    CASES = ((32, "gauss"), (64, "gauss"), (100, "gauss"), (110, "graded"), (128, "gauss"))
+for n, kind in CASES:
     X = rng.standard_normal((n, n))
     if kind == "graded":
         X = X * np.logspace(0, -8, n)[None, :]

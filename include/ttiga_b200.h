@@ -196,6 +196,13 @@ int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, co
  * M[a, i, t, b] permuted to (i, t, a, b) (forward) or (i, t, b, a) (reverse). */
 int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
                   double* out);
+/* The same contraction as Ozaki-scheme FP64 on the int8 tensor cores (ttb_band_gemm dispatches to it for
+ * >= 2^35 flop, X >= 512, (2h+1) Rin <= 4096; TTB_BAND_OZAKI=0 disables): Tp sliced once per group of G
+ * batches (one exponent per row over the group's G + 2h blocks), Mt per batch; ws:
+ * ttb_band_gemm_ozaki_workspace bytes. */
+long long ttb_band_gemm_ozaki_workspace(int n, int h, int Rin, int Rout, int X, int G);
+int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
+                        double* out, void* ws, int G);
 /* Local projected operator (amen.py:147-150 matvec3) with vectors in the mode-major (i, x, z) layout:
  * phiLp = phiL permuted (a, x, y), Mf = (n, 2h+1, Ra, Rb), phiRp = phiR permuted (z, w, b) and
  * zero-padded to (r1, r1 + (r0 & r1 & 1), Rb) (the staged operand keeps an even column count).

@@ -80,6 +80,8 @@ SIGNATURES = {
     "ttb_ozaki_gram_rows": (i32, [vp, i32, i32, vp, i64, vp, i64, vp]),
     "ttb_trtri_lower": (i32, [vp, i32, vp, i64, vp, i64, vp]),
     "ttb_band_gemm": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
+    "ttb_band_gemm_ozaki_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
+    "ttb_band_gemm_ozaki": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i32]),
     "ttb_local_gemm_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
     "ttb_local_gemm_ws_init": (i32, [vp, i32, i32, i32, i32, i32, vp]),
     "ttb_local_matvec_gemm": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),

@@ -619,6 +619,9 @@ __global__ void sum_final(int np, const double* part, double* out, int take_sqrt
 
 }  // namespace
 
+// per-stream scratch buffer for other translation units (tt.cu band GEMM workspaces)
+double* ttb_scratch(size_t bytes, cudaStream_t st) { return scratch(bytes, st); }
+
 TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                       long long sA, const double* B, long long ldb, long long sB, double beta, double* C, long long ldc,
                       long long sC, int batch);

@@ -134,6 +134,15 @@ struct OzOut {
   int trilA;  // A lower triangular (M == K, one K range): row block m0 stops at k = m0 + 128
 };
 
+// Banded batched mode (ttb_band_gemm_ozaki): batch i multiplies a K window of its group's A slice stack
+// (group g = i / G holds the Tp blocks of batches gG .. gG+G-1 under one exponent per row) by its own B
+// slices: units are (batch, 128 x 64 tile); A rows come from z = 7 g of the 3-D map at K offset
+// (i - gG) Rin, B rows from i Np, C from out + i cstride with rows < X and columns < Rout written.
+struct OzBand {
+  int G, Rin /* K block per batch offset (padded) */, Mp, Np, Kp, X, Rout, nb;
+  long long cstride;
+};
+
 constexpr int OZ_SUB = 64;
 
 // tile t -> (m0, n0); sym: only the tiles touching the upper block triangle of a square output
@@ -153,12 +162,13 @@ __device__ __forceinline__ void oz_tile(int t, int ntn, int sym, int& m0, int& n
   n0 = (2 * mt + t) * OA_N;
 }  // k steps (of 64) per TMEM accumulation: K <= 4096 keeps every level sum exact in int32
 
-template <int LEV, bool LONGK>  // LONGK: K ranges deeper than OZ_SUB k steps (several TMEM accumulations)
+template <int LEV, bool LONGK, bool BAND = false>  // LONGK: K ranges deeper than OZ_SUB k steps
 __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                                                         int kchunk, int ksplit, int tiles, int sym,
                                                         const int* __restrict__ ea,
-                                                        const int* __restrict__ fb, const OzOut o) {
+                                                        const int* __restrict__ fb, const OzOut o,
+                                                        const OzBand bd = OzBand{}) {
   extern __shared__ __align__(1024) uint8_t dyn[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[OA_ST], empty[OA_ST], tfull, tempty;
@@ -186,15 +196,29 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
   const uint32_t tmem = tmem_base;
   // work unit u: K range u / tiles (kchunk deep), tile u % tiles (n fastest, so CTAs that run
   // together share the A rows); a range is accumulated in TMEM OZ_SUB k steps at a time
-  const int ntn = N / OA_N, units = tiles * ksplit;
+  const int ntn = (BAND ? bd.Np : N) / OA_N, units = BAND ? tiles * bd.nb : tiles * ksplit;
+  // work unit -> output tile (m0, n0) and k-step range [kt0, kt1); banded mode: batch bi
+  auto unit = [&](int u, int& m0, int& n0, int& kt0, int& kt1, int& bi) {
+    if constexpr (BAND) {
+      bi = u / tiles;
+      const int t = u % tiles;
+      m0 = (t / ntn) * OZ_M;
+      n0 = (t % ntn) * OA_N;
+      kt0 = 0;
+      kt1 = bd.Kp / OA_K;
+    } else {
+      bi = 0;
+      oz_tile(u % tiles, ntn, sym, m0, n0);
+      kt0 = (u / tiles) * (kchunk / OA_K);
+      kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K;
+    }
+  };
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: per stage one box of all 7 A slice tiles, one of all 7 B
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int m0, n0;
-        oz_tile(u % tiles, ntn, sym, m0, n0);
-        const int kt0 = (u / tiles) * (kchunk / OA_K);
-        const int kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K;
+        int m0, n0, kt0, kt1, bi;
+        unit(u, m0, n0, kt0, kt1, bi);
         for (int kt = kt0; kt < kt1; ++kt, ++it) {
           const int st = it % OA_ST;
           if (it >= OA_ST) mbar_wait(smem_u32(&empty[st]), ((it / OA_ST) - 1) & 1);
@@ -202,8 +226,14 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fbar), "r"(OA_SBYTES)
                        : "memory");
           const uint32_t base = smem_u32(sm + st * OA_SBYTES);
-          tma_load_3d(base, &tmA, kt * OA_K, m0, 0, fbar);
-          tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, 0, fbar);
+          if constexpr (BAND) {
+            const int gi = bi / bd.G;
+            tma_load_3d(base, &tmA, (bi - gi * bd.G) * bd.Rin + kt * OA_K, m0, OZ_S * gi, fbar);
+            tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, OZ_S * bi, fbar);
+          } else {
+            tma_load_3d(base, &tmA, kt * OA_K, m0, 0, fbar);
+            tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, 0, fbar);
+          }
         }
       }
     }
@@ -211,10 +241,8 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
     if (lane == 0) {  // MMA issuer
       int it = 0, g = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int m0, n0;
-        oz_tile(u % tiles, ntn, sym, m0, n0);
-        const int kt0 = (u / tiles) * (kchunk / OA_K);
-        const int kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K;
+        int m0, n0, kt0, kt1, bi;
+        unit(u, m0, n0, kt0, kt1, bi);
         for (int ks = kt0; ks < kt1; ks += OZ_SUB, ++g) {
           if (g > 0) {  // the epilogue has the previous accumulation's level sums in registers
             mbar_wait(smem_u32(&tempty), (g - 1) & 1);
@@ -251,13 +279,11 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
     constexpr int LO_EXP = -12 - 8 * (LEV - 1);
     int g = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      int m0, n0;
-      oz_tile(u % tiles, ntn, sym, m0, n0);
+      int m0, n0, kt0, kt1, bi;
+      unit(u, m0, n0, kt0, kt1, bi);
       n0 += h * 32;
-      const int kt0 = (u / tiles) * (kchunk / OA_K);
-      const int kt1 = LONGK ? min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K : 0;
-      const int my_ea = ea[m0 + q * 32 + lane];
-      const int my_fb = fb[n0 + lane];  // column n0 + lane's exponent, broadcast per column below
+      const int my_ea = BAND ? ea[(bi / bd.G) * bd.Mp + m0 + q * 32 + lane] : ea[m0 + q * 32 + lane];
+      const int my_fb = BAND ? fb[bi * bd.Np + n0 + lane] : fb[n0 + lane];  // column n0 + lane's exponent
       long long hi[32], lo[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0;
@@ -309,7 +335,16 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
         __syncwarp();
         double* crow = o.out + (o.mode == 1 ? (long long)(u / tiles) * o.so : 0LL) + (long long)(m0 + q * 32) * o.ldo +
                        n0 + j * 16 + cq;
-        if (o.mode == 2) {
+        if constexpr (BAND) {
+          crow = o.out + (long long)bi * bd.cstride + (long long)(m0 + q * 32) * o.ldo + n0 + j * 16 + cq;
+          if (n0 + j * 16 + cq < bd.Rout) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int rr = 2 * i + half;
+              if (m0 + q * 32 + rr < bd.X) crow[(long long)rr * o.ldo] = stg[rr * OA_EPAD + cq];
+            }
+          }
+        } else if (o.mode == 2) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int rr = 2 * i + half;
@@ -835,6 +870,164 @@ int ozaki_gemm(cudaStream_t st, int tB, int M, int N, int K, double alpha, const
   else
     oz_cols(st, K, N, B, ldb, w.fb, w.bmax, w.Bs);
   return oz_run(st, w, M, N, K, alpha, beta, C, ldc, 0);
+}
+
+// ---- banded batched FP64 product on the int8 tensor cores (the AMEn band contraction)
+//   out[i, x, o] = sum_{t < 2h+1, r < Rin} Tp[i + t, r, x] Mt[i, t, r, o],   i < n
+// (tensor_train/banded.py band_gemm, the ttb_band_gemm DMMA batch). Batch i is an X x K (K = (2h+1) Rin)
+// by K x Rout product whose A operand is the K window of Tp blocks i .. i+2h, so the Tp blocks are shared
+// by 2h+1 consecutive batches. A is sliced once per GROUP of G batches (blocks gG .. gG+G+2h-1, one
+// exponent per row x over the group, i.e. 2^-54 relative to the row's maximum over G+2h consecutive mode
+// indices instead of the batch's own 2h+1), each batch's A tiles are TMA boxes at K offset (i - gG) Rin of
+// its group's stack; B (Mt[i]) is sliced per batch with per-column exponents. Padding: rows X -> Mp (128),
+// columns Rout -> Np (64), K -> Kp (64); padded slices are zero. The kernel is oz_gemm_kernel<8, false,
+// true> (same MMA schedule, level folding and epilogue; rows >= X and columns >= Rout are not written).
+namespace {
+// cmax[b Cp + c] = max_k |X[(b rs + k) ld + c]| over k < Kv with b rs + k < lim (sticky NaN as oz_amax)
+__global__ void oz_bcolmax_kernel(int Kv, int Cv, int Cp, const double* __restrict__ X, long long ld, long long rs,
+                                  long long lim, unsigned long long* cmax) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.z;
+  if (c >= Cv) return;
+  const int k0 = blockIdx.y * 256;
+  const int k1 = (int)min((long long)min(Kv, k0 + 256), lim - (long long)b * rs);
+  double m = 0.0;
+  for (int k = k0; k < k1; ++k) m = oz_amax(m, X[((long long)b * rs + k) * ld + c]);
+  atomicMax(cmax + (long long)b * Cp + c, (unsigned long long)__double_as_longlong(m));
+}
+__global__ void oz_bexp_kernel(long long total, const unsigned long long* cmax, int* e) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < total) e[i] = oz_exp_of(__longlong_as_double((long long)cmax[i]));
+}
+// out[((b 7 + s) Cp + c) Kp + k] = slice s of X[(b rs + k) ld + c] (transposed, zero-padded to Cp x Kp)
+// K is laid out in blocks of Rp >= Rin (zero rows r >= Rin): output k = blk Rp + r <- source row blk Rin + r,
+// so that every batch window starts at a multiple of the 64-byte TMA k step
+__global__ void __launch_bounds__(256) oz_bslice_kernel(int Kv, int Cv, int Cp, int Kp, const double* __restrict__ X,
+                                                        long long ld, long long rs, long long lim, int Rin, int Rp,
+                                                        const int* __restrict__ e, uint8_t* out) {
+  __shared__ uint32_t t[OZ_S][64][17];
+  const int k0 = blockIdx.y * 64, c0 = blockIdx.x * 64, b = blockIdx.z;
+  const long long plane = (long long)Cp * Kp;
+  uint8_t* ob = out + (long long)b * OZ_S * plane;
+  const long long kl = min((long long)Kv, lim - (long long)b * rs);
+  for (int it = threadIdx.x; it < 64 * 16; it += 256) {
+    const int cc = it & 63, kq = it >> 6;
+    const int c = c0 + cc;
+    uint32_t w[OZ_S];
+#pragma unroll
+    for (int q = 0; q < OZ_S; ++q) w[q] = 0;
+    if (c < Cv) {
+      const int ex = e[(long long)b * Cp + c];
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 4 * kq + q;
+        const int r = k % Rp, src = (k / Rp) * Rin + r;
+        v[q] = (r < Rin && src < kl) ? __ldg(X + ((long long)b * rs + src) * ld + c) : 0.0;
+      }
+      oz_digits4(v, ex, oz_scale_of(ex), w);
+    }
+#pragma unroll
+    for (int q = 0; q < OZ_S; ++q) t[q][cc][kq] = w[q];
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < OZ_S * 64 * 16; it += 256) {
+    const int kq = it & 15, cc = (it >> 4) & 63, q = it >> 10;
+    const int c = c0 + cc, k = k0 + 4 * kq;
+    if (c < Cp && k < Kp) *reinterpret_cast<uint32_t*>(ob + q * plane + (long long)c * Kp + k) = t[q][cc][kq];
+  }
+}
+
+void oz_bslice(cudaStream_t st, int nb, int Kv, int Cv, int Cp, int Kp, const double* X, long long ld, long long rs,
+               long long lim, int Rin, int Rp, unsigned long long* cmax, int* e, uint8_t* out) {
+  cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * (size_t)nb * Cp, st);
+  oz_bcolmax_kernel<<<dim3(ceil_div(Cv, 256), ceil_div(Kv, 256), nb), 256, 0, st>>>(Kv, Cv, Cp, X, ld, rs, lim, cmax);
+  ttb_count();
+  oz_bexp_kernel<<<ceil_div((long long)nb * Cp, 256), 256, 0, st>>>((long long)nb * Cp, cmax, e); ttb_count();
+  oz_bslice_kernel<<<dim3(Cp / 64, Kp / 64, nb), 256, 0, st>>>(Kv, Cv, Cp, Kp, X, ld, rs, lim, Rin, Rp, e, out);
+  ttb_count();
+}
+
+struct OzBandLayout {
+  int Mp, Np, Rp, Kb, Kp, Kg, ng;
+  uint8_t *As, *Bs;
+  int *ea, *fb;
+  unsigned long long *amax, *bmax;
+  long long bytes;
+};
+
+OzBandLayout oz_band_layout(void* base, int n, int h, int Rin, int Rout, int X, int G) {
+  OzBandLayout w;
+  w.Mp = (X + OZ_M - 1) / OZ_M * OZ_M;
+  w.Np = (Rout + OA_N - 1) / OA_N * OA_N;
+  w.Rp = (Rin + OA_K - 1) / OA_K * OA_K;           // K block per Tp block / band offset (64-byte aligned)
+  w.Kb = (2 * h + 1) * Rin;
+  w.Kp = (2 * h + 1) * w.Rp;
+  w.Kg = (G - 1) * w.Rp + w.Kp;
+  w.ng = (n + G - 1) / G;
+  uintptr_t p = reinterpret_cast<uintptr_t>(base);
+  const uintptr_t p0 = p;
+  auto take = [&](long long bytes) { const uintptr_t r = p; p = (p + bytes + 255) & ~uintptr_t(255); return r; };
+  w.As = reinterpret_cast<uint8_t*>(take((long long)w.ng * OZ_S * w.Mp * w.Kg));
+  w.Bs = reinterpret_cast<uint8_t*>(take((long long)n * OZ_S * w.Np * w.Kp));
+  w.ea = reinterpret_cast<int*>(take(4LL * w.ng * w.Mp));
+  w.fb = reinterpret_cast<int*>(take(4LL * n * w.Np));
+  w.amax = reinterpret_cast<unsigned long long*>(take(8LL * w.ng * w.Mp));
+  w.bmax = reinterpret_cast<unsigned long long*>(take(8LL * n * w.Np));
+  w.bytes = (long long)(p - p0) + 256;
+  return w;
+}
+
+bool oz_tmap3(CUtensorMap* tm, const void* ptr, int K, int rows, int planes, int box_rows) {
+  auto enc = oz_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)rows * K};
+  cuuint32_t box[3] = {(cuuint32_t)OA_K, (cuuint32_t)box_rows, (cuuint32_t)OZ_S};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = OA_K == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+TTB_API long long ttb_band_gemm_ozaki_workspace(int n, int h, int Rin, int Rout, int X, int G) {
+  if (n < 1 || h < 0 || Rin < 1 || Rout < 1 || X < 1 || G < 1) return 0;
+  return oz_band_layout(nullptr, n, h, Rin, Rout, X, G).bytes;
+}
+
+// Tp: (n + 2h, Rin, X) row-major (h zero blocks per end, banded.py _padded); Mt: (n, 2h+1, Rin, Rout);
+// out: (n, X, Rout). ws: ttb_band_gemm_ozaki_workspace bytes. G: batches per A slice group.
+TTB_API int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp,
+                                const double* Mt, double* out, void* ws, int G) {
+  if (n < 1 || h < 0 || Rin < 1 || Rout < 1 || X < 1 || G < 1 || !ws) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  OzBandLayout w = oz_band_layout(ws, n, h, Rin, Rout, X, G);
+  if (w.Kp > OZ_SUB * OA_K) return TTB_EARG;     // one TMEM accumulation per tile (K <= 4096)
+  // A: group g = rows k of Tp blocks gG .. gG + G + 2h - 1 (row-major (rows x X), ld X)
+  oz_bslice(st, w.ng, (G + 2 * h) * Rin, X, w.Mp, w.Kg, Tp, X, (long long)G * Rin, (long long)(n + 2 * h) * Rin, Rin,
+            w.Rp, w.amax, w.ea, w.As);
+  // B: batch i = Mt[i] as ((2h+1) Rin x Rout), ld Rout
+  oz_bslice(st, n, w.Kb, Rout, w.Np, w.Kp, Mt, Rout, (long long)w.Kb, (long long)n * w.Kb, Rin, w.Rp, w.bmax, w.fb,
+            w.Bs);
+  // both stacks are [batch][slice][rows][K]: 3-D maps with 7 planes per batch (z = 7 batch)
+  CUtensorMap ta, tb;
+  if (!oz_tmap3(&ta, w.As, w.Kg, w.Mp, w.ng * OZ_S, OZ_M) || !oz_tmap3(&tb, w.Bs, w.Kp, w.Np, n * OZ_S, OA_N))
+    return TTB_EARG;
+  const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(oz_gemm_kernel<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cfg = true;
+  }
+  const int tiles = (w.Mp / OZ_M) * (w.Np / OA_N);
+  const long long units = (long long)tiles * n;
+  const int grid = units < oz_nsm() ? (int)units : oz_nsm();
+  OzOut o{out, Rout, 0, 1.0, 0.0, 0, 0};
+  OzBand bd{G, w.Rp, w.Mp, w.Np, w.Kp, X, Rout, n, (long long)X * Rout};
+  oz_gemm_kernel<8, false, true><<<grid, 320, smem, st>>>(ta, tb, w.Mp, w.Np, w.Kp, w.Kp, 1, tiles, 0, w.ea, w.fb, o, bd);
+  ttb_count();
+  return ttb_last_error();
 }
 
 TTB_API long long ttb_ozaki_workspace(int M, int N, int K) { return ozaki_ws_bytes(M, N, K); }

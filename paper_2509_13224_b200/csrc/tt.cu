@@ -367,9 +367,35 @@ TTB_API long long ttb_pcg_workspace(int r0, int n, int r1, int Ra, int Rb) {
 // is, for every mode index i, one GEMM whose K = (2h+1) Ra operand is the contiguous window of
 // Tp rows starting at block i: C_i (X x Rb) = Tp_window_i^T (X x K) * Mf_i (K x Rb).
 // The padding blocks of Tp must be zero (they meet the zero out-of-band slots of Mf).
+TTB_API long long ttb_band_gemm_ozaki_workspace(int n, int h, int Rin, int Rout, int X, int G);
+TTB_API int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp,
+                                const double* Mt, double* out, void* ws, int G);
+double* ttb_scratch(size_t bytes, cudaStream_t st);
+
+// Large band contractions (>= 2^35 flop, X >= 512, K <= 4096) run as Ozaki-scheme FP64 on the int8
+// tensor cores (ozaki.cu ttb_band_gemm_ozaki, 2.4x the DMMA batch at the configs[3] local shape);
+// TTB_BAND_OZAKI=0 keeps every band GEMM on DMMA, TTB_BAND_OZ_G sets the A slice group size (32).
+static int band_oz_group() {
+  static int g = -1;
+  if (g < 0) {
+    const char* e = getenv("TTB_BAND_OZAKI");
+    const char* eg = getenv("TTB_BAND_OZ_G");
+    g = (e && e[0] == '0') ? 0 : (eg ? atoi(eg) : 32);
+    if (g < 0) g = 0;
+  }
+  return g;
+}
+
 TTB_API int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
                           double* out) {
   const int B = 2 * h + 1;
+  const int G = band_oz_group();
+  const double flop = 2.0 * n * (double)X * Rout * B * Rin;
+  if (G > 0 && flop >= 34359738368.0 && X >= 512 && B * Rin <= 4096) {
+    cudaStream_t st = as_stream(stream);
+    void* ws = ttb_scratch((size_t)ttb_band_gemm_ozaki_workspace(n, h, Rin, Rout, X, G), st);
+    if (ws) return ttb_band_gemm_ozaki(stream, n, h, Rin, Rout, X, Tp, Mt, out, ws, G);
+  }
   return ttb_dgemm(stream, 1, 0, X, Rout, B * Rin, 1.0, Tp, X, (long long)Rin * X, Mt, Rout,
                    (long long)B * Rin * Rout, 0.0, out, Rout, (long long)X * Rout, n);
 }

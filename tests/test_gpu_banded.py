@@ -205,3 +205,44 @@ def test_truncation_residuals_basis_form(forward):
         xq = L.gemm(Uf[:, :q], SVf[:q]).reshape(r0, n, r1)
         direct = float(L.nrm2(sy.matvec3(xq) - rhs3).item())
         assert abs(res(q) - direct) <= 1e-12 * direct
+
+
+def _band_ref(Tp, Mt, n, h, Rin, Rout, X):
+    from paper_2509_13224_b200 import linalg as L
+    B = 2 * h + 1
+    out = L.empty(n, X, Rout)
+    L.gemm_strided(1, 0, X, Rout, B * Rin, Tp, X, Rin * X, Mt, Rout, B * Rin * Rout, out, Rout, X * Rout, n)
+    return out
+
+
+@pytest.mark.parametrize("graded", [False, True])
+def test_band_gemm_ozaki_vs_dmma(graded, record_property):
+    """The banded batched contraction on the int8 tensor cores (ttb_band_gemm_ozaki; padding of X, Rout and
+    K; a partial last slice group) against the DMMA batch at FP64: normwise <= 1e-14. Graded inputs
+    (Tp blocks scaled over 1e6 along the mode index, like a solution spanning boundary layers) compare
+    the group exponents (G = 8) with per-window ones (G = 1)."""
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    n, h, Rin, Rout, X = 43, 3, 121, 121, 1000
+    B = 2 * h + 1
+    g = torch.Generator(device="cuda").manual_seed(7)
+    Tp = torch.randn(n + 2 * h, Rin, X, generator=g, dtype=torch.float64, device="cuda")
+    Tp[:h] = 0
+    Tp[n + h:] = 0
+    if graded:
+        Tp *= torch.logspace(-3, 3, n + 2 * h, dtype=torch.float64, device="cuda")[:, None, None]
+    Mt = torch.randn(n, B, Rin, Rout, generator=g, dtype=torch.float64, device="cuda")
+    ref = _band_ref(Tp, Mt, n, h, Rin, Rout, X)
+    errs = {}
+    for G in (1, 8):
+        ws = torch.empty(int(call_raw("ttb_band_gemm_ozaki_workspace", n, h, Rin, Rout, X, G)), dtype=torch.uint8,
+                         device="cuda")
+        out = torch.full((n, X, Rout), float("nan"), dtype=torch.float64, device="cuda")
+        call("ttb_band_gemm_ozaki", n, h, Rin, Rout, X, ptr(Tp), ptr(Mt), ptr(out), ptr(ws), G)
+        assert torch.isfinite(out).all()
+        # per batch (the graded batches differ by 1e6 in scale)
+        e = ((out - ref).flatten(1).norm(dim=1) / ref.flatten(1).norm(dim=1)).max().item()
+        errs[G] = e
+    print(f"band GEMM Ozaki vs DMMA (graded={graded}): max per-batch normwise error G=1 {errs[1]:.2e}, G=8 {errs[8]:.2e}")
+    record_property("err_G1", errs[1])
+    record_property("err_G8", errs[8])
+    assert errs[1] <= 1e-14 and errs[8] <= (1e-14 if not graded else 1e-12), errs

@@ -407,7 +407,7 @@ int launch_wy_update_t(int M, int N, int K, double alpha, const double* A, long 
   }
   const int mt = (M + WU_BM - 1) / WU_BM;
   const int ntn = (N + BN - 1) / BN;
-  static const int sms = getenv("TTB_WY_SMS") ? atoi(getenv("TTB_WY_SMS")) : 148;
+  static const int sms = getenv("TTB_WY_SMS") ? atoi(getenv("TTB_WY_SMS")) : ttb_num_sms();
   int gy = sms / mt;
   if (gy < 1) gy = 1;
   if (gy > ntn) gy = ntn;
@@ -667,6 +667,9 @@ static bool mid96_tiles() {  // TTB_GEMM_N96=0 disables the 128x96 tiles (A/B)
 TTB_API int ttb_dgemm(void* stream, int tA, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                       long long sA, const double* B, long long ldb, long long sB, double beta, double* C,
                       long long ldc, long long sC, int batch) {
+  static const bool log = getenv("TTB_GEMM_LOG") != nullptr;   // shape log of the large DMMA GEMMs (tools)
+  if (log && 2.0 * M * N * (double)K * batch >= 1e10)
+    fprintf(stderr, "ttb_gemm tA=%d tB=%d M=%d N=%d K=%d batch=%d\n", tA, tB, M, N, K, batch);
   const int rc = ttb_dgemm_impl(stream, tA, tB, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, batch);
   if (ttb_debug_sync()) {
     const cudaError_t e = cudaStreamSynchronize(as_stream(stream));
@@ -705,15 +708,15 @@ static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, dou
   long long work = (long long)M * N * batch;
   // (N in [96, 128) stays on 64x64 tiles: measured faster than 128x128 for the banded-operator GEMMs,
   // 31.0 vs 26.8 TF/s at the configs[3] local shape even with even (16-byte) strides)
-  const bool big = (work >= (long long)148 * 128 * 128 * 2 || K >= 8192) && M >= 128 && N >= 128;
+  const bool big = (work >= (long long)ttb_num_sms() * 128 * 128 * 2 || K >= 8192) && M >= 128 && N >= 128;
   const bool narrow = !big && N <= 32 && M >= 48;  // thin outputs (WY products over panel widths)
   const long long tiles = big ? (long long)ceil_div(M, 128) * ceil_div(N, 128) * batch
                         : narrow ? (long long)ceil_div(M, 128) * ceil_div(N, 32) * batch
                                  : (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch;
-  if (batch == 1 && tiles < 148 && K >= 1024) {
+  if (batch == 1 && tiles < ttb_num_sms() && K >= 1024) {
     // split-K: chunks filling (not exceeding) two waves of 148 SMs, each chunk >= 256 deep,
     // deterministic reduction
-    long long S = 296 / tiles;
+    long long S = 2LL * ttb_num_sms() / tiles;
     long long maxS = K / 256;
     if (S > maxS) S = maxS;
     if (S > 1) {
@@ -728,7 +731,7 @@ static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, dou
       if (rc) return rc;
       long long tot = (long long)M * N;
       int blocks = ceil_div(tot, 256);
-      if (blocks > 148 * 8) blocks = 148 * 8;
+      if (blocks > ttb_num_sms() * 8) blocks = ttb_num_sms() * 8;
       splitk_reduce<<<blocks, 256, 0, st>>>(M, N, (int)S, part, alpha, beta, C, ldc); ttb_count();
       return ttb_last_error();
     }
@@ -744,7 +747,7 @@ static int ttb_dgemm_impl(void* stream, int tA, int tB, int M, int N, int K, dou
   if (narrow) return launch_gemm<128, 32, 4, 1>(g, batch, st);
   // TT-rank-wide outputs (65 <= N <= 96, e.g. the AMEn local operator's phiR stage): one 96-wide
   // column tile instead of two 64-wide ones (which would be 50-75% full)
-  if (N > 64 && N <= 96 && M >= 256 && work >= (long long)148 * 128 * 96 && mid96_tiles())
+  if (N > 64 && N <= 96 && M >= 256 && work >= (long long)ttb_num_sms() * 128 * 96 && mid96_tiles())
     return launch_gemm<128, 96, 4, 2>(g, batch, st);
   return launch_gemm<64, 64, 2, 2>(g, batch, st);
 }
@@ -794,7 +797,7 @@ TTB_API int ttb_permute(void* stream, int nd, const long long* in_dims, const in
         }
         if (S >= 8) {
           int blocks = ceil_div(total, 256);
-          if (blocks > 148 * 16) blocks = 148 * 16;
+          if (blocks > ttb_num_sms() * 16) blocks = ttb_num_sms() * 16;
           transpose_runs_kernel<<<blocks, 256, 0, st>>>(total, R, Cc, S, src, dst); ttb_count();
           return ttb_last_error();
         }
@@ -802,7 +805,7 @@ TTB_API int ttb_permute(void* stream, int nd, const long long* in_dims, const in
     }
   }
   int blocks = ceil_div(total, 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > ttb_num_sms() * 16) blocks = ttb_num_sms() * 16;
   permute_kernel<<<blocks, 256, 0, as_stream(stream)>>>(a, total, src, dst); ttb_count();
   return ttb_last_error();
 }

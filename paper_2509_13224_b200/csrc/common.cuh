@@ -43,6 +43,18 @@ static inline void ttb_count() { __atomic_add_fetch(&g_ttb_launches, 1LL, __ATOM
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// SM count of the current device (grid sizes of grid-stride and persistent kernels; 148 on B200)
+static inline int ttb_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -153,7 +153,7 @@ TTB_API int ttb_stencil_spmv(void* stream, int n0, int n1, int n2, int p0, int p
                              const double* x, const unsigned char* mask, double* y) {
   const long long N = (long long)n0 * n1 * n2;
   if (N <= 0) return TTB_OK;
-  const long long blocks = (N + 255) / 256 < 148 * 16 ? (N + 255) / 256 : 148 * 16;
+  const long long blocks = (N + 255) / 256 < ttb_num_sms() * 16 ? (N + 255) / 256 : ttb_num_sms() * 16;
   stencil_spmv_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(n0, n1, n2, p0, p1, p2, K, x, mask, y); ttb_count();
   return ttb_last_error();
 }

@@ -537,7 +537,7 @@ __global__ void pair_sum_kernel(long long np, const double* part, double* out) {
 
 int grid_for(long long tot, int threads = 256) {
   long long b = (tot + threads - 1) / threads;
-  if (b > 148LL * 16) b = 148LL * 16;
+  if (b > (long long)ttb_num_sms() * 16) b = (long long)ttb_num_sms() * 16;
   if (b < 1) b = 1;
   return (int)b;
 }

@@ -719,7 +719,7 @@ void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, in
   } else {
     oz_rowexp_kernel<<<ceil_div((long long)rows * 32, 256), 256, 0, st>>>(rows, K, X, ld, e); ttb_count();
   }
-  oz_slice_rows_kernel<<<148 * 16, 256, 0, st>>>(rows, K, X, ld, e, out); ttb_count();
+  oz_slice_rows_kernel<<<ttb_num_sms() * 16, 256, 0, st>>>(rows, K, X, ld, e, out); ttb_count();
 }
 
 // exponents (and transposed slices) of the columns of a row-major (K x cols, ld) operand
@@ -838,13 +838,13 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   if (ks > 1) {
     const long long tot = (long long)M * N;
     int blocks = ceil_div(tot, 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > ttb_num_sms() * 8) blocks = ttb_num_sms() * 8;
     oz_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, ks, w.part, alpha, beta, C, ldc); ttb_count();
   }
   if (sym) {
     const long long tot = (long long)M * N;
     int blocks = ceil_div(tot, 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > ttb_num_sms() * 8) blocks = ttb_num_sms() * 8;
     oz_mirror_kernel<<<blocks, 256, 0, st>>>(M, C, ldc); ttb_count();
   }
   return ttb_last_error();

@@ -599,7 +599,7 @@ bool coop_panels() {
 
 int grid_v(long long tot) {
   int b = ceil_div(tot, 256);
-  if (b > 148 * 8) b = 148 * 8;
+  if (b > ttb_num_sms() * 8) b = ttb_num_sms() * 8;
   return b < 1 ? 1 : b;
 }
 
@@ -950,7 +950,7 @@ TTB_API int ttb_extract_r(void* stream, int k, int n, const double* A, long long
   long long tot = (long long)k * n;
   if (tot == 0) return TTB_OK;
   int blocks = ceil_div(tot, 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > ttb_num_sms() * 8) blocks = ttb_num_sms() * 8;
   extract_r_kernel<<<blocks, 256, 0, as_stream(stream)>>>(k, n, A, lda, R); ttb_count();
   return ttb_last_error();
 }

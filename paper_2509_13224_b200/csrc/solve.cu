@@ -428,7 +428,7 @@ TTB_API int ttb_potrf(void* stream, int n, double* A, long long lda, int* info) 
     {
       int g = ceil_div(n - j0 - nb, 256);
       if (g < 1) g = 1;
-      if (g > 148) g = 148;
+      if (g > ttb_num_sms()) g = ttb_num_sms();
       chol_panel_kernel<<<g, 256, 0, st>>>(n, j0, A, lda, info); ttb_count();
     }
     const int m2 = n - j0 - nb;

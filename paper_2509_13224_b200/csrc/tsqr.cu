@@ -521,7 +521,7 @@ int tsqr_panel(long long m, int jb, double* P, long long ld, double* tau, double
   if (rc) return rc;
   {
     int blocks = ceil_div(rt, 256);
-    if (blocks > 148 * 4) blocks = 148 * 4;
+    if (blocks > ttb_num_sms() * 4) blocks = ttb_num_sms() * 4;
     tsqr_q1_kernel<<<blocks, 256, 0, st>>>(rt, jb, Vtop, Ttop, Xtop); ttb_count();
     TTB_DBG(st, "tsqr q1");
   }

@@ -16,7 +16,7 @@ namespace {
 
 int grid_for(long long tot, int threads = 256) {
   long long b = (tot + threads - 1) / threads;
-  if (b > 148LL * 16) b = 148LL * 16;
+  if (b > (long long)ttb_num_sms() * 16) b = (long long)ttb_num_sms() * 16;
   if (b < 1) b = 1;
   return (int)b;
 }

@@ -197,7 +197,7 @@ int ttb_local_pcg(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, co
 int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
                   double* out);
 /* The same contraction as Ozaki-scheme FP64 on the int8 tensor cores (ttb_band_gemm dispatches to it for
- * >= 2^35 flop, X >= 512, (2h+1) Rin <= 4096; TTB_BAND_OZAKI=0 disables): Tp sliced once per group of G
+ * >= 2e10 flop, X >= 128, (2h+1) Rin <= 4096; TTB_BAND_OZAKI=0 disables): Tp sliced once per group of G
  * batches (one exponent per row over the group's G + 2h blocks), Mt per batch; ws:
  * ttb_band_gemm_ozaki_workspace bytes. */
 long long ttb_band_gemm_ozaki_workspace(int n, int h, int Rin, int Rout, int X, int G);

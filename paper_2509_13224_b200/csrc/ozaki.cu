@@ -132,6 +132,7 @@ struct OzOut {
   double alpha, beta;
   int mode;
   int trilA;  // A lower triangular (M == K, one K range): row block m0 stops at k = m0 + 128
+  int mv, nv; // modes 0 / 2 of a padded product: only rows < mv and columns < nv are written (0: all)
 };
 
 // Banded batched mode (ttb_band_gemm_ozaki): batch i multiplies a K window of its group's A slice stack
@@ -344,6 +345,18 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
               if (m0 + q * 32 + rr < bd.X) crow[(long long)rr * o.ldo] = stg[rr * OA_EPAD + cq];
             }
           }
+        } else if (o.mv > 0) {   // padded product: rows >= mv / columns >= nv are padding
+          if (n0 + j * 16 + cq < o.nv) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int rr = 2 * i + half;
+              if (m0 + q * 32 + rr < o.mv) {
+                const double y = o.alpha * stg[rr * OA_EPAD + cq];
+                crow[(long long)rr * o.ldo] =
+                    (o.mode != 2 || o.beta == 0.0) ? y : fma(o.beta, crow[(long long)rr * o.ldo], y);
+              }
+            }
+          }
         } else if (o.mode == 2) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -406,13 +419,14 @@ __global__ void oz_rowmax_kernel(int rows, int K, const double* __restrict__ X, 
 }
 
 // C = alpha sum_s part[s] + beta C (fixed summation order: deterministic)
+// C (M x N valid of the pM x pN partial layout) = alpha sum_s part[s] + beta C
 __global__ void oz_reduce_kernel(int M, int N, int S, const double* __restrict__ part, double alpha, double beta,
-                                 double* C, long long ldc) {
-  const long long tot = (long long)M * N;
+                                 double* C, long long ldc, int pM, int pN) {
+  const long long tot = (long long)M * N, ptot = (long long)pM * pN;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int s = 0; s < S; ++s) acc += part[(long long)s * tot + e];
     const long long i = e / N, j = e % N;
+    double acc = 0.0;
+    for (int s = 0; s < S; ++s) acc += part[(long long)s * ptot + i * pN + j];
     double* c = C + i * ldc + j;
     *c = beta == 0.0 ? alpha * acc : fma(beta, *c, alpha * acc);
   }
@@ -701,6 +715,39 @@ __global__ void __launch_bounds__(256) oz_rowslice_fused_kernel(int rows, int K,
   }
 }
 
+// Row exponent + slicing with zero padding to Mp x Kp (any K): one warp per row, max pass then slice pass
+// (the second read of the row hits L1/L2); rows >= rows are zero with exponent 0.
+__global__ void __launch_bounds__(256) oz_prows_kernel(int rows, int K, const double* __restrict__ X, long long ld,
+                                                       int Mp, int Kp, int* __restrict__ e, uint8_t* out) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= Mp) return;
+  const long long plane = (long long)Mp * Kp;
+  uint8_t* o = out + (long long)r * Kp;
+  if (r >= rows) {
+    for (int q = lane; q < Kp / 4; q += 32)
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane + 4 * q) = 0u;
+    if (lane == 0) e[r] = 0;
+    return;
+  }
+  const double* x = X + (long long)r * ld;
+  double m = 0.0;
+  for (int k = lane; k < K; k += 32) m = oz_amax(m, __ldg(x + k));
+  for (int of = 16; of; of >>= 1) m = oz_amax(m, __shfl_xor_sync(0xffffffffu, m, of));
+  const int ex = oz_exp_of(m);
+  if (lane == 0) e[r] = ex;
+  const double sc = oz_scale_of(ex);
+  for (int q = lane; q < Kp / 4; q += 32) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = 4 * q + u < K ? __ldg(x + 4 * q + u) : 0.0;
+    uint32_t w[OZ_S];
+    oz_digits4(v, ex, sc, w);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane + 4 * q) = w[s];
+  }
+}
+
 // exponents (and slices) of the rows of a row-major (rows x K, ld) operand
 void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, int* e, unsigned long long* rmax,
              uint8_t* out) {
@@ -803,7 +850,7 @@ __global__ void oz_mirror_kernel(int n, double* G, long long ldg) {
 
 // the int8 GEMM over prepared slices + split-K reduction (+ mirror for sym)
 int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, double beta, double* C, long long ldc,
-           int sym, int trilA = 0) {
+           int sym, int trilA = 0, int mv = 0, int nv = 0) {
   CUtensorMap ta, tb;
   if (!oz_tmap(&ta, w.As, M, K, OZ_M, OA_K) || !oz_tmap(&tb, w.Bs, N, K, OA_N, OA_K)) return TTB_EARG;
   const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
@@ -825,7 +872,7 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   if (ks > 1)
     o = OzOut{w.part, N, (long long)M * N, 1.0, 0.0, 1, 0};
   else
-    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2, trilA && M == K ? 1 : 0};
+    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2, trilA && M == K ? 1 : 0, mv, nv};
   const long long units = tiles * ks;
   const int grid = units < oz_nsm() ? (int)units : oz_nsm();
   if (kc > OZ_SUB * OA_K)
@@ -839,7 +886,8 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
     const long long tot = (long long)M * N;
     int blocks = ceil_div(tot, 256);
     if (blocks > ttb_num_sms() * 8) blocks = ttb_num_sms() * 8;
-    oz_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, ks, w.part, alpha, beta, C, ldc); ttb_count();
+    oz_reduce_kernel<<<blocks, 256, 0, st>>>(mv > 0 ? mv : M, mv > 0 ? nv : N, ks, w.part, alpha, beta, C, ldc, M, N);
+    ttb_count();
   }
   if (sym) {
     const long long tot = (long long)M * N;
@@ -852,17 +900,22 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
 }  // namespace
 
 // Workspace (bytes) of ttb_dgemm_ozaki: slice stacks of A and B, exponents, maxima, split-K partials.
+static inline int oz_rup(int v, int m) { return (v + m - 1) / m * m; }
+// any shape: the padded shape's workspace (Mp = M rounded up to 128, Np, Kp to 64)
 long long ozaki_ws_bytes(int M, int N, int K) {
-  if (!oz_shape_ok(M, N, K)) return 0;
-  return oz_ws_layout(nullptr, M, N, K, 0).bytes;
+  if (M < 1 || N < 1 || K < 1) return 0;
+  return oz_ws_layout(nullptr, oz_rup(M, OZ_M), oz_rup(N, OA_N), oz_rup(K, OA_K), 0).bytes;
 }
+int ozaki_gemm_padded(cudaStream_t st, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                      const double* B, long long ldb, double beta, double* C, long long ldc, void* ws);
 bool ozaki_shape_ok(int M, int N, int K) { return oz_shape_ok(M, N, K); }
 
 // C (M x N, ldc) = alpha A B + beta C, FP64 via the Ozaki scheme on the INT8 tensor cores. A: row-major
 // M x K (lda); B: row-major K x N (ldb) when tB == 0, N x K (ldb) when tB == 1. ws: ozaki_ws_bytes.
 int ozaki_gemm(cudaStream_t st, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
                const double* B, long long ldb, double beta, double* C, long long ldc, void* ws) {
-  if (!oz_shape_ok(M, N, K)) return TTB_EARG;
+  if (M < 1 || N < 1 || K < 1) return TTB_EARG;
+  if (!oz_shape_ok(M, N, K)) return ozaki_gemm_padded(st, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws);
   OzWs w = oz_ws_layout(ws, M, N, K, 0);
   oz_rows(st, M, K, A, lda, w.ea, w.amax, w.As);
   if (tB)
@@ -1030,10 +1083,27 @@ TTB_API int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, i
   return ttb_last_error();
 }
 
+// Padded general product: operands sliced into Mp x Kp / Np x Kp stacks with zero padding (rows by
+// oz_prows_kernel, columns of a K x N B by the batched column slicer with nb = 1), the kernel runs the
+// padded shape and writes only the M x N block (OzOut.mv / nv; split-K partials are reduced over it).
+int ozaki_gemm_padded(cudaStream_t st, int tB, int M, int N, int K, double alpha, const double* A, long long lda,
+                      const double* B, long long ldb, double beta, double* C, long long ldc, void* ws) {
+  const int Mp = oz_rup(M, OZ_M), Np = oz_rup(N, OA_N), Kp = oz_rup(K, OA_K);
+  OzWs w = oz_ws_layout(ws, Mp, Np, Kp, 0);
+  oz_prows_kernel<<<ceil_div((long long)Mp * 32, 256), 256, 0, st>>>(M, K, A, lda, Mp, Kp, w.ea, w.As); ttb_count();
+  if (tB) {
+    oz_prows_kernel<<<ceil_div((long long)Np * 32, 256), 256, 0, st>>>(N, K, B, ldb, Np, Kp, w.fb, w.Bs); ttb_count();
+  } else {
+    oz_bslice(st, 1, K, N, Np, Kp, B, ldb, 0, K, Kp, Kp, w.bmax, w.fb, w.Bs);
+  }
+  return oz_run(st, w, Mp, Np, Kp, alpha, beta, C, ldc, 0, 0, M, N);
+}
+
 TTB_API long long ttb_ozaki_workspace(int M, int N, int K) { return ozaki_ws_bytes(M, N, K); }
 
-// Whether ttb_dgemm_ozaki takes this shape (M % 128, N % 64, K % 64; any K: ranges of 4096 are
-// accumulated exactly in TMEM and combined in int64).
+// Whether ttb_dgemm_ozaki runs this shape without padding (M % 128, N % 64, K % 64; any K: ranges of
+// 4096 are accumulated exactly in TMEM and combined in int64). Other shapes run padded (zero slices,
+// masked epilogue); the caller weighs the padding waste (linalg.gemm).
 TTB_API int ttb_ozaki_applies(int M, int N, int K) { return oz_shape_ok(M, N, K) ? 1 : 0; }
 
 // C (M x N, ldc) = A op(B), FP64 via the Ozaki scheme (see ozaki_gemm). ws: ttb_ozaki_workspace bytes.

@@ -372,8 +372,9 @@ TTB_API int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, i
                                 const double* Mt, double* out, void* ws, int G);
 double* ttb_scratch(size_t bytes, cudaStream_t st);
 
-// Large band contractions (>= 2^35 flop, X >= 512, K <= 4096) run as Ozaki-scheme FP64 on the int8
-// tensor cores (ozaki.cu ttb_band_gemm_ozaki, 2.4x the DMMA batch at the configs[3] local shape);
+// Large band contractions (>= 2e10 flop, X >= 128, K <= 4096) run as Ozaki-scheme FP64 on the int8
+// tensor cores (ozaki.cu ttb_band_gemm_ozaki: 1.9x the DMMA batch at the configs[3] local shape, 1.2-1.4x
+// from 2-3e10 flop, break-even below; tools/bench_band_ozaki.py);
 // TTB_BAND_OZAKI=0 keeps every band GEMM on DMMA, TTB_BAND_OZ_G sets the A slice group size (32).
 static int band_oz_group() {
   static int g = -1;
@@ -391,7 +392,7 @@ TTB_API int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, 
   const int B = 2 * h + 1;
   const int G = band_oz_group();
   const double flop = 2.0 * n * (double)X * Rout * B * Rin;
-  if (G > 0 && flop >= 34359738368.0 && X >= 512 && B * Rin <= 4096) {
+  if (G > 0 && flop >= 2.0e10 && X >= 128 && B * Rin <= 4096) {
     cudaStream_t st = as_stream(stream);
     void* ws = ttb_scratch((size_t)ttb_band_gemm_ozaki_workspace(n, h, Rin, Rout, X, G), st);
     if (ws) return ttb_band_gemm_ozaki(stream, n, h, Rin, Rout, X, Tp, Mt, out, ws, G);

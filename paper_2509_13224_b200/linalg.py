@@ -58,11 +58,19 @@ _OZAKI_MIN_WORK = 1 << 33          # M N K: only the rounding-sized products (>=
 _OZAKI_CHECK = os.environ.get("TTB_OZAKI_CHECK", "0") == "1"   # debug: compare every emulated product with DMMA
 
 
+_OZAKI_MAX_PAD = 1.6    # padded shapes (M to 128, N and K to 64) run emulated while padded work <= 1.6x
+
+
+def _ozaki_padding_ok(M, N, K):
+    r = lambda v, m: -(-v // m) * m   # noqa: E731
+    return r(M, 128) * r(N, 64) * r(K, 64) <= _OZAKI_MAX_PAD * M * N * K
+
+
 def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False):
     """out = alpha op(A) op(B) + beta out (row-major, FP64 DMMA kernel).
 
-    emulate: large products (M N K >= 2^33, M % 128, N % 64, K % 64, alpha = 1, beta = 0, A not
-    transposed) run as the Ozaki-scheme FP64 GEMM on the INT8 tensor cores (ttb_dgemm_ozaki: 54-bit
+    emulate: large products (M N K >= 2^33, padding to M % 128, N % 64, K % 64 costing <= 1.6x, alpha = 1,
+    beta = 0, A not transposed) run as the Ozaki-scheme FP64 GEMM on the INT8 tensor cores (ttb_dgemm_ozaki: 54-bit
     operands in 7 balanced 8-bit slices, 8 exact int32 level sums; agrees with DGEMM to ~1e-15
     normwise). TTB_OZAKI=0 keeps every product on DMMA."""
     A = _rows(A)
@@ -77,7 +85,7 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False)
     elif out.shape != (M, N) or out.stride(1) != 1:
         raise ValueError("bad gemm output")
     if (emulate and _OZAKI and not tA and alpha == 1.0 and beta == 0.0 and M * N * K >= _OZAKI_MIN_WORK
-            and call_raw("ttb_ozaki_applies", M, N, K)):
+            and _ozaki_padding_ok(M, N, K)):
         ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, K)), dtype=torch.uint8, device=device())
         prof = _GEMM_PROFILE
         if prof is not None:

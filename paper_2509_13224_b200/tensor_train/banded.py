@@ -227,6 +227,6 @@ def compressed_residual(lay, u, F):
     kL, kR = Lf.shape[0], Rf.shape[1]
     Zm = L.gemm(L.gemm(Lf, Fm.reshape(c, n * fr)).reshape(kL * n, fr), Rf).reshape(kL, n, kR)
     out = _a_left(LA, Um, lay, m)                                     # (i, k', y, b)
-    ZA = L.gemm(out.reshape(n * kL, -1), RA.reshape(-1, kR))          # (i, k', kR)
+    ZA = L.gemm(out.reshape(n * kL, -1), RA.reshape(-1, kR), emulate=True)   # (i, k', kR)
     Zm = Zm + L.permute(ZA.reshape(n, kL, kR), (1, 0, 2))
     return left + [Zm] + right, L.nrm2(Zm)

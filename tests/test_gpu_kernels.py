@@ -316,6 +316,10 @@ def test_dgemm_ozaki_fp64_accuracy(tB, graded):
     (256, 128, 16384, 0, 1.0, 0.0),     # split-K, ranges <= 4096, column-sliced B
     (256, 8192, 128, 0, -1.0, 1.0),     # WY trailing update: C -= W2 V (beta epilogue)
     (384, 4096, 256, 1, 0.5, -2.0),     # general alpha / beta
+    (1000, 510, 11011, 0, 1.0, 0.0),    # padded shape (rows, columns, K), split-K partials over the padded tile grid
+    (260, 130, 777, 1, 0.5, -2.0),      # padded, row-sliced B, masked beta epilogue
+    (4000, 68, 8296, 1, 1.0, 0.0),      # padded narrow N (the AMEn right-stage shape), long K
+    (1000, 510, 4099, 0, -1.0, 1.0),    # padded, K ranges > 4096
 ])
 def test_dgemm_ozaki_ex_splitk_beta(M, N, K, tB, alpha, beta):
     """ttb_dgemm_ozaki_ex (split-K, beta) against the DMMA DGEMM: normwise and per element relative to

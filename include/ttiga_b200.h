@@ -249,6 +249,14 @@ int ttb_ozaki_gram_rows(void* stream, int n, int m, const double* T, long long l
 /* Linv = L^{-1} of a lower-triangular row-major n x n L (strict upper triangle ignored), n % 128 == 0;
  * ws: n * n doubles. */
 int ttb_trtri_lower(void* stream, int n, const double* L, long long ldl, double* Li, long long ldi, double* ws);
+/* Row-major lower L (ldl) from the buffer ttb_potrf left (col-major lower factor; its row-major view holds
+ * L^T above the diagonal and the untouched Gram entries below); offmax (device double, nullable) receives
+ * max |G_ij| over the strict lower part (CholeskyQR2's second-Gram test). Replaces triu().t() / tril().abs().max(). */
+int ttb_tri_from_potrf(void* stream, int n, const double* G, long long ldg, double* L, long long ldl, double* offmax);
+/* ||A||_2 estimate of a square row-major matrix by `iters` power-iteration steps on B = A^T A (one DMMA GEMM,
+ * then one cooperative launch; ws: n^2 + 2n + 2 doubles; out: device double). CholeskyQR's one-pass test
+ * cond(L1) <= 4. */
+int ttb_norm2_est(void* stream, int n, const double* A, long long lda, int iters, double* ws, double* out);
 
 #ifdef __cplusplus
 }

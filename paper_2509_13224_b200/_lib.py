@@ -79,6 +79,8 @@ SIGNATURES = {
     "ttb_ozaki_gram_rows_workspace": (i64, [i32, i32]),
     "ttb_ozaki_gram_rows": (i32, [vp, i32, i32, vp, i64, vp, i64, vp]),
     "ttb_trtri_lower": (i32, [vp, i32, vp, i64, vp, i64, vp]),
+    "ttb_tri_from_potrf": (i32, [vp, i32, vp, i64, vp, i64, vp]),
+    "ttb_norm2_est": (i32, [vp, i32, vp, i64, i32, vp, vp]),
     "ttb_band_gemm": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
     "ttb_band_gemm_ozaki_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
     "ttb_band_gemm_ozaki": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i32]),

@@ -241,9 +241,12 @@ def _chol_rows(T, n, m, offdiag=False):
     call("ttb_potrf", n, ptr(G), n, ptr(info))   # col-major lower L: row-major view of the buffer = L^T
     if int(info.item()) != 0:
         return None
-    Lr = torch.triu(G).t().contiguous()
+    Lr = empty(n, n)
     if offdiag:
-        return Lr, float(torch.tril(G, -1).abs().max())
+        off = empty(1)
+        call("ttb_tri_from_potrf", n, ptr(G), n, ptr(Lr), n, ptr(off))
+        return Lr, float(off.item())
+    call("ttb_tri_from_potrf", n, ptr(G), n, ptr(Lr), n, None)
     return Lr
 
 
@@ -261,15 +264,10 @@ def _norm2_est(A, iters=24):
     """||A||_2 of a square device matrix by power iteration on A^T A (seeded start; a lower estimate
     that is within a few percent after 24 steps for the clustered spectra it is used on)."""
     n = A.shape[0]
-    g = torch.Generator(device=A.device).manual_seed(12345)
-    v = torch.randn(n, 1, generator=g, device=A.device, dtype=A.dtype)
-    v /= v.norm()
-    nrm = 0.0
-    for _ in range(iters):
-        w = gemm(A, gemm(A, v), tA=True)                 # A^T A v
-        nrm = w.norm()
-        v = w / nrm
-    return float(nrm) ** 0.5
+    ws = empty(n * n + 2 * n + 2)
+    out = empty(1)
+    call("ttb_norm2_est", n, ptr(A.contiguous()), n, int(iters), ptr(ws), ptr(out))   # one cooperative launch
+    return float(out.item())
 
 
 def _trmm_oz(Li, X, n, m):
@@ -409,8 +407,8 @@ def _gram_jacobi(X, m, n):
     call("ttb_potrf", n, ptr(G), n, ptr(info))   # col-major lower L: row-major view of the buffer = L^T = R
     if int(info.item()) != 0:
         return None
-    R = torch.triu(G)
-    Rt = R.t().contiguous()                      # col-major R (the QR path's layout)
+    Rt = empty(n, n)                             # col-major R (the QR path's layout) = row-major L
+    call("ttb_tri_from_potrf", n, ptr(G), n, ptr(Rt), n, None)
     Vr, S, _ = _jacobi_rt(Rt, n)                 # Jacobi on R^T: its U = X's right singular vectors
     s = S.cpu().numpy()
     if not (s.max() > 0.0 and s.min() >= _GRAM_MIN_RATIO * s.max()):

@@ -125,25 +125,36 @@ def lib():
     return _LIB
 
 
+_current_device = torch._C._cuda_getDevice if hasattr(torch._C, "_cuda_getDevice") else torch.cuda.current_device
+
+
 def stream():
-    """Current torch stream of the device the library runs on (cheap raw-handle path per call)."""
+    """Current torch stream of the device the library runs on, as the raw handle (an int: ctypes passes it
+    as void* through the argtypes; no per-call object construction)."""
     global _DEV_INDEX
     if _DEV_INDEX is None:
         _DEV_INDEX = torch.cuda.current_device()
-    if _raw_stream is not None and torch.cuda.current_device() == _DEV_INDEX:
-        return C.c_void_p(_raw_stream(_DEV_INDEX))
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if _raw_stream is not None and _current_device() == _DEV_INDEX:
+        return _raw_stream(_DEV_INDEX)
+    return torch.cuda.current_stream().cuda_stream
 
 
 def ptr(t):
+    """Device address of a tensor as an int (None for a null pointer)."""
     if t is None:
         return None
-    return C.c_void_p(t.data_ptr())
+    return t.data_ptr()
+
+
+_FNS = {}
 
 
 def call(name, *args):
     """Invoke an entry point with the current torch stream prepended; raise on non-zero status."""
-    rc = getattr(lib(), name)(stream(), *args)
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(lib(), name)
+    rc = fn(stream(), *args)
     if rc != 0:
         raise NativeError(f"{name} returned {rc}")
     return rc
@@ -151,7 +162,10 @@ def call(name, *args):
 
 def call_raw(name, *args):
     """Invoke an entry point that takes no stream (workspace queries)."""
-    return getattr(lib(), name)(*args)
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(lib(), name)
+    return fn(*args)
 
 
 DEV = None

@@ -672,12 +672,18 @@ __device__ __forceinline__ void st_relaxed(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// CROSS: only the 16 pairs between the two blocks (4 rounds of 4 disjoint rotations instead of the
+// 7-round sweep over all 28 pairs): used for every visit but the first of a sweep, so that over a sweep
+// every column pair is rotated exactly once (a block's own pairs at its round-0 visit, every cross pair
+// when its two blocks meet) -- a cyclic-by-blocks ordering -- instead of the intra-block pairs at every
+// one of the 255 visits.
+template <bool CROSS = false>
 __device__ __forceinline__ bool jw_eigen8(double* G, double* J, double tol, int lane) {
   // absent columns (n % 4 != 0) are zero: they pass the test and never rotate
   bool nd = false;
   for (int e = lane; e < 64; e += 32) {
     const int p = e >> 3, q = e & 7;
-    if (p < q) {
+    if (p < q && (!CROSS || (p < 4 && q >= 4))) {
       const double ga = G[e];
       if (!(ga == 0.0 || fabs(ga) <= tol * sqrt(G[p * 9] * G[q * 9]))) nd = true;
     }
@@ -689,9 +695,9 @@ __device__ __forceinline__ bool jw_eigen8(double* G, double* J, double tol, int 
     const double thr2 = 0.0625 * tol * tol;
     const int k1 = lane >> 3, k2 = (lane >> 1) & 3, rr = lane & 1, ji = lane & 7;
 #pragma unroll
-    for (int rd = 0; rd < 7; ++rd) {
-      int p1 = rr_index(k1, rd, 8), q1 = rr_index(7 - k1, rd, 8);
-      int p2 = rr_index(k2, rd, 8), q2 = rr_index(7 - k2, rd, 8);
+    for (int rd = 0; rd < (CROSS ? 4 : 7); ++rd) {
+      int p1 = CROSS ? k1 : rr_index(k1, rd, 8), q1 = CROSS ? 4 + ((k1 + rd) & 3) : rr_index(7 - k1, rd, 8);
+      int p2 = CROSS ? k2 : rr_index(k2, rd, 8), q2 = CROSS ? 4 + ((k2 + rd) & 3) : rr_index(7 - k2, rd, 8);
       if (p1 > q1) { int t = p1; p1 = q1; q1 = t; }
       if (p2 > q2) { int t = p2; p2 = q2; q2 = t; }
       const double a1 = G[p1 * 9], b1 = G[q1 * 9], g1 = G[p1 * 8 + q1];
@@ -719,7 +725,7 @@ __device__ __forceinline__ bool jw_eigen8(double* G, double* J, double tol, int 
 
 __global__ void __launch_bounds__(WS_T) jacobi_wslice_kernel(int n, int RW, double* A, double* V, int* cnt, int* ver,
                                                               int max_sweeps, double tol, int* sweeps_out,
-                                                              long long* prof = nullptr) {
+                                                              long long* prof = nullptr, int cross = 1) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   __shared__ double Gp[2][WS_W][64];
@@ -829,7 +835,10 @@ __global__ void __launch_bounds__(WS_T) jacobi_wslice_kernel(int n, int RW, doub
             J[e] = ((e >> 3) == (e & 7)) ? 1.0 : 0.0;
           }
           __syncwarp();
-          const bool nd = jw_eigen8(G, J, tol, lane);
+          // full visits at round 0 (and round 1 when a dummy block pads an odd block count: the block
+          // paired with the dummy at round 0 gets its own pairs at round 1)
+          const bool nd = (cross && r >= (NBL != nb ? 2 : 1)) ? jw_eigen8<true>(G, J, tol, lane)
+                                                              : jw_eigen8<false>(G, J, tol, lane);
           if (lane == 0) need_s = nd;
         }
         gpar ^= 1;
@@ -935,7 +944,10 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
   int threads = n >= 64 ? JT : ((n + 1) / 2 * 32 > 1024 ? 1024 : ((n + 1) / 2) * 32);
   if (threads < 32) threads = 32;
   const size_t smem = ((size_t)(V ? 2 : 1) * n * n + n) * sizeof(double);
-  if (smem <= 200 * 1024) {
+  // single matrices with n >= 72 (even) take the multi-CTA warp-sliced kernel below: 2-3x faster than the
+  // one-CTA shared-memory sweep from there on (n = 100: 4.3 -> ~1.5 ms; tools/jacobi_wslice_check.py)
+  const bool wslice_ok = batch == 1 && n >= 72 && n % 2 == 0 && work != nullptr;
+  if (smem <= 200 * 1024 && !wslice_ok) {
     static bool cfg = false;
     if (!cfg) {
       cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -943,7 +955,7 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
     }
     jacobi_kernel<true><<<batch, threads, smem, st>>>(n, A, strideA, S, strideS, U, V, strideUV, nullptr, max_sweeps,
                                                       tol, info); ttb_count();
-  } else if (batch > 1 || n <= 128) {
+  } else if (batch > 1 || (n <= 128 && !wslice_ok)) {
     if (!work) return TTB_EARG;
     jacobi_kernel<false><<<batch, JT, 0, st>>>(n, A, strideA, S, strideS, U, V, strideUV, work, max_sweeps, tol, info); ttb_count();
   } else {
@@ -1005,7 +1017,8 @@ TTB_API int ttb_svd_jacobi(void* stream, int n, double* A, long long strideA, do
       }
       int rw = wrw;
       long long* noprof = nullptr;
-      void* args[] = {&n, &rw, &Aw, &Vw, &cnt, &wver, &ms, &tl, &sw, &noprof};
+      static int cross = env_int("TTB_JACOBI_CROSS", 1);   // 0: every visit sweeps all 28 pairs
+      void* args[] = {&n, &rw, &Aw, &Vw, &cnt, &wver, &ms, &tl, &sw, &noprof, &cross};
       e = cudaLaunchCooperativeKernel((const void*)jacobi_wslice_kernel, dim3(nblk), dim3(WS_T), args, wsmem, st); ttb_count();
     } else if (jalg != 1 && gsmem8 <= 200 * 1024) {
       const int GBsel = use16 ? 16 : 8;

@@ -14,8 +14,10 @@ alg = os.environ.get("TTB_JACOBI", "default")
 rng = np.random.default_rng(0)
 CASES = ((130, "gauss"), (256, "gauss"), (512, "gauss"), (1000, "gauss"), (1024, "gauss"), (1024, "graded"),
          (1024, "R^T gram"))
+if os.environ.get("ODD"):
+    CASES = ((130, "gauss"), (134, "graded"), (258, "gauss"), (510, "gauss"), (766, "R^T gram"), (1022, "gauss"))
 if os.environ.get("SMALL"):
-    CASES = ((32, "gauss"), (64, "gauss"), (100, "gauss"), (110, "graded"), (128, "gauss"))
+    CASES = ((32, "gauss"), (64, "gauss"), (72, "gauss"), (100, "gauss"), (110, "graded"), (128, "gauss"))
 for n, kind in CASES:
     X = rng.standard_normal((n, n))
     if kind == "graded":

@@ -26,7 +26,8 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(jacobi_wslice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   int ms = 60;
   double tol = 4e-16 * sqrt((double)n);
-  void* args[] = {&n, &RW, &A, &V, &cnt, &ver, &ms, &tol, &sw, &prof};
+  int cross = getenv("TTB_JACOBI_CROSS") ? atoi(getenv("TTB_JACOBI_CROSS")) : 1;
+  void* args[] = {&n, &RW, &A, &V, &cnt, &ver, &ms, &tol, &sw, &prof, &cross};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);

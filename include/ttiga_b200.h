@@ -200,6 +200,13 @@ int ttb_band_gemm(void* stream, int n, int h, int Rin, int Rout, int X, const do
  * >= 2e10 flop, X >= 128, (2h+1) Rin <= 4096; TTB_BAND_OZAKI=0 disables): Tp sliced once per group of G
  * batches (one exponent per row over the group's G + 2h blocks), Mt per batch; ws:
  * ttb_band_gemm_ozaki_workspace bytes. */
+/* TT-matvec core (tensor_train/core.py tt_matvec, reference core.py:327-338) as ONE Ozaki-scheme FP64 GEMM:
+ * Y (Ra rc, n, Rb rd) [(a,c), i, (b,d)] = sum_j M (Ra, n, m, Rb)[a,i,j,b] G (rc, m, rd)[c,j,d], both operands
+ * sliced from their core layouts, Y written in its core layout (no regrouping passes). Shapes: Ra n Rb % 128,
+ * rc rd % 64, m % 64, rd % 16, Rb, rd <= 64 dividing 256, no split-K (TTB_EARG otherwise). */
+long long ttb_matvec_core_ozaki_workspace(int Ra, int n, int m, int Rb, int rc, int rd);
+int ttb_matvec_core_ozaki(void* stream, int Ra, int n, int m, int Rb, int rc, int rd, const double* M, const double* G,
+                          double* Y, void* ws);
 long long ttb_band_gemm_ozaki_workspace(int n, int h, int Rin, int Rout, int X, int G);
 int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, int X, const double* Tp, const double* Mt,
                         double* out, void* ws, int G);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "ttb_norm2_est": (i32, [vp, i32, vp, i64, i32, vp, vp]),
     "ttb_band_gemm": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
     "ttb_band_gemm_ozaki_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
+    "ttb_matvec_core_ozaki_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
+    "ttb_matvec_core_ozaki": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ttb_band_gemm_ozaki": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i32]),
     "ttb_local_gemm_workspace": (i64, [i32, i32, i32, i32, i32, i32]),
     "ttb_local_gemm_ws_init": (i32, [vp, i32, i32, i32, i32, i32, vp]),

@@ -133,6 +133,9 @@ struct OzOut {
   int mode;
   int trilA;  // A lower triangular (M == K, one K range): row block m0 stops at k = m0 + 128
   int mv, nv; // modes 0 / 2 of a padded product: only rows < mv and columns < nv are written (0: all)
+  // mode 3 (TT-matvec core layout): row r = (a n + i) Rb + b, column c rd + d of the product go to
+  // out[((a rc + c) n + i) Rb rd + b rd + d] (rd % 16 == 0, so a 16-column store segment has one c)
+  int sn, sRb, src_, srd;
 };
 
 // Banded batched mode (ttb_band_gemm_ozaki): batch i multiplies a K window of its group's A slice stack
@@ -336,7 +339,20 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
         __syncwarp();
         double* crow = o.out + (o.mode == 1 ? (long long)(u / tiles) * o.so : 0LL) + (long long)(m0 + q * 32) * o.ldo +
                        n0 + j * 16 + cq;
-        if constexpr (BAND) {
+        if (!BAND && o.mode == 3) {
+          const int col = n0 + j * 16 + cq;
+          const int cc = col / o.srd, dd = col - cc * o.srd;
+          const long long cb = (long long)cc * o.sn * o.sRb * o.srd + dd;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int rr = 2 * i + half;
+            const int r = m0 + q * 32 + rr;
+            const int b = r % o.sRb, ai = r / o.sRb;
+            const int ii = ai % o.sn, a = ai / o.sn;
+            o.out[(((long long)a * o.src_) * o.sn + ii) * o.sRb * o.srd + (long long)b * o.srd + cb] =
+                stg[rr * OA_EPAD + cq];
+          }
+        } else if constexpr (BAND) {
           crow = o.out + (long long)bi * bd.cstride + (long long)(m0 + q * 32) * o.ldo + n0 + j * 16 + cq;
           if (n0 + j * 16 + cq < bd.Rout) {
 #pragma unroll
@@ -1097,6 +1113,108 @@ int ozaki_gemm_padded(cudaStream_t st, int tB, int M, int N, int K, double alpha
     oz_bslice(st, 1, K, N, Np, Kp, B, ldb, 0, K, Kp, Kp, w.bmax, w.fb, w.Bs);
   }
   return oz_run(st, w, Mp, Np, Kp, alpha, beta, C, ldc, 0, 0, M, N);
+}
+
+// ---- TT-matvec core contraction without the two regrouping passes (tensor_train/core.py tt_matvec):
+//   Y[(a, c), i, (b, d)] = sum_j M[a, i, j, b] G[c, j, d]
+// is the GEMM (rows (a, i, b), K = j) x (K = j, columns (c, d)); both operands are sliced straight from
+// their TT-core layout -- every (a, i) block of M and every c block of G is a K x Cb row-major matrix
+// whose Cb columns are rows of the slice stack (block-column slicing, per-row exponents over j) -- and
+// the epilogue writes Y in its core layout (OzOut mode 3). Replaces the 2.15 GB operand permute and
+// the 8.6 GB output permute of the configs[4] step.
+namespace {
+__global__ void __launch_bounds__(256) oz_blkcols_kernel(int K, int Cb, const double* __restrict__ X, int* __restrict__ e,
+                                                         uint8_t* out, long long plane) {
+  __shared__ uint32_t t[OZ_S][64][17];
+  __shared__ double pm[256];
+  __shared__ int es[64];
+  const long long blk = blockIdx.x;
+  const double* Xb = X + blk * (long long)K * Cb;
+  // pass 1: column maxima over K (thread (kr, c): rows kr, kr + 256 / Cb, ...)
+  const int per = 256 / Cb;
+  {
+    const int c = threadIdx.x % Cb, kr = threadIdx.x / Cb;
+    double m = 0.0;
+    if (kr < per)
+      for (int k = kr; k < K; k += per) m = oz_amax(m, __ldg(Xb + (long long)k * Cb + c));
+    pm[threadIdx.x] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < Cb) {
+    double m = 0.0;
+    for (int r = 0; r < per; ++r) m = oz_amax(m, pm[r * Cb + threadIdx.x]);
+    const int ex = oz_exp_of(m);
+    es[threadIdx.x] = ex;
+    e[blk * Cb + threadIdx.x] = ex;
+  }
+  __syncthreads();
+  // pass 2: 64-deep k tiles, transposed through shared memory into rows blk Cb + c of the stack
+  for (int k0 = 0; k0 < K; k0 += 64) {
+    for (int it = threadIdx.x; it < Cb * 16; it += 256) {
+      const int cc = it % Cb, kq = it / Cb;
+      const int ex = es[cc];
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 4 * kq + q;
+        v[q] = k < K ? __ldg(Xb + (long long)k * Cb + cc) : 0.0;
+      }
+      uint32_t w[OZ_S];
+      oz_digits4(v, ex, oz_scale_of(ex), w);
+#pragma unroll
+      for (int q = 0; q < OZ_S; ++q) t[q][cc][kq] = w[q];
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < OZ_S * Cb * 16; it += 256) {
+      const int kq = it & 15, cc = (it >> 4) % Cb, q = (it >> 4) / Cb;
+      const int k = k0 + 4 * kq;
+      if (k < K) *reinterpret_cast<uint32_t*>(out + q * plane + (blk * Cb + cc) * (long long)K + k) = t[q][cc][kq];
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+TTB_API long long ttb_matvec_core_ozaki_workspace(int Ra, int n, int m, int Rb, int rc, int rd) {
+  const long long M = (long long)Ra * n * Rb, N = (long long)rc * rd;
+  if (M > 0x7fffffffLL || N > 0x7fffffffLL) return 0;
+  return ozaki_ws_bytes((int)M, (int)N, m);
+}
+
+// Y (Ra rc, n, Rb rd) = the TT-matvec core of M (Ra, n, m, Rb) and G (rc, m, rd). Shapes: Ra n Rb % 128,
+// rc rd % 64, m % 64, rd % 16 == 0, Rb and rd <= 64 (TTB_EARG otherwise; the caller falls back).
+TTB_API int ttb_matvec_core_ozaki(void* stream, int Ra, int n, int m, int Rb, int rc, int rd, const double* Mc,
+                                  const double* Gc, double* Y, void* ws) {
+  const long long Ml = (long long)Ra * n * Rb, Nl = (long long)rc * rd;
+  if (Ml > 0x7fffffffLL || Nl > 0x7fffffffLL || Ml % OZ_M || Nl % OA_N || m % OA_K || rd % 16 || Rb > 64 || rd > 64 ||
+      Rb < 1 || 256 % Rb || 256 % rd)
+    return TTB_EARG;
+  const int M = (int)Ml, N = (int)Nl;
+  cudaStream_t st = as_stream(stream);
+  OzWs w = oz_ws_layout(ws, M, N, m, 0);
+  oz_blkcols_kernel<<<(unsigned)((long long)Ra * n), 256, 0, st>>>(m, Rb, Mc, w.ea, w.As, (long long)M * m); ttb_count();
+  oz_blkcols_kernel<<<(unsigned)rc, 256, 0, st>>>(m, rd, Gc, w.fb, w.Bs, (long long)N * m); ttb_count();
+  CUtensorMap ta, tb;
+  if (!oz_tmap(&ta, w.As, M, m, OZ_M, OA_K) || !oz_tmap(&tb, w.Bs, N, m, OA_N, OA_K)) return TTB_EARG;
+  const size_t smem = (size_t)OA_ST * OA_SBYTES + 8 * 32 * OA_EPAD * sizeof(double) + 1024;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(oz_gemm_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(oz_gemm_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cfg = true;
+  }
+  const long long tiles = oz_tiles(M, N, 0);
+  int ks, kc;
+  oz_split(tiles, m, &ks, &kc);
+  if (ks > 1) return TTB_EARG;   // the scatter epilogue writes final values: no split-K partials
+  OzOut o{Y, 0, 0, 1.0, 0.0, 3, 0, 0, 0, n, Rb, rc, rd};
+  const int grid = tiles < oz_nsm() ? (int)tiles : oz_nsm();
+  if (kc > OZ_SUB * OA_K)
+    oz_gemm_kernel<8, true><<<grid, 320, smem, st>>>(ta, tb, M, N, m, kc, 1, (int)tiles, 0, w.ea, w.fb, o);
+  else
+    oz_gemm_kernel<8, false><<<grid, 320, smem, st>>>(ta, tb, M, N, m, kc, 1, (int)tiles, 0, w.ea, w.fb, o);
+  ttb_count();
+  return ttb_last_error();
 }
 
 TTB_API long long ttb_ozaki_workspace(int M, int N, int K) { return ozaki_ws_bytes(M, N, K); }

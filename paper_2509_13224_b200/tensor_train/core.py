@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from .. import linalg as L
-from .._lib import call, device, ptr
+from .._lib import call_raw, call, device, ptr
 
 __all__ = [
     "TtShapeError", "TtTensor", "TtMatrix", "tt_add", "tt_sub", "tt_scale", "tt_dot", "tt_norm", "tt_matvec",
@@ -431,6 +431,14 @@ def tt_norm(a):
     return float(n0.item())
 
 
+def _matvec_core_fused(Ra, n, m, Rb, rc, rd):
+    """Whether a dense core contraction takes ttb_matvec_core_ozaki (large, tile-aligned, rd % 16 == 0)."""
+    M, N = Ra * n * Rb, rc * rd
+    return (L._OZAKI and M * N * m >= L._OZAKI_MIN_WORK and M % 128 == 0 and N % 64 == 0 and m % 64 == 0
+            and rd % 16 == 0 and Rb <= 64 and rd <= 64 and 256 % Rb == 0 and 256 % rd == 0
+            and M * m < 2 ** 31 * 64)
+
+
 def tt_matvec(A, x):
     """Operator application, ranks multiply (reference core.py:327-338)."""
     if A.col_sizes != x.mode_sizes:
@@ -445,8 +453,17 @@ def tt_matvec(A, x):
         else:
             Ra, n, m, Rb = M.shape
             rc, _, rd = G.shape
-            T = L.tdot(M, G, ([2], [1]), emulate=True)       # (a, i, b, c, d)
-            Y = L.permute(T, (0, 3, 1, 2, 4)).reshape(Ra * rc, n, Rb * rd)
+            if _matvec_core_fused(Ra, n, m, Rb, rc, rd):
+                # one Ozaki GEMM slicing M and G in their core layouts and writing Y in its own
+                # (ttb_matvec_core_ozaki): no operand / output regrouping passes
+                Y = L.empty(Ra * rc, n, Rb * rd)
+                ws = torch.empty(int(call_raw("ttb_matvec_core_ozaki_workspace", Ra, n, m, Rb, rc, rd)),
+                                 dtype=torch.uint8, device=device())
+                call("ttb_matvec_core_ozaki", Ra, n, m, Rb, rc, rd, ptr(M.contiguous()), ptr(G.contiguous()), ptr(Y),
+                     ptr(ws))
+            else:
+                T = L.tdot(M, G, ([2], [1]), emulate=True)       # (a, i, b, c, d)
+                Y = L.permute(T, (0, 3, 1, 2, 4)).reshape(Ra * rc, n, Rb * rd)
         out.append(Y)
     return TtTensor(out)
 

@@ -23,7 +23,8 @@ import numpy as np
 import torch
 
 from .. import linalg as L
-from .core import TtShapeError, _chop, _rl_orthogonalize
+from .._lib import call, call_raw, ptr
+from .core import TtShapeError, _chop, _matvec_core_fused, _rl_orthogonalize
 
 __all__ = ["tt_matvec_round_host"]
 
@@ -175,11 +176,17 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
             Y = L.empty(Ra * rc, n, Rb * rd)
             Yv = Y.view(Ra, rc, n, Rb, rd)
             xk = xd[len(cores)]
+            fused = _matvec_core_fused(1, n, m, Rb, rc, rd)
+            ws = (torch.empty(int(call_raw("ttb_matvec_core_ozaki_workspace", 1, n, m, Rb, rc, rd)), dtype=torch.uint8,
+                              device=Y.device) if fused else None)
             for a0, a1, tok in slabs:
                 up.wait(tok, comp)
                 for a in range(a0, a1):
-                    T = L.tdot(Md[a], xk, ([1], [1]), emulate=True)    # (i, b, c, d)
-                    L.permute(T, (2, 0, 1, 3), out=Yv[a])              # (c, i, b, d)
+                    if fused:   # one Ozaki GEMM per leading rank index, Y[a] written in its core layout
+                        call("ttb_matvec_core_ozaki", 1, n, m, Rb, rc, rd, ptr(Md[a]), ptr(xk), ptr(Yv[a]), ptr(ws))
+                    else:
+                        T = L.tdot(Md[a], xk, ([1], [1]), emulate=True)    # (i, b, c, d)
+                        L.permute(T, (2, 0, 1, 3), out=Yv[a])              # (c, i, b, d)
             Md.record_stream(comp)
             cores.append(Y)
         for t in xd:

@@ -505,3 +505,23 @@ def test_dgemm_ozaki_nonfinite_propagates(tB):
     Bf[~torch.isfinite(Bf)] = 0.0
     Cd = L.gemm(Af, Bf, tB=bool(tB))
     assert float(((C - Cd).abs()[ok]).max() / Cd.abs().max()) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("Ra,n,m,Rb,rc,rd", [(16, 256, 256, 16, 16, 64), (1, 512, 128, 16, 4, 64), (4, 128, 192, 8, 2, 32)])
+def test_matvec_core_ozaki_layouts(Ra, n, m, Rb, rc, rd):
+    """ttb_matvec_core_ozaki (operands sliced in their TT-core layouts, Y scattered in its core layout) against the
+    DMMA tensordot + permute of tt_matvec: normwise <= 1e-14."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(Ra + n + rd)
+    M = torch.randn(Ra, n, m, Rb, generator=g, dtype=torch.float64, device="cuda")
+    G = torch.randn(rc, m, rd, generator=g, dtype=torch.float64, device="cuda")
+    T = L.tdot(M, G, ([2], [1]))                               # DMMA
+    ref = L.permute(T, (0, 3, 1, 2, 4)).reshape(Ra * rc, n, Rb * rd)
+    Y = torch.full((Ra * rc, n, Rb * rd), float("nan"), dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(call_raw("ttb_matvec_core_ozaki_workspace", Ra, n, m, Rb, rc, rd)), dtype=torch.uint8,
+                     device="cuda")
+    call("ttb_matvec_core_ozaki", Ra, n, m, Rb, rc, rd, ptr(M), ptr(G), ptr(Y), ptr(ws))
+    assert torch.isfinite(Y).all()
+    assert float((Y - ref).norm() / ref.norm()) <= 1e-14

@@ -11,13 +11,30 @@ constexpr int PMAX = 8;
 
 // ---------------------------------------------------------------------------
 // Cox-de Boor (NURBS Book A2.2/A2.3) for one parameter; reference splines.py:146-221.
-__global__ void basis_kernel(int nq, const double* __restrict__ x, const double* __restrict__ t, int nk, int p,
-                             const double* __restrict__ w, int* first, double* V, double* D, int* bad) {
-  int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nq) return;
-  const double xv = x[q];
+// One thread per quadrature point; the (p+1)-long value / derivative records of the CTA's 128 points are
+// staged in shared memory and written as one contiguous, coalesced range per table (a thread-strided
+// store of (p+1)-records would touch p+1 times the sectors per instruction).
+constexpr int BASIS_T = 128;
+__global__ void __launch_bounds__(BASIS_T) basis_kernel(int nq, const double* __restrict__ x, const double* __restrict__ t,
+                                                        int nk, int p, const double* __restrict__ w, int* first,
+                                                        double* V, double* D, int* bad) {
+  __shared__ double sV[BASIS_T * (PMAX + 1)], sD[BASIS_T * (PMAX + 1)];
+  const int q0 = blockIdx.x * BASIS_T;
+  const int q = q0 + threadIdx.x;
+  const int cnt = min(BASIS_T, nq - q0) * (p + 1);
+  const long long base = (long long)q0 * (p + 1);
+  auto flush = [&]() {
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += BASIS_T) {
+      V[base + e] = sV[e];
+      D[base + e] = sD[e];
+    }
+  };
+  const double xq = q < nq ? x[q] : t[0];
+  const bool ok = q < nq && xq >= t[0] && xq <= t[nk - 1];
+  if (q < nq && !ok) atomicMin(bad, q);
+  const double xv = ok ? xq : t[0];   // out-of-range points: evaluated at t[0], records zeroed below
   const int nb = nk - p - 1;
-  if (xv < t[0] || xv > t[nk - 1]) { atomicMin(bad, q); return; }
   int k;
   if (xv >= t[nb]) {
     k = nb - 1;
@@ -74,11 +91,12 @@ __global__ void basis_kernel(int nq, const double* __restrict__ x, const double*
       dN[j] = d;
     }
   }
-  first[q] = k - p;
+  if (q < nq) first[q] = k - p;
   for (int j = 0; j <= p; ++j) {
-    V[(long long)q * (p + 1) + j] = N[j];
-    D[(long long)q * (p + 1) + j] = dN[j];
+    sV[threadIdx.x * (p + 1) + j] = ok ? N[j] : 0.0;
+    sD[threadIdx.x * (p + 1) + j] = ok ? dN[j] : 0.0;
   }
+  flush();
 }
 
 // ---------------------------------------------------------------------------
@@ -564,7 +582,8 @@ TTB_API int ttb_basis_eval(void* stream, int nq, const double* x, const double* 
                            const double* weights, int* first, double* V, double* D, int* bad) {
   if (p < 0 || p > PMAX || nk < 2 * p + 2) return TTB_EARG;
   if (nq == 0) return TTB_OK;
-  basis_kernel<<<ceil_div(nq, 128), 128, 0, as_stream(stream)>>>(nq, x, knots, nk, p, weights, first, V, D, bad); ttb_count();
+  basis_kernel<<<ceil_div(nq, BASIS_T), BASIS_T, 0, as_stream(stream)>>>(nq, x, knots, nk, p, weights, first, V, D, bad);
+  ttb_count();
   return ttb_last_error();
 }
 

@@ -214,8 +214,8 @@ def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step):
         achieved = float(OZ_PAIRS) * fp64_eq
         rec.update(pipe=("INT8 tcgen05.mma kind::i8 (Ozaki-scheme FP64 emulation: 7 balanced int8 slices per operand, "
                          "8 levels = 34 exact slice products)"),
-                   kernel=(f"oz_gemm_kernel, C({M}x{N}) = A({M}x{K}) B({K}x{N}): the matvec, right-to-left carry, "
-                           f"S Vt carry and implicit-U products of the step (all this shape)"),
+                   kernel=(f"oz_gemm_kernel, C({M}x{N}) = A({M}x{K}) B({K}x{N}) ({len(recs) / steps:g} launches per step: "
+                           f"the products of the step with the largest share of device time)"),
                    timed="whole ttb_dgemm_ozaki calls (operand slicing + oz_gemm_kernel), CUDA events on the launching stream",
                    achieved=achieved, peak=peak, unit="TOPS", frac=achieved / peak,
                    frac_of_burst_peak=(achieved / (2.0 * burst)) if burst else None,

@@ -459,8 +459,15 @@ def tt_matvec(A, x):
                 Y = L.empty(Ra * rc, n, Rb * rd)
                 ws = torch.empty(int(call_raw("ttb_matvec_core_ozaki_workspace", Ra, n, m, Rb, rc, rd)),
                                  dtype=torch.uint8, device=device())
+                prof = L._GEMM_PROFILE
+                if prof is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
                 call("ttb_matvec_core_ozaki", Ra, n, m, Rb, rc, rd, ptr(M.contiguous()), ptr(G.contiguous()), ptr(Y),
                      ptr(ws))
+                if prof is not None:
+                    e1.record()
+                    prof.append((e0, e1, 2.0 * Ra * n * Rb * rc * rd * m, "ozaki", (Ra * n * Rb, rc * rd, m)))
             else:
                 T = L.tdot(M, G, ([2], [1]), emulate=True)       # (a, i, b, c, d)
                 Y = L.permute(T, (0, 3, 1, 2, 4)).reshape(Ra * rc, n, Rb * rd)

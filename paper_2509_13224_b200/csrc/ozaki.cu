@@ -55,6 +55,21 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// multicast variant: the box lands at the same shared-memory offset in every CTA of ctamask and signals
+// the mbarrier at the same offset in each of them
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t mbar,
+                                               uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(mbar), "h"(ctamask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 // ---- all levels in one pass: 128 x 64 tiles, every k stage (64 bytes of K) holds all 7 A and all 7 B
 // slices (84 KB, 2-stage ring, 64-byte swizzle), the 34 slice-pair MMAs accumulate into 8 TMEM
 // accumulators of 64 columns (all 512), and C is written once.
@@ -166,7 +181,10 @@ __device__ __forceinline__ void oz_tile(int t, int ntn, int sym, int& m0, int& n
   n0 = (2 * mt + t) * OA_N;
 }  // k steps (of 64) per TMEM accumulation: K <= 4096 keeps every level sum exact in int32
 
-template <int LEV, bool LONGK, bool BAND = false>  // LONGK: K ranges deeper than OZ_SUB k steps
+// CL = 2: 2-CTA clusters whose CTAs take consecutive units (same A rows, same K range, in lockstep); the A
+// slice tiles are loaded once by rank 0 and multicast into both CTAs' shared memory, and every stage is
+// released only when both CTAs' MMAs are done with it (empty barriers count one commit from each)
+template <int LEV, bool LONGK, bool BAND = false, int CL = 1>  // LONGK: K ranges deeper than OZ_SUB k steps
 __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                                                         int kchunk, int ksplit, int tiles, int sym,
@@ -186,7 +204,7 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
   if (tid == 32) {
     for (int s = 0; s < OA_ST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&empty[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&empty[s])), "r"(CL));
     }
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tfull)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(&tempty)));
@@ -196,8 +214,10 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync_all();   // peer barriers initialised before any multicast / commit
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
+  const int crank = CL == 2 ? (int)(blockIdx.x & 1) : 0;
   // work unit u: K range u / tiles (kchunk deep), tile u % tiles (n fastest, so CTAs that run
   // together share the A rows); a range is accumulated in TMEM OZ_SUB k steps at a time
   const int ntn = (BAND ? bd.Np : N) / OA_N, units = BAND ? tiles * bd.nb : tiles * ksplit;
@@ -235,10 +255,17 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
             tma_load_3d(base, &tmA, (bi - gi * bd.G) * bd.Rin + kt * OA_K, m0, OZ_S * gi, fbar);
             tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, OZ_S * bi, fbar);
           } else {
-            tma_load_3d(base, &tmA, kt * OA_K, m0, 0, fbar);
+            if constexpr (CL == 2) {
+              if (crank == 0) tma_load_3d_mc(base, &tmA, kt * OA_K, m0, 0, fbar, (uint16_t)3);
+            } else {
+              tma_load_3d(base, &tmA, kt * OA_K, m0, 0, fbar);
+            }
             tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, 0, fbar);
           }
         }
+      }
+      if constexpr (CL == 2) {   // drain: every commit (own and peer) of the last stages has arrived
+        for (int j = (it > OA_ST ? it - OA_ST : 0); j < it; ++j) mbar_wait(smem_u32(&empty[j % OA_ST]), (j / OA_ST) & 1);
       }
     }
   } else if (warp == 1) {
@@ -261,8 +288,14 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
             const uint64_t da = sw_desc(a0), db = sw_desc(b0);
 #pragma unroll
             for (int kk = 0; kk < OA_K / 32; ++kk) oz_issue<LEV>(tmem, da, db, kk, kt == ks && kk == 0);
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                smem_u32(&empty[st])));
+            if constexpr (CL == 2)
+              asm volatile(
+                  "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                      smem_u32(&empty[st])),
+                  "h"((uint16_t)3));
+            else
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                  smem_u32(&empty[st])));
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
               smem_u32(&tfull)));
@@ -393,6 +426,7 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync_all();   // no CTA leaves while its peer may still signal it
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
 }
 
@@ -864,6 +898,32 @@ __global__ void oz_mirror_kernel(int n, double* G, long long ldg) {
   }
 }
 
+template <int LEV, bool LONGK>
+int oz_launch_cluster(cudaStream_t st, int grid, size_t smem, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
+                      int K, int kc, int ks, int tiles, int sym, const int* ea, const int* fb, const OzOut& o) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(oz_gemm_kernel<LEV, LONGK, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cfg = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(320);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const OzBand nob{};
+  const cudaError_t e = cudaLaunchKernelEx(&lc, oz_gemm_kernel<LEV, LONGK, false, 2>, ta, tb, M, N, K, kc, ks, tiles, sym,
+                                           ea, fb, o, nob);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
 // the int8 GEMM over prepared slices + split-K reduction (+ mirror for sym)
 int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, double beta, double* C, long long ldc,
            int sym, int trilA = 0, int mv = 0, int nv = 0) {
@@ -891,7 +951,18 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
     o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2, trilA && M == K ? 1 : 0, mv, nv};
   const long long units = tiles * ks;
   const int grid = units < oz_nsm() ? (int)units : oz_nsm();
-  if (kc > OZ_SUB * OA_K)
+  // 2-CTA clusters that multicast the A tiles (TTB_OZAKI_CLUSTER: 0 off, 1 Grams only (default), 2 all):
+  // the Grams (both operands one slice stack, ~148 CTAs reading the same k-slabs) are shared-bandwidth
+  // bound (profiles/README.md), multicast halves their A traffic: 18.5 -> 15.4 ms on 1024 x 1M
+  static const int cluster_mode = getenv("TTB_OZAKI_CLUSTER") ? atoi(getenv("TTB_OZAKI_CLUSTER")) : 1;
+  const bool cluster = levels == 8 && tiles % 2 == 0 && grid % 2 == 0 && (cluster_mode == 2 || (cluster_mode == 1 && sym));
+  if (cluster && kc > OZ_SUB * OA_K) {
+    const int e = oz_launch_cluster<8, true>(st, grid, smem, ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
+    if (e) return e;
+  } else if (cluster) {
+    const int e = oz_launch_cluster<8, false>(st, grid, smem, ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
+    if (e) return e;
+  } else if (kc > OZ_SUB * OA_K)
     oz_gemm_kernel<8, true><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
   else if (levels == 7)
     oz_gemm_kernel<7, false><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);

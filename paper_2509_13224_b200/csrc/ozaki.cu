@@ -252,7 +252,12 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
           const uint32_t base = smem_u32(sm + st * OA_SBYTES);
           if constexpr (BAND) {
             const int gi = bi / bd.G;
-            tma_load_3d(base, &tmA, (bi - gi * bd.G) * bd.Rin + kt * OA_K, m0, OZ_S * gi, fbar);
+            if constexpr (CL == 2) {
+              if (crank == 0)
+                tma_load_3d_mc(base, &tmA, (bi - gi * bd.G) * bd.Rin + kt * OA_K, m0, OZ_S * gi, fbar, (uint16_t)3);
+            } else {
+              tma_load_3d(base, &tmA, (bi - gi * bd.G) * bd.Rin + kt * OA_K, m0, OZ_S * gi, fbar);
+            }
             tma_load_3d(base + OZ_S * OA_ABYTES, &tmB, kt * OA_K, n0, OZ_S * bi, fbar);
           } else {
             if constexpr (CL == 2) {
@@ -1165,6 +1170,31 @@ TTB_API int ttb_band_gemm_ozaki(void* stream, int n, int h, int Rin, int Rout, i
   const int grid = units < oz_nsm() ? (int)units : oz_nsm();
   OzOut o{out, Rout, 0, 1.0, 0.0, 0, 0};
   OzBand bd{G, w.Rp, w.Mp, w.Np, w.Kp, X, Rout, n, (long long)X * Rout};
+  // the n-tiles of one batch share its A window: 2-CTA clusters multicast it (TTB_BAND_CLUSTER=0 disables)
+  static const bool bcl = getenv("TTB_BAND_CLUSTER") == nullptr || getenv("TTB_BAND_CLUSTER")[0] != '0';
+  if (bcl && tiles % 2 == 0 && grid % 2 == 0) {
+    static bool cfg2 = false;
+    if (!cfg2) {
+      cudaFuncSetAttribute(oz_gemm_kernel<8, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg2 = true;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(320);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&lc, oz_gemm_kernel<8, false, true, 2>, ta, tb, w.Mp, w.Np, w.Kp, w.Kp, 1,
+                                             tiles, 0, (const int*)w.ea, (const int*)w.fb, o, bd);
+    ttb_count();
+    return e == cudaSuccess ? ttb_last_error() : (int)e;
+  }
   oz_gemm_kernel<8, false, true><<<grid, 320, smem, st>>>(ta, tb, w.Mp, w.Np, w.Kp, w.Kp, 1, tiles, 0, w.ea, w.fb, o, bd);
   ttb_count();
   return ttb_last_error();

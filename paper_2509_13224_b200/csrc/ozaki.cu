@@ -770,6 +770,65 @@ __global__ void __launch_bounds__(256) oz_rowslice_fused_kernel(int rows, int K,
   }
 }
 
+// The same with the rows staged in shared memory by 1-D bulk copies (cp.async.bulk, one per row of K * 8
+// bytes, 16-byte aligned rows): 8 rows per CTA, <= 64 KB, so 3 CTAs per SM keep ~190 KB of loads in flight
+// per SM with few registers, and the load / slice / store phases of different CTAs overlap. The register
+// version (oz_rowslice_fused_kernel, 94 registers: 2 CTAs per SM) reached 3.6 TB/s on 1M x 1024.
+template <int NQ>
+__global__ void __launch_bounds__(256) oz_rowslice_bulk_kernel(int rows, int K, const double* __restrict__ X,
+                                                                long long ld, int* __restrict__ e, uint8_t* out) {
+  extern __shared__ __align__(128) double oz_rs[];
+  __shared__ __align__(8) unsigned long long bar[8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + w;
+  if (r >= rows) return;
+  const double* row = oz_rs + (size_t)w * K;
+  const uint32_t mb = smem_u32(&bar[w]);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(K * 8) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(row)),
+                 "l"(X + (long long)r * ld), "r"(K * 8), "r"(mb)
+                 : "memory");
+  }
+  __syncwarp();
+  mbar_wait(mb, 0);
+  const int kq = K / 4;
+  const long long plane = (long long)rows * K;
+  double m = 0.0;
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int q = lane + 32 * j;
+    if (q < kq) {
+      const double2 a = reinterpret_cast<const double2*>(row + 4 * q)[0];
+      const double2 b = reinterpret_cast<const double2*>(row + 4 * q)[1];
+      m = oz_amax(oz_amax(m, a.x), a.y);
+      m = oz_amax(oz_amax(m, b.x), b.y);
+    }
+  }
+  for (int o = 16; o; o >>= 1) m = oz_amax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int ex = oz_exp_of(m);
+  if (lane == 0) e[r] = ex;
+  const double sc = oz_scale_of(ex);
+  uint8_t* o = out + (long long)r * K;
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int q = lane + 32 * j;
+    if (q < kq) {
+      const double2 a = reinterpret_cast<const double2*>(row + 4 * q)[0];
+      const double2 b = reinterpret_cast<const double2*>(row + 4 * q)[1];
+      const double v[4] = {a.x, a.y, b.x, b.y};
+      uint32_t wd[OZ_S];
+      oz_digits4(v, ex, sc, wd);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane + 4 * q) = wd[s];
+    }
+  }
+}
+
 // Row exponent + slicing with zero padding to Mp x Kp (any K): one warp per row, max pass then slice pass
 // (the second read of the row hits L1/L2); rows >= rows are zero with exponent 0.
 __global__ void __launch_bounds__(256) oz_prows_kernel(int rows, int K, const double* __restrict__ X, long long ld,
@@ -803,6 +862,12 @@ __global__ void __launch_bounds__(256) oz_prows_kernel(int rows, int K, const do
   }
 }
 
+// TTB_OZ_BULK=0: the register-staged slicers (A/B comparison)
+bool oz_bulk_rows() {
+  static const bool on = getenv("TTB_OZ_BULK") == nullptr || getenv("TTB_OZ_BULK")[0] != '0';
+  return on;
+}
+
 // exponents (and slices) of the rows of a row-major (rows x K, ld) operand
 void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, int* e, unsigned long long* rmax,
              uint8_t* out) {
@@ -810,6 +875,22 @@ void oz_rows(cudaStream_t st, int rows, int K, const double* X, long long ld, in
     cudaMemsetAsync(rmax, 0, sizeof(unsigned long long) * rows, st);
     oz_rowmax_kernel<<<dim3(ceil_div(rows, 8), ceil_div(K, 8192)), 256, 0, st>>>(rows, K, X, ld, rmax); ttb_count();
     oz_colexp_kernel<<<ceil_div(rows, 256), 256, 0, st>>>(rows, rmax, e); ttb_count();
+  } else if (K % 4 == 0 && K <= 128 * 8 && oz_bulk_rows() &&
+             ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)(ld * 8)) & 15) == 0) {
+    const unsigned g = (unsigned)ceil_div((long long)rows, 8);
+    const size_t sm = (size_t)8 * K * sizeof(double);
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(oz_rowslice_bulk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(oz_rowslice_bulk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(oz_rowslice_bulk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cfg = true;
+    }
+    if (K <= 128 * 2) oz_rowslice_bulk_kernel<2><<<g, 256, sm, st>>>(rows, K, X, ld, e, out);
+    else if (K <= 128 * 4) oz_rowslice_bulk_kernel<4><<<g, 256, sm, st>>>(rows, K, X, ld, e, out);
+    else oz_rowslice_bulk_kernel<8><<<g, 256, sm, st>>>(rows, K, X, ld, e, out);
+    ttb_count();
+    return;
   } else if (K % 4 == 0 && K <= 128 * 16) {
     const unsigned g = (unsigned)ceil_div((long long)rows * 32, 256);
     if (K <= 128 * 2) oz_rowslice_fused_kernel<2><<<g, 256, 0, st>>>(rows, K, X, ld, e, out);
@@ -882,8 +963,91 @@ __global__ void __launch_bounds__(256) oz_cols_fused_kernel(int K, int cols, con
   }
 }
 
+// Column exponent + transposed slicing with the CTA's 8 columns x K rows (64-byte row segments, <= 64 KB)
+// staged in shared memory by 16-byte cp.async: the operand is read from DRAM exactly once (the two-pass
+// oz_cols_fused_kernel re-reads its tile and, with ~5 CTAs x 512 KB per SM in flight, misses L2: 17.2 GB
+// read for an 8.6 GB operand). Row k sits at smem row k ^ ((k >> 4) & 1) so that the slice pass (thread =
+// one column x 16 consecutive k; a warp covers 4 such k-groups 16 rows apart) reads conflict-free; it
+// writes 16 bytes per slice plane (out[s][c][k], K contiguous).
+__global__ void __launch_bounds__(256) oz_cols_stage_kernel(int K, int cols, const double* __restrict__ X, long long ld,
+                                                            int* __restrict__ e, uint8_t* out) {
+  extern __shared__ __align__(128) double oz_cs[];   // [K][8]
+  __shared__ double pm[8][4][2];
+  __shared__ int es[8];
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  const int c0 = blockIdx.x * 8;
+  const long long plane = (long long)cols * K;
+  for (int idx = t; idx < 4 * K; idx += 256) {
+    const int k = idx >> 2, ch = idx & 3;
+    const int ks = k ^ ((k >> 4) & 1);
+    const uint32_t dst = smem_u32(oz_cs + ks * 8 + 2 * ch);
+    const double* src = X + (long long)k * ld + c0 + 2 * ch;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  {
+    // column maxima: thread t always sees 16-byte chunk t & 3 (columns 2 (t & 3), 2 (t & 3) + 1)
+    double m0 = 0.0, m1 = 0.0;
+    for (int idx = t; idx < 4 * K; idx += 256) {
+      const double2 v = reinterpret_cast<const double2*>(oz_cs)[idx];
+      m0 = oz_amax(m0, v.x);
+      m1 = oz_amax(m1, v.y);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      m0 = oz_amax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+      m1 = oz_amax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    if (lane < 4) {
+      pm[wp][lane][0] = m0;
+      pm[wp][lane][1] = m1;
+    }
+  }
+  __syncthreads();
+  if (t < 8) {
+    double m = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m = oz_amax(m, pm[w][t >> 1][t & 1]);
+    const int ex = oz_exp_of(m);
+    es[t] = ex;
+    e[c0 + t] = ex;
+  }
+  __syncthreads();
+  const int c = t & 7;
+  const int ex = es[c];
+  const double sc = oz_scale_of(ex);
+  uint8_t* o = out + (long long)(c0 + c) * K;
+  for (int kb = (t >> 3) * 16; kb < K; kb += 32 * 16) {
+    uint32_t wd[4][OZ_S];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = kb + 4 * g + u;
+        v[u] = oz_cs[(k ^ ((k >> 4) & 1)) * 8 + c];
+      }
+      oz_digits4(v, ex, sc, wd[g]);
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < OZ_S; ++s2)
+      *reinterpret_cast<uint4*>(o + s2 * plane + kb) = make_uint4(wd[0][s2], wd[1][s2], wd[2][s2], wd[3][s2]);
+  }
+}
+
 void oz_cols(cudaStream_t st, int K, int cols, const double* X, long long ld, int* e, unsigned long long* cmax,
              uint8_t* out) {
+  if (K <= 1024 && K % 16 == 0 && cols % 8 == 0 && oz_bulk_rows() &&
+      ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)(ld * 8)) & 15) == 0) {
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(oz_cols_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cfg = true;
+    }
+    oz_cols_stage_kernel<<<cols / 8, 256, (size_t)K * 64, st>>>(K, cols, X, ld, e, out); ttb_count();
+    return;
+  }
   if (K <= 2048) {
     oz_cols_fused_kernel<<<ceil_div(cols, 64), 256, 0, st>>>(K, cols, X, ld, e, out); ttb_count();
     return;

@@ -246,6 +246,11 @@ int ttb_dgemm_ozaki_ex(void* stream, int tB, int M, int N, int K, double alpha, 
  * only the k steps below its diagonal block (half the work). B row-major M x N; ws as ttb_ozaki_workspace(M, N, M). */
 int ttb_dgemm_ozaki_trilA(void* stream, int M, int N, const double* A, long long lda, const double* B, long long ldb,
                           double* C, long long ldc, void* ws);
+/* C = A B with B (N x N) upper triangular (strict lower triangle zero): each 64-column block of C runs only
+ * the k steps above its diagonal block (~half the work). A row-major M x N; ws as ttb_ozaki_workspace(M, N, N).
+ * Q = X R^-1 of a rounding step certified full rank (reference tensor_train/core.py:377-386 with keep == r1). */
+int ttb_dgemm_ozaki_triuB(void* stream, int M, int N, const double* A, long long lda, const double* B, long long ldb,
+                          double* C, long long ldc, void* ws);
 /* Gram matrix G (n x n) = X^T X of a row-major m x n X, FP64 via the Ozaki scheme (columns sliced once,
  * upper block triangle computed, mirrored); n % 128 == 0, m % 64 == 0 (else workspace 0 / TTB_EARG). */
 long long ttb_ozaki_gram_workspace(int m, int n); /* bytes */

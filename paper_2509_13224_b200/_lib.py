@@ -74,6 +74,7 @@ SIGNATURES = {
     "ttb_dgemm_ozaki": (i32, [vp, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
     "ttb_dgemm_ozaki_ex": (i32, [vp, i32, i32, i32, i32, f64, vp, i64, vp, i64, f64, vp, i64, vp]),
     "ttb_dgemm_ozaki_trilA": (i32, [vp, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
+    "ttb_dgemm_ozaki_triuB": (i32, [vp, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
     "ttb_ozaki_gram_workspace": (i64, [i32, i32]),
     "ttb_ozaki_gram": (i32, [vp, i32, i32, vp, i64, vp, i64, vp]),
     "ttb_ozaki_gram_rows_workspace": (i64, [i32, i32]),

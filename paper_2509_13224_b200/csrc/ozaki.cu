@@ -146,7 +146,8 @@ struct OzOut {
   long long ldo, so;
   double alpha, beta;
   int mode;
-  int trilA;  // A lower triangular (M == K, one K range): row block m0 stops at k = m0 + 128
+  int trilA;  // 1: A lower triangular (M == K, one K range): row block m0 stops at k = m0 + 128;
+              // 2: B upper triangular (N == K, one K range): column block n0 stops at k = n0 + 64
   int mv, nv; // modes 0 / 2 of a padded product: only rows < mv and columns < nv are written (0: all)
   // mode 3 (TT-matvec core layout): row r = (a n + i) Rb + b, column c rd + d of the product go to
   // out[((a rc + c) n + i) Rb rd + b rd + d] (rd % 16 == 0, so a 16-column store segment has one c)
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
       bi = 0;
       oz_tile(u % tiles, ntn, sym, m0, n0);
       kt0 = (u / tiles) * (kchunk / OA_K);
-      kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA ? m0 + OZ_M : K) / OA_K;
+      kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA == 1 ? m0 + OZ_M : (o.trilA == 2 ? n0 + OA_N : K)) / OA_K;
     }
   };
   if (warp == 0) {
@@ -1117,7 +1118,8 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   if (ks > 1)
     o = OzOut{w.part, N, (long long)M * N, 1.0, 0.0, 1, 0};
   else
-    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2, trilA && M == K ? 1 : 0, mv, nv};
+    o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2,
+              trilA == 1 && M == K ? 1 : (trilA == 2 && N == K ? 2 : 0), mv, nv};
   const long long units = tiles * ks;
   const int grid = units < oz_nsm() ? (int)units : oz_nsm();
   // 2-CTA clusters that multicast the A tiles (TTB_OZAKI_CLUSTER: 0 off, 1 Grams only (default), 2 all):
@@ -1507,6 +1509,20 @@ TTB_API int ttb_dgemm_ozaki_trilA(void* stream, int M, int N, const double* A, l
   oz_rows(st, M, M, A, lda, w.ea, w.amax, w.As);
   oz_cols(st, M, N, B, ldb, w.fb, w.bmax, w.Bs);
   return oz_run(st, w, M, N, M, 1.0, 0.0, C, ldc, 0, 1);
+}
+
+// C = A B with B (N x N, ldb) upper triangular (its strict lower triangle must be zero): column block
+// n0 of C only runs the k steps below n0 + 64 (~half the work; Q = X R^-1 of the rounding's certified
+// full-rank cores, output row-major as the core layout wants it). A: row-major M x N (lda).
+// ws: ttb_ozaki_workspace(M, N, N) bytes.
+TTB_API int ttb_dgemm_ozaki_triuB(void* stream, int M, int N, const double* A, long long lda, const double* B,
+                                  long long ldb, double* C, long long ldc, void* ws) {
+  if (!oz_shape_ok(M, N, N)) return TTB_EARG;
+  cudaStream_t st = as_stream(stream);
+  OzWs w = oz_ws_layout(ws, M, N, N, 0);
+  oz_rows(st, M, N, A, lda, w.ea, w.amax, w.As);
+  oz_cols(st, N, N, B, ldb, w.fb, w.bmax, w.Bs);
+  return oz_run(st, w, M, N, N, 1.0, 0.0, C, ldc, 0, 2);
 }
 
 // General form: C = alpha A op(B) + beta C.

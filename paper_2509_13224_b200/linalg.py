@@ -118,6 +118,34 @@ def gemm(A, B, tA=False, tB=False, alpha=1.0, beta=0.0, out=None, emulate=False)
     return out
 
 
+def gemm_triu(A, W, out=None):
+    """out = A W for a row-major A (M x N) and an upper-triangular W (N x N, strict lower triangle zero):
+    the Ozaki GEMM that skips the zero k steps of every column block (ttb_dgemm_ozaki_triuB) when the
+    shape takes it, else the general product."""
+    A = _rows(A)
+    W = _rows(W)
+    M, N = A.shape
+    if W.shape != (N, N):
+        raise ValueError("gemm_triu: W must be N x N")
+    if not (_OZAKI and M * N * N >= _OZAKI_MIN_WORK and call_raw("ttb_ozaki_applies", M, N, N)):
+        return gemm(A, W, out=out, emulate=True)
+    if out is None:
+        out = empty(M, N)
+    elif out.shape != (M, N) or out.stride(1) != 1:
+        raise ValueError("bad gemm output")
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, N)), dtype=torch.uint8, device=device())
+    prof = _GEMM_PROFILE
+    if prof is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+    call("ttb_dgemm_ozaki_triuB", M, N, ptr(A), max(A.stride(0), 1), ptr(W), N, ptr(out), max(out.stride(0), 1), ptr(ws))
+    if prof is not None:
+        e1.record()
+        prof.append((e0, e1, 1.0 * M * N * (N + 64), "ozaki-triu", (M, N, N)))
+    return out
+
+
 def gemm_strided(tA, tB, M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, alpha=1.0, beta=0.0):
     """Strided-batched C_b = alpha op(A_b) op(B_b) + beta C_b on raw device tensors (row-major views;
     A, B, C are tensors whose data_ptr is the first batch's first element)."""
@@ -263,11 +291,16 @@ _CHOLQR1_KAPPA = float(os.environ.get("TTB_CHOLQR_ONEPASS_KAPPA", "4"))
 def _norm2_est(A, iters=24):
     """||A||_2 of a square device matrix by power iteration on A^T A (seeded start; a lower estimate
     that is within a few percent after 24 steps for the clustered spectra it is used on)."""
+    return float(_norm2_est_dev(A, iters).item())
+
+
+def _norm2_est_dev(A, iters=24):
+    """_norm2_est as a 1-element device tensor (no host sync)."""
     n = A.shape[0]
     ws = empty(n * n + 2 * n + 2)
     out = empty(1)
     call("ttb_norm2_est", n, ptr(A.contiguous()), n, int(iters), ptr(ws), ptr(out))   # one cooperative launch
-    return float(out.item())
+    return out
 
 
 def _trmm_oz(Li, X, n, m):
@@ -390,13 +423,48 @@ _GRAM_MIN_M = int(os.environ.get("TTB_SVD_GRAM_MIN_M", str(1 << 19)))
 _GRAM_MIN_RATIO = 1e-4   # s_min / s_max: singular values from X^T X carry relative error ~ eps (s_max / s)^2
 
 
-def _gram_jacobi(X, m, n):
+# Full-rank certificate of a rounding step (reference tensor_train/core.py:377-386). _chop keeps every
+# singular value of the unfolding X when the smallest one exceeds delta (the tail of dropping even one is
+# s_min > delta), and then U[:, :keep] diag(s) Vt = X = Q R: the step's output core may be the QR factor Q
+# and its carry R -- the same tensor, the same ranks, the same left-orthogonality, without the SVD. The
+# certificate is rigorous: for the triangular factor L (X^T X = L L^T, so X and L share singular values)
+#   s_min(X) = 1 / ||L^-1||_2 >= 1 / ||L^-1||_F,
+# with a factor 2 of margin over delta for the rounding of L and L^-1. Only taken for the large factors
+# (n >= 256, n % 128 == 0) where the Jacobi SVD costs milliseconds; TTB_ROUND_FULLRANK_QR=0 disables it.
+_FULLRANK = os.environ.get("TTB_ROUND_FULLRANK_QR", "1") != "0"
+_FULLRANK_MIN_N = 256
+_FULLRANK_MARGIN = 2.0
+
+
+def _fullrank_wanted(delta, m, n, want_v):
+    return (_FULLRANK and delta is not None and delta > 0.0 and not want_v and m >= n >= _FULLRANK_MIN_N
+            and n % 128 == 0)
+
+
+def _fullrank_inverse(Lr, n, delta, cond_max=None):
+    """L^-1 (row-major lower) of the row-major lower-triangular Lr when 1 / ||L^-1||_F > 2 delta (and,
+    with cond_max, the power-iteration estimate of cond_2(L) is <= cond_max), else None. One host sync."""
+    Li = _trtri(Lr, n)
+    vals = [nrm2(Li).reshape(1)]
+    if cond_max is not None:
+        vals += [_norm2_est_dev(Lr), _norm2_est_dev(Li)]
+    v = torch.cat(vals).cpu().numpy()
+    if not (np.isfinite(v).all() and v[0] > 0.0 and 1.0 / v[0] > _FULLRANK_MARGIN * delta):
+        return None
+    if cond_max is not None and not (1.1 * v[1] * v[2] <= cond_max):
+        return None
+    return Li
+
+
+def _gram_jacobi(X, m, n, fullrank_delta=None):
     """Right singular vectors and singular values of a very tall X (m x n) without its QR: R from the
     Cholesky factor of G = X^T X (Ozaki-scheme FP64 Gram on the int8 tensor cores), then the same
     one-sided Jacobi on R^T as the QR path (R^T R = G, so R differs from the Householder R only by row
     signs and rounding). Used only when X is well conditioned (s_min >= 1e-4 s_max over ALL singular
     values, so eps (s_max / s)^2 <= 1e-8 relative and <= 1e-12 s_max absolute); returns
-    (Rt, Vr, S) or None (the caller takes the Householder QR path)."""
+    (Rt, Vr, S) or None (the caller takes the Householder QR path). With ``fullrank_delta`` the
+    full-rank certificate is tried first on the Cholesky factor (same conditioning limit, by estimate):
+    certified, returns (Rt, L^-1, None) and no SVD is computed."""
     if not (_GRAM and _OZAKI and m >= _GRAM_MIN_M and n >= 256 and n % 128 == 0 and m % 64 == 0):
         return None
     ws = torch.empty(int(call_raw("ttb_ozaki_gram_workspace", m, n)), dtype=torch.uint8, device=device())
@@ -409,6 +477,10 @@ def _gram_jacobi(X, m, n):
         return None
     Rt = empty(n, n)                             # col-major R (the QR path's layout) = row-major L
     call("ttb_tri_from_potrf", n, ptr(G), n, ptr(Rt), n, None)
+    if fullrank_delta is not None:
+        Li = _fullrank_inverse(Rt, n, fullrank_delta, cond_max=1.0 / _GRAM_MIN_RATIO)
+        if Li is not None:
+            return Rt, Li, None
     Vr, S, _ = _jacobi_rt(Rt, n)                 # Jacobi on R^T: its U = X's right singular vectors
     s = S.cpu().numpy()
     if not (s.max() > 0.0 and s.min() >= _GRAM_MIN_RATIO * s.max()):
@@ -425,15 +497,21 @@ class SVDFactors:
     Tall X = Q R: Jacobi on R.  Wide X (X^T = Q R): Jacobi on R^T.
     """
 
-    def __init__(self, X, want_v=False):
+    def __init__(self, X, want_v=False, fullrank_delta=None):
+        """fullrank_delta: the rounding step's truncation threshold; when the full-rank certificate
+        (see _fullrank_inverse) holds, ``fullrank`` is set, no SVD is computed, U(n) is the QR factor Q
+        and SVt(n) is R (keep == n: the caller must not truncate)."""
         X = X.contiguous()
         m, n = X.shape
         self.m, self.n = m, n
+        fr = fullrank_delta if _fullrank_wanted(fullrank_delta, m, n, want_v) else None
         # square: one-sided Jacobi straight on X (its column Gram equals R's, so the rotation
         # sequence and sweep count are those of Jacobi on R, and the QR is saved)
         self.direct = m == n and n > 64
         self.tall = m >= n and not self.direct
-        if self.direct:
+        if self.direct and fr is not None and self._direct_fullrank(X, n, fr):
+            pass
+        elif self.direct:
             self.X = X
             if not want_v and _graded(torch.linalg.vector_norm(X, dim=0)):
                 # X^T = Q2 R2, X = R2^T Q2^T: Jacobi on the columns of R2^T gives U and S of X directly
@@ -450,13 +528,16 @@ class SVDFactors:
             self.implicit = True
             self.X = X
             self._want_v = want_v
-            got = _gram_jacobi(X, m, n)
+            got = _gram_jacobi(X, m, n, fr)
             if got is None:
                 _, Rt = qr_colmajor(permute(X, (1, 0)), m, n, want_q=False)
                 got = (Rt,) + _jacobi_rt(Rt, n)[:2]   # rows: right singular vectors
             self.Rt, self.Vr, self.S = got
             self.UJ = self.VJ = self.Qt = None
             self._W = None
+            if self.S is None:          # certified full rank: Vr holds L^-1, U = X L^-T, carry = R = L^T
+                self.fullrank = True
+                self._W = self.Vr.t().contiguous()
         elif self.tall:
             # small R: one-sided Jacobi on R^T (rows of R, graded by the QR) converges in fewer
             # rounds; R = V' S U'^T, so U_R is the accumulated rotation V' and V_R = U'
@@ -477,7 +558,25 @@ class SVDFactors:
             self.UJ, self.S, self.VJ = _jacobi_rt(Rt, m, want_v)  # Jacobi on R^T
 
     implicit = False
+    fullrank = False
     _s = None
+
+    def _direct_fullrank(self, X, n, delta):
+        """Square X: Householder X = Q R, the certificate on R^T (its L^-1 and norm on a side stream
+        while Q is formed); certified -> full-rank mode with the explicit Q, else nothing is kept."""
+        def cert(Rt):
+            Li = _trtri(Rt, n)        # Rt row-major = R^T, lower triangular
+            return nrm2(Li).reshape(1)
+        Qt, Rt, nrm = qr_colmajor(permute(X, (1, 0)), n, n, overlap_r=cert)
+        v = float(nrm.item())
+        if not (np.isfinite(v) and v > 0.0 and 1.0 / v > _FULLRANK_MARGIN * delta):
+            return False
+        self.fullrank = True
+        self.direct = False
+        self.tall = True
+        self.Qt, self.Rt = Qt, Rt
+        self.S = self.UJ = self.VJ = None
+        return True
 
     def record_stream(self, stream):
         """Mark every device tensor held here as used on ``stream`` (factors made on a side stream)."""
@@ -486,6 +585,8 @@ class SVDFactors:
                 v.record_stream(stream)
 
     def s_host(self):
+        if self.fullrank:
+            raise ValueError("certified full-rank factors hold no singular values (keep == n)")
         if self._s is None:
             self._s = self.S.cpu().numpy()
         return self._s
@@ -493,6 +594,8 @@ class SVDFactors:
     def _implicit_w(self, r):
         """W = U'[:r]^T S[:r]^-1 (n x r) when every kept singular value is well separated from 0,
         else switch to the explicit-Q path (returns None)."""
+        if self.fullrank:
+            return self._W
         s = self.s_host()
         if s[0] > 0.0 and s[r - 1] >= _IMPLICIT_U_MIN_RATIO * s[0]:
             if self._W is None or self._W.shape[1] != r:
@@ -513,6 +616,11 @@ class SVDFactors:
 
     def U(self, r):
         """First r left singular vectors, row-major (m x r)."""
+        if self.fullrank:
+            self._full(r)
+            if self.implicit:
+                return gemm_triu(self.X, self._W)
+            return self.Qt.t().contiguous()
         if self.implicit and self._implicit_w(r) is not None:
             return gemm(self.X, self._W, emulate=True)
         if self.tall:
@@ -521,6 +629,12 @@ class SVDFactors:
 
     def U_rows(self, r, i0, i1, out):
         """Rows [i0, i1) of U(r) into ``out`` ((i1 - i0) x r, row-major) -- chunked formation."""
+        if self.fullrank:
+            self._full(r)
+            if self.implicit:
+                return gemm_triu(self.X[i0:i1], self._W, out=out)
+            out.copy_(self.Qt[:, i0:i1].t())
+            return out
         if self.implicit and self._implicit_w(r) is not None:
             return gemm(self.X[i0:i1], self._W, out=out, emulate=True)
         if self.tall:
@@ -530,6 +644,9 @@ class SVDFactors:
 
     def SVt(self, r):
         """diag(S[:r]) Vt[:r] = U[:, :r]^T X  (r x n)."""
+        if self.fullrank:
+            self._full(r)
+            return self.Rt.t().contiguous()      # R (n x n, row-major): U(n) R = X
         if self.implicit:
             return (self.S[:r, None] * self.Vr[:r]).contiguous()
         if self.direct:
@@ -538,6 +655,10 @@ class SVDFactors:
             return gemm(self.UJ[:r], self.Rt, tB=True)          # U_R^T R
         W = gemm(self.UJ[:r], self.Rt)                          # U'^T R^T  (r x m)
         return gemm(W, self.Qt)                                 # ... Q^T   (r x n)
+
+    def _full(self, r):
+        if r != self.n:
+            raise ValueError("certified full-rank factors cannot be truncated")
 
     def Vt(self, r):
         """First r right singular vectors as rows (r x n); needs want_v=True."""

@@ -374,12 +374,14 @@ def _dot_dev(a, b):
     return v[0, 0]
 
 
-def _rl_orthogonalize(cores, renorm=False, svd0=False):
+def _rl_orthogonalize(cores, renorm=False, svd0=False, fullrank_eps=None):
     """Right-to-left Householder sweep: cores[1:] right-orthonormal (reference core.py:368-373).
 
     svd0: also return the SVD factors of the final cores[0] (the first step of the rounding's
     left-to-right pass); its carry and SVD run on a side stream while the explicit Q of core 1 is
-    formed, since neither needs the other."""
+    formed, since neither needs the other. fullrank_eps (eps / sqrt(d - 1) of the rounding, or None):
+    the first step's threshold delta = fullrank_eps ||cores[0]|| is known here, so its factors may take
+    the certified full-rank QR route (linalg._fullrank_inverse)."""
     cores = list(cores)
     scale = None
     f0 = None
@@ -391,7 +393,8 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False):
 
             def first_svd(Rt):
                 c0 = L.gemm(prev.reshape(a * m, r0), Rt)
-                return c0, L.SVDFactors(c0)
+                dl = None if fullrank_eps is None else fullrank_eps * float(L.nrm2(c0).item())
+                return c0, L.SVDFactors(c0, fullrank_delta=dl)
 
             got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0)
             if got is not None:
@@ -494,16 +497,18 @@ def tt_round(t, eps, max_rank=None):
     d = len(cores)
     if d == 1:
         return _unfused([G.clone() for G in cores], tag)
-    cores, _, f0 = _rl_orthogonalize(cores, svd0=True)
+    fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
+    cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps)
     total = float(L.nrm2(cores[0]).item())
     if total == 0.0:
         return _unfused([L.zeros(1, G.shape[1], 1) for G in cores], tag)
     delta = eps * total / np.sqrt(d - 1)
     for k in range(d - 1):
         r0, n, r1 = cores[k].shape
-        f = f0 if (k == 0 and f0 is not None) else L.SVDFactors(cores[k].reshape(r0 * n, r1))
-        s = f.s_host()
-        keep = _chop(s, delta, max_rank)
+        f = f0 if (k == 0 and f0 is not None) else L.SVDFactors(
+            cores[k].reshape(r0 * n, r1), fullrank_delta=delta if max_rank is None else None)
+        # certified full rank (s_min > delta): _chop would keep every singular value, U S Vt = Q R
+        keep = f.n if f.fullrank else _chop(f.s_host(), delta, max_rank)
         cores[k] = f.U(keep).reshape(r0, n, keep)
         carry = f.SVt(keep)
         nxt = cores[k + 1]

@@ -221,7 +221,8 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
     if d == 1:
         download(0, cores[0])
     else:
-        cores, _, f0 = _rl_orthogonalize(cores, svd0=True)
+        fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
+        cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps)
         total = float(L.nrm2(cores[0]).item())
         if total == 0.0:
             cores = [L.zeros(1, G.shape[1], 1) for G in cores]
@@ -231,8 +232,9 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
             delta = eps * total / np.sqrt(d - 1)
             for k in range(d - 1):
                 r0, n, r1 = cores[k].shape
-                f = f0 if (k == 0 and f0 is not None) else L.SVDFactors(cores[k].reshape(r0 * n, r1))
-                keep = _chop(f.s_host(), delta, max_rank)
+                f = f0 if (k == 0 and f0 is not None) else L.SVDFactors(
+                    cores[k].reshape(r0 * n, r1), fullrank_delta=delta if max_rank is None else None)
+                keep = f.n if f.fullrank else _chop(f.s_host(), delta, max_rank)
                 rows = r0 * n
                 Uk = L.empty(rows, keep)
                 if k < d - 2 or not f.tall:

@@ -404,6 +404,71 @@ def test_dgemm_ozaki_trilA():
 
 
 @pytest.mark.gpu
+def test_dgemm_ozaki_triuB():
+    """Upper-triangular B: the k steps below each column block's diagonal are skipped, result == full product."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200._lib import call, call_raw, ptr
+    g = torch.Generator(device="cuda").manual_seed(6)
+    M, N = 4096, 384
+    A = torch.randn(M, N, generator=g, device="cuda", dtype=torch.float64)
+    B = torch.triu(torch.randn(N, N, generator=g, device="cuda", dtype=torch.float64))
+    C = torch.empty(M, N, device="cuda", dtype=torch.float64)
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, N)), dtype=torch.uint8, device="cuda")
+    call("ttb_dgemm_ozaki_triuB", M, N, ptr(A), N, ptr(B), N, ptr(C), N, ptr(ws))
+    Cd = L.gemm(A, B)
+    scale = N * A.abs().max(1).values[:, None] * B.abs().max(0).values[None, :]
+    assert float(((C - Cd).abs() / scale).max()) < 2 ** -52
+    assert float((C - Cd).norm() / Cd.norm()) < 1e-14
+    # a nonzero strict lower triangle must not be read beyond the diagonal blocks' 64-row granularity:
+    # entries below the block diagonal are skipped (documented precondition: they are zero)
+    assert L.gemm_triu(A, B).shape == (M, N)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", ["square", "tall"])
+def test_svd_fullrank_certificate(monkeypatch, shape):
+    """The rounding's certified full-rank route (linalg._fullrank_inverse): a factor whose smallest
+    singular value is provably above delta yields Q, R with Q R = X and Q^T Q = I and no SVD; a factor
+    with singular values below delta (or a delta too close to s_min) takes the SVD route."""
+    from paper_2509_13224_b200 import linalg as L
+    monkeypatch.setattr(L, "_GRAM_MIN_M", 65536)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    m, n = (512, 512) if shape == "square" else (65536 * 2, 256)
+    X = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    s = torch.linalg.svdvals(X)
+    eye = torch.eye(n, device="cuda", dtype=torch.float64)
+    # certified: delta far below s_min
+    f = L.SVDFactors(X, fullrank_delta=1e-8 * float(X.norm()))
+    assert f.fullrank and f.S is None
+    U, R = f.U(n), f.SVt(n)
+    assert float((L.gemm(U, R) - X).norm() / X.norm()) < 1e-14
+    assert float((L.gemm(U, U, tA=True) - eye).abs().max()) < 1e-12
+    assert float(torch.tril(R, -1).abs().max()) == 0.0
+    Uc = L.empty(m, n)
+    for i0 in range(0, m, m // 4):
+        f.U_rows(n, i0, i0 + m // 4, Uc[i0:i0 + m // 4])
+    assert float((Uc - U).abs().max()) < 1e-13     # chunks below the Ozaki size run on DMMA
+    with pytest.raises(ValueError):
+        f.U(n - 1)
+    with pytest.raises(ValueError):
+        f.s_host()
+    # the certificate is one-sided: a delta above s_min / margin is never certified
+    f = L.SVDFactors(X, fullrank_delta=0.6 * float(s[-1]))
+    assert not f.fullrank and f.S is not None
+    # rank deficient: the last quarter of the columns repeats the first (s_min ~ 1e-16 s_max)
+    Xd = X.clone()
+    Xd[:, -n // 4:] = Xd[:, :n // 4]
+    f = L.SVDFactors(Xd, fullrank_delta=1e-8 * float(Xd.norm()))
+    assert not f.fullrank
+    S = f.S.sort(descending=True).values
+    S_ref = torch.linalg.svdvals(Xd)
+    assert float(((S - S_ref).abs() / S_ref[0]).max()) < 5e-13
+    # disabled by the switch
+    monkeypatch.setattr(L, "_FULLRANK", False)
+    assert not L.SVDFactors(X, fullrank_delta=1e-8 * float(X.norm())).fullrank
+
+
+@pytest.mark.gpu
 def test_trtri_lower():
     from paper_2509_13224_b200._lib import call, ptr
     g = torch.Generator(device="cuda").manual_seed(2)

@@ -39,7 +39,7 @@ def _instance(n):
 def _route_spy(monkeypatch):
     """Record which large-scale routes returned a result (None = fell back to Householder)."""
     from paper_2509_13224_b200 import linalg as L
-    used = {"cholqr2": 0, "gram": 0, "ozaki": 0}
+    used = {"cholqr2": 0, "gram": 0, "ozaki": 0, "fullrank": 0}
     chol, gram, oz = L.cholqr2_colmajor, L._gram_jacobi, L.call
 
     def chol_spy(*a, **k):
@@ -50,10 +50,11 @@ def _route_spy(monkeypatch):
     def gram_spy(*a, **k):
         r = gram(*a, **k)
         used["gram"] += r is not None
+        used["fullrank"] += r is not None and r[2] is None      # certified full rank: no SVD
         return r
 
     def call_spy(name, *a, **k):
-        if name == "ttb_dgemm_ozaki":
+        if name in ("ttb_dgemm_ozaki", "ttb_dgemm_ozaki_triuB"):
             used["ozaki"] += 1
         return oz(name, *a, **k)
 
@@ -81,29 +82,41 @@ def _bond_singular_values(Y):
     return s1, s2
 
 
-def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property):
+_ORACLE_N512 = {}
+
+
+@pytest.mark.parametrize("fullrank", [True, False], ids=["certified-qr", "svd"])
+def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fullrank):
+    """fullrank: the rounding's certified full-rank QR steps on (default) / off (every step a Jacobi SVD)."""
     from oracle import tt as OT
     from paper_2509_13224_b200 import linalg as L
     from paper_2509_13224_b200.tensor_train import tt_matvec, tt_round
     n = 512
     monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 1 << 18)
     monkeypatch.setattr(L, "_GRAM_MIN_M", 1 << 18)
+    monkeypatch.setattr(L, "_FULLRANK", fullrank)
     used = _route_spy(monkeypatch)
     A, X, Ad, Xd = _instance(n)
     Y = tt_round(tt_matvec(Ad, Xd), 1e-8)
     torch.cuda.synchronize()
     assert used["cholqr2"] >= 1 and used["gram"] >= 1 and used["ozaki"] >= 3, used
-    Yo = OT.round_tt(OT.matvec(OT.TTOp(A), OT.TT(X)), 1e-8)
+    assert (used["fullrank"] >= 1) == fullrank, used
+    if "Y" not in _ORACLE_N512:
+        _ORACLE_N512["Y"] = OT.round_tt(OT.matvec(OT.TTOp(A), OT.TT(X)), 1e-8)
+    Yo = _ORACLE_N512["Y"]
     assert tuple(Y.ranks) == tuple(Yo.ranks), (Y.ranks, Yo.ranks)
     Yh = OT.TT([G.cpu().numpy() for G in Y.cores])
     err = OT.norm(OT.sub(Yh, Yo)) / OT.norm(Yo)
-    print(f"matvec+round n=512 (all routes): rel. error vs oracle {err:.3e}, ranks {Y.ranks}, routes {used}")
+    print(f"matvec+round n=512 (all routes, fullrank={fullrank}): rel. error vs oracle {err:.3e}, ranks {Y.ranks}, routes {used}")
     record_property("rel_error", err)
     assert err <= 1e-12, err
 
 
-def test_matvec_round_n1024_vs_oracle_fixture(record_property):
+@pytest.mark.parametrize("fullrank", [True, False], ids=["certified-qr", "svd"])
+def test_matvec_round_n1024_vs_oracle_fixture(monkeypatch, record_property, fullrank):
+    from paper_2509_13224_b200 import linalg as L
     from paper_2509_13224_b200.tensor_train import tt_matvec, tt_norm, tt_round
+    monkeypatch.setattr(L, "_FULLRANK", fullrank)
     if not os.path.exists(GOLDEN):
         pytest.fail("tests/golden/matvec_round_oracle.npz missing (tests/golden/make_matvec_round_fixture.py)")
     g = np.load(GOLDEN)
@@ -123,7 +136,7 @@ def test_matvec_round_n1024_vs_oracle_fixture(record_property):
     vals = Y.gather(torch.as_tensor(g["n1024_idx"].astype(np.int64), device="cuda")).cpu().numpy()
     ev = float(np.abs(vals - g["n1024_vals"]).max() / np.sqrt(np.mean(g["n1024_vals"] ** 2)))
     en = abs(tt_norm(Y) - float(g["n1024_norm"])) / float(g["n1024_norm"])
-    print(f"matvec+round n=1024 vs oracle fixture: singular values {es1:.2e} / {es2:.2e} (of s_max), "
+    print(f"matvec+round n=1024 (fullrank={fullrank}) vs oracle fixture: singular values {es1:.2e} / {es2:.2e} (of s_max), "
           f"sampled entries {ev:.2e} (of rms), norm {en:.2e}")
     for k, v in (("s1", es1), ("s2", es2), ("entries", ev), ("norm", en)):
         record_property(k, v)

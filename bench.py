@@ -202,12 +202,22 @@ def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step):
     oz_ms = sum(a.elapsed_time(b) for a, b, _, _, _ in oz)
     oz_fl = sum(r[2] for r in oz)
     M, N, K = shape
+    by_cls = {}
+    for a, b, f, kd, sh in prof:
+        c = by_cls.setdefault((kd, sh), [0, 0.0, 0.0])
+        c[0] += 1
+        c[1] += a.elapsed_time(b)
+        c[2] += f
+    classes = [{"kind": kd, "shape": list(sh), "launches_per_step": c[0] / steps, "ms_per_step": c[1] / steps,
+                "fp64_equivalent_tflops": c[2] / (c[1] / 1e3) / 1e12 if c[1] else None}
+               for (kd, sh), c in sorted(by_cls.items(), key=lambda kv: -kv[1][1])][:8]
     rec = {"bound": "tensor", "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
            "launches_per_step": len(recs) / steps, "share_of_step": ms / steps / ms_step,
            "all_gemms": {"fp64_equivalent_tflops": g_fl / (g_ms / 1e3) / 1e12 if g_ms else None,
                          "share_of_step": g_ms / steps / ms_step, "launches_per_step": len(prof) / steps,
                          "executed_gflop_per_step": g_fl / steps / 1e9,
-                         "ozaki_fp64_equivalent_tflops": oz_fl / (oz_ms / 1e3) / 1e12 if oz_ms else None}}
+                         "ozaki_fp64_equivalent_tflops": oz_fl / (oz_ms / 1e3) / 1e12 if oz_ms else None},
+           "gemm_classes": classes}
     if kind.startswith("ozaki"):
         burst, sus = _peaks()
         peak = 2.0 * sus if sus else (2.0 * burst if burst else 4500.0)
@@ -215,7 +225,10 @@ def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step):
         rec.update(pipe=("INT8 tcgen05.mma kind::i8 (Ozaki-scheme FP64 emulation: 7 balanced int8 slices per operand, "
                          "8 levels = 34 exact slice products)"),
                    kernel=(f"oz_gemm_kernel, C({M}x{N}) = A({M}x{K}) B({K}x{N}) "
-                           + ("(B upper triangular, zero k steps skipped: executed flops counted) " if kind == "ozaki-triu" else "")
+                           + {"ozaki-triu": "(B upper triangular, zero k steps skipped: executed flops counted) ",
+                              "ozaki-tril": "(A lower triangular, zero k steps skipped: executed flops counted) ",
+                              "ozaki-gram": "(symmetric Gram B = A^T on one slice stack, lower-triangle tiles only: "
+                                            "executed flops counted) "}.get(kind, "")
                            + f"({len(recs) / steps:g} launches per step: "
                            f"the products of the step with the largest share of device time)"),
                    timed="whole ttb_dgemm_ozaki calls (operand slicing + oz_gemm_kernel), CUDA events on the launching stream",
@@ -348,13 +361,14 @@ def run_b200(args):
     del hA, hX
 
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "r2_dominant_kernel_ozaki.json" if cls[0] == "ozaki"
+    tf = os.path.join(ROOT, "profiles", "r2_dominant_kernel_ozaki.json" if cls[0].startswith("ozaki")
                       else "r1_dominant_kernel.json")
     if os.path.exists(tf):
         with open(tf) as fh:
             d = json.load(fh)
-        if tuple(d.get("shape", cls[1])) == tuple(cls[1]):
-            traffic = d["dram_bytes_read"] + d["dram_bytes_write"]
+        for e in [d] + list(d.get("other_shapes", [])):     # ncu --set full captures, one per GEMM shape
+            if tuple(e.get("shape", ())) == tuple(cls[1]):
+                traffic = e["dram_bytes_read"] + e["dram_bytes_write"]
 
     # ---------------- the same step with every product on DMMA and Householder factorizations
     # (TTB_OZAKI=0 path), for comparison: what the Ozaki / CholeskyQR2 / Gram routes buy

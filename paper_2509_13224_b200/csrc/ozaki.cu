@@ -152,6 +152,10 @@ struct OzOut {
   // mode 3 (TT-matvec core layout): row r = (a n + i) Rb + b, column c rd + d of the product go to
   // out[((a rc + c) n + i) Rb rd + b rd + d] (rd % 16 == 0, so a 16-column store segment has one c)
   int sn, sRb, src_, srd;
+  // 1: tiles in row-block-fastest order (unit t -> row block t % (M / 128), column block t / (M / 128)):
+  // few row blocks over a small A and a long B (C = carry x core, 1024 x 1M): the CTAs running together
+  // then share B's column blocks through L2 instead of each row block re-reading the whole B stack
+  int mfast;
 };
 
 // Banded batched mode (ttb_band_gemm_ozaki): batch i multiplies a K window of its group's A slice stack
@@ -233,7 +237,20 @@ __global__ void __launch_bounds__(320, 1) oz_gemm_kernel(const __grid_constant__
       kt1 = bd.Kp / OA_K;
     } else {
       bi = 0;
-      oz_tile(u % tiles, ntn, sym, m0, n0);
+      if (o.mfast) {
+        const int t = u % tiles, ntm = M / OZ_M;
+        m0 = (t % ntm) * OZ_M;
+        n0 = (t / ntm) * OA_N;
+      } else {
+        oz_tile(u % tiles, ntn, sym, m0, n0);
+      }
+      if (o.trilA == 2) {
+        // column block c of an upper-triangular B has c + 1 k steps: rotate the column order by the row
+        // block, so the units a CTA takes (u, u + grid, ...) cycle through every depth instead of a
+        // fixed residue class of c (148 = 4 mod 16: the deepest class did 10 k steps on average, the
+        // mean is 8.5); a row block's tiles still run together and share its A rows
+        n0 = (int)(((unsigned)(n0 / OA_N) + (unsigned)(m0 / OZ_M)) % (unsigned)ntn) * OA_N;
+      }
       kt0 = (u / tiles) * (kchunk / OA_K);
       kt1 = min(min(K, (u / tiles + 1) * kchunk), o.trilA == 1 ? m0 + OZ_M : (o.trilA == 2 ? n0 + OA_N : K)) / OA_K;
     }
@@ -1120,6 +1137,13 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   else
     o = OzOut{C, ldc, 0, alpha, beta, (alpha == 1.0 && beta == 0.0) ? 0 : 2,
               trilA == 1 && M == K ? 1 : (trilA == 2 && N == K ? 2 : 0), mv, nv};
+  // unit order: column block fastest shares the A row block among the CTAs running together and streams
+  // every A row block once, but reads the B stack once per row block; when A's whole slice stack stays
+  // in L2 (<= 32 MB) and B's does not, row block fastest reads B once instead (ncu, 1024 x 1M x 1024:
+  // 60.2 GB read with column-fastest order = 8 row blocks x 7.5 GB of B slices)
+  static const bool mfast_on = !(getenv("TTB_OZAKI_MFAST") && atoi(getenv("TTB_OZAKI_MFAST")) == 0);
+  o.mfast = (mfast_on && !sym && o.trilA == 0 && M < N && (long long)OZ_S * M * K <= (32LL << 20) &&
+             (long long)OZ_S * N * K > (32LL << 20)) ? 1 : 0;
   const long long units = tiles * ks;
   const int grid = units < oz_nsm() ? (int)units : oz_nsm();
   // 2-CTA clusters that multicast the A tiles (TTB_OZAKI_CLUSTER: 0 off, 1 Grams only (default), 2 all):
@@ -1127,6 +1151,7 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   // bound (profiles/README.md), multicast halves their A traffic: 18.5 -> 15.4 ms on 1024 x 1M
   static const int cluster_mode = getenv("TTB_OZAKI_CLUSTER") ? atoi(getenv("TTB_OZAKI_CLUSTER")) : 1;
   const bool cluster = levels == 8 && tiles % 2 == 0 && grid % 2 == 0 && (cluster_mode == 2 || (cluster_mode == 1 && sym));
+  if (cluster) o.mfast = 0;   // a cluster's two CTAs take consecutive units that must share the A row block
   if (cluster && kc > OZ_SUB * OA_K) {
     const int e = oz_launch_cluster<8, true>(st, grid, smem, ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
     if (e) return e;

@@ -258,12 +258,33 @@ _CHOLQR2 = os.environ.get("TTB_RL_CHOLQR2", "1") != "0"
 _CHOLQR2_MIN_M = int(os.environ.get("TTB_RL_CHOLQR2_MIN_M", str(1 << 19)))
 
 
+class _profiled:
+    """Records (start, end, flops, kind, shape) of the enclosed launches when gemm_profile is on."""
+
+    def __init__(self, kind, shape, flops):
+        self.rec = (kind, shape, flops)
+
+    def __enter__(self):
+        if _GEMM_PROFILE is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+
+    def __exit__(self, *exc):
+        if _GEMM_PROFILE is not None and exc[0] is None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            kind, shape, flops = self.rec
+            _GEMM_PROFILE.append((self.e0, e1, flops, kind, shape))
+        return False
+
+
 def _chol_rows(T, n, m, offdiag=False):
     """Row-major lower Cholesky factor L of G = T T^T (T: n x m row-major, Ozaki-scheme Gram), or None;
     offdiag: also max |G_ij| over i != j (read from the triangle potrf leaves untouched)."""
     ws = torch.empty(int(call_raw("ttb_ozaki_gram_rows_workspace", n, m)), dtype=torch.uint8, device=device())
     G = empty(n, n)
-    call("ttb_ozaki_gram_rows", n, m, ptr(T), max(T.stride(0), 1), ptr(G), n, ptr(ws))
+    with _profiled("ozaki-gram", (n, n, m), 1.0 * n * (n + 128) * m):     # the lower-triangle tiles only
+        call("ttb_ozaki_gram_rows", n, m, ptr(T), max(T.stride(0), 1), ptr(G), n, ptr(ws))
     del ws
     info = empty(1, dtype=I32)
     call("ttb_potrf", n, ptr(G), n, ptr(info))   # col-major lower L: row-major view of the buffer = L^T
@@ -307,11 +328,35 @@ def _trmm_oz(Li, X, n, m):
     """Li (n x n lower) @ X (n x m) as the Ozaki GEMM that skips the zero upper triangle."""
     out = empty(n, m)
     ws = torch.empty(int(call_raw("ttb_ozaki_workspace", n, m, n)), dtype=torch.uint8, device=device())
-    call("ttb_dgemm_ozaki_trilA", n, m, ptr(Li), n, ptr(X), max(X.stride(0), 1), ptr(out), m, ptr(ws))
+    with _profiled("ozaki-tril", (n, m, n), 1.0 * n * (n + 128) * m):
+        call("ttb_dgemm_ozaki_trilA", n, m, ptr(Li), n, ptr(X), max(X.stride(0), 1), ptr(out), m, ptr(ws))
     return out
 
 
-def cholqr2_colmajor(Acm, m, n):
+_LAZY_Q = os.environ.get("TTB_ROUND_LAZY_Q", "1") != "0"
+
+
+class LazyQt:
+    """The transposed orthonormal factor Q^T = Li @ X (n x m) of a one-pass CholeskyQR, held as its
+    factors: Li = L1^-1 (n x n row-major lower) and the factored rows X (torch (n, m), not copied).
+    The rounding's left-to-right pass only ever needs carry @ Q^T, which is (carry @ Li) @ X: one small
+    product and ONE large one, instead of forming Q^T (a large triangular product) and then carrying
+    into it (a second large product)."""
+
+    def __init__(self, Li, X):
+        self.Li, self.X = Li, X
+        self.shape = X.shape
+
+    def carried(self, carry):
+        """carry @ Q^T for a row-major carry (k x n)."""
+        return gemm(gemm(carry, self.Li), self.X, emulate=True)
+
+    def dense(self):
+        n, m = self.X.shape
+        return _trmm_oz(self.Li, self.X, n, m)
+
+
+def cholqr2_colmajor(Acm, m, n, lazy=False):
     """Q R of a very tall col-major m x n matrix held as torch (n, m), by CholeskyQR2 with Ozaki-scheme
     FP64 Gram matrices and products on the int8 tensor cores:
         G1 = X^T X = L1 L1^T,  Q1 = X L1^-T,  G2 = Q1^T Q1 = L2 L2^T,  Q = Q1 L2^-T,  R = L2^T L1^T.
@@ -320,7 +365,8 @@ def cholqr2_colmajor(Acm, m, n):
     needs cond(X) well below eps^-1/2: the Cholesky factorizations must succeed and the second Gram
     must be within 0.1 of I (else the first pass lost orthogonality beyond what one repeat restores).
     When the power-iteration estimate of cond(L1) is <= 4 (TTB_CHOLQR_ONEPASS_KAPPA) the first pass
-    is kept as is (orthogonality error ~ eps cond^2 <= 16 eps);
+    is kept as is (orthogonality error ~ eps cond^2 <= 16 eps), and with ``lazy`` its Q^T is returned
+    unformed (LazyQt: the caller multiplies through the factors; TTB_ROUND_LAZY_Q=0 forms it);
     returns (Qt, Rt) in qr_colmajor's layout, or None (the caller takes the Householder path).
     Used for the rounding's right-to-left sweep (core.py _rl_orthogonalize)."""
     if not (_CHOLQR2 and _OZAKI and m >= _CHOLQR2_MIN_M and n >= 256 and n % 128 == 0 and m % 64 == 0):
@@ -329,8 +375,14 @@ def cholqr2_colmajor(Acm, m, n):
     if L1 is None:
         return None
     Li1 = _trtri(L1, n)
+    onepass = False
+    if _CHOLQR1_KAPPA > 0.0:
+        est = torch.cat([_norm2_est_dev(L1), _norm2_est_dev(Li1)]).cpu().numpy()   # one host sync
+        onepass = bool(np.isfinite(est).all() and est[0] * est[1] <= _CHOLQR1_KAPPA)
+    if onepass and lazy and _LAZY_Q:
+        return LazyQt(Li1, Acm), L1
     Q1 = _trmm_oz(Li1, Acm, n, m)                        # (n, m) = L1^-1 X^T = Q1^T
-    if _CHOLQR1_KAPPA > 0.0 and _norm2_est(L1) * _norm2_est(Li1) <= _CHOLQR1_KAPPA:
+    if onepass:
         # cond(X) = cond(L1) <= 4: one CholeskyQR pass is already orthogonal to ~eps cond^2
         return Q1, L1
     got = _chol_rows(Q1, n, m, offdiag=True)
@@ -469,7 +521,8 @@ def _gram_jacobi(X, m, n, fullrank_delta=None):
         return None
     ws = torch.empty(int(call_raw("ttb_ozaki_gram_workspace", m, n)), dtype=torch.uint8, device=device())
     G = empty(n, n)
-    call("ttb_ozaki_gram", m, n, ptr(X), max(X.stride(0), 1), ptr(G), n, ptr(ws))
+    with _profiled("ozaki-gram", (n, n, m), 1.0 * n * (n + 128) * m):
+        call("ttb_ozaki_gram", m, n, ptr(X), max(X.stride(0), 1), ptr(G), n, ptr(ws))
     del ws
     info = empty(1, dtype=I32)
     call("ttb_potrf", n, ptr(G), n, ptr(info))   # col-major lower L: row-major view of the buffer = L^T = R

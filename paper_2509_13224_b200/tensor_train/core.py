@@ -374,15 +374,34 @@ def _dot_dev(a, b):
     return v[0, 0]
 
 
-def _rl_orthogonalize(cores, renorm=False, svd0=False, fullrank_eps=None):
+def _carry_into(carry, nxt):
+    """carry @ (the next core's left unfolding); nxt: a core, or the unformed Q^T of a one-pass CholeskyQR
+    (linalg.LazyQt over the core's (r0, n r1) unfolding, its ``shape`` set to the core's)."""
+    if isinstance(nxt, L.LazyQt):
+        _, n, r1 = nxt.shape
+        return nxt.carried(carry).reshape(carry.shape[0], n, r1)
+    return L.gemm(carry, nxt.reshape(nxt.shape[0], -1), emulate=True).reshape(carry.shape[0], nxt.shape[1],
+                                                                             nxt.shape[2])
+
+
+def _rl_orthogonalize(cores, renorm=False, svd0=False, fullrank_eps=None, lazy_q=False):
     """Right-to-left Householder sweep: cores[1:] right-orthonormal (reference core.py:368-373).
 
     svd0: also return the SVD factors of the final cores[0] (the first step of the rounding's
     left-to-right pass); its carry and SVD run on a side stream while the explicit Q of core 1 is
     formed, since neither needs the other. fullrank_eps (eps / sqrt(d - 1) of the rounding, or None):
     the first step's threshold delta = fullrank_eps ||cores[0]|| is known here, so its factors may take
-    the certified full-rank QR route (linalg._fullrank_inverse)."""
+    the certified full-rank QR route (linalg._fullrank_inverse). lazy_q: cores orthogonalized by a
+    one-pass CholeskyQR stay unformed (linalg.LazyQt in place of the core; the caller's left-to-right
+    pass multiplies through the factors with _carry_into), since this sweep itself never reads Q."""
     cores = list(cores)
+
+    def as_core(Qt, n, r1):
+        if isinstance(Qt, L.LazyQt):
+            Qt.shape = (Qt.shape[0], n, r1)
+            return Qt
+        return Qt.reshape(Qt.shape[0], n, r1)
+
     scale = None
     f0 = None
     for k in range(len(cores) - 1, 0, -1):
@@ -396,7 +415,7 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False, fullrank_eps=None):
                 dl = None if fullrank_eps is None else fullrank_eps * float(L.nrm2(c0).item())
                 return c0, L.SVDFactors(c0, fullrank_delta=dl)
 
-            got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0)
+            got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0, lazy=lazy_q)
             if got is not None:
                 Qt, Rt = got
                 c0, f0 = first_svd(Rt)
@@ -405,13 +424,13 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False, fullrank_eps=None):
                                                  overlap_r=first_svd)
                 f0.record_stream(torch.cuda.current_stream())
             kk = Qt.shape[0]
-            cores[k] = Qt.reshape(kk, n, r1)
+            cores[k] = as_core(Qt, n, r1)
             cores[0] = c0.reshape(a, m, kk)
             continue
-        got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0)
+        got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0, lazy=lazy_q and not renorm)
         Qt, Rt = got if got is not None else L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
         kk = Qt.shape[0]
-        cores[k] = Qt.reshape(kk, n, r1)
+        cores[k] = as_core(Qt, n, r1)
         cores[k - 1] = L.gemm(cores[k - 1].reshape(a * m, r0), Rt, emulate=True).reshape(a, m, kk)
         if renorm:
             s = L.nrm2(cores[k - 1])
@@ -498,7 +517,7 @@ def tt_round(t, eps, max_rank=None):
     if d == 1:
         return _unfused([G.clone() for G in cores], tag)
     fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
-    cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps)
+    cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps, lazy_q=True)
     total = float(L.nrm2(cores[0]).item())
     if total == 0.0:
         return _unfused([L.zeros(1, G.shape[1], 1) for G in cores], tag)
@@ -510,10 +529,7 @@ def tt_round(t, eps, max_rank=None):
         # certified full rank (s_min > delta): _chop would keep every singular value, U S Vt = Q R
         keep = f.n if f.fullrank else _chop(f.s_host(), delta, max_rank)
         cores[k] = f.U(keep).reshape(r0, n, keep)
-        carry = f.SVt(keep)
-        nxt = cores[k + 1]
-        cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1), emulate=True).reshape(keep, nxt.shape[1],
-                                                                                         nxt.shape[2])
+        cores[k + 1] = _carry_into(f.SVt(keep), cores[k + 1])
     return _unfused(cores, tag)
 
 

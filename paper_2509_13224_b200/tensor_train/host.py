@@ -24,7 +24,7 @@ import torch
 
 from .. import linalg as L
 from .._lib import call, call_raw, ptr
-from .core import TtShapeError, _chop, _matvec_core_fused, _rl_orthogonalize
+from .core import TtShapeError, _carry_into, _chop, _matvec_core_fused, _rl_orthogonalize
 
 __all__ = ["tt_matvec_round_host"]
 
@@ -222,7 +222,7 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
         download(0, cores[0])
     else:
         fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
-        cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps)
+        cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps, lazy_q=True)
         total = float(L.nrm2(cores[0]).item())
         if total == 0.0:
             cores = [L.zeros(1, G.shape[1], 1) for G in cores]
@@ -253,10 +253,7 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
                             h[i0:i1].copy_(Uk[i0:i1], non_blocking=True)
                     Uk.record_stream(copy)
                 cores[k] = Uk.view(r0, n, keep)
-                carry = f.SVt(keep)
-                nxt = cores[k + 1]
-                cores[k + 1] = L.gemm(carry, nxt.reshape(nxt.shape[0], -1), emulate=True).reshape(
-                    keep, nxt.shape[1], nxt.shape[2])
+                cores[k + 1] = _carry_into(f.SVt(keep), cores[k + 1])
             download(d - 1, cores[d - 1])
     done = torch.cuda.Event()
     done.record(copy)

@@ -320,6 +320,9 @@ def test_dgemm_ozaki_fp64_accuracy(tB, graded):
     (260, 130, 777, 1, 0.5, -2.0),      # padded, row-sliced B, masked beta epilogue
     (4000, 68, 8296, 1, 1.0, 0.0),      # padded narrow N (the AMEn right-stage shape), long K
     (1000, 510, 4099, 0, -1.0, 1.0),    # padded, K ranges > 4096
+    (256, 16384, 512, 0, 1.0, 0.0),     # small A, B stack > 32 MB: row-block-fastest unit order
+    (384, 20480, 320, 1, 0.5, -2.0),    # the same order with a row-sliced B and the beta epilogue
+    (300, 16390, 500, 0, 1.0, 0.0),     # the same order on a padded shape
 ])
 def test_dgemm_ozaki_ex_splitk_beta(M, N, K, tB, alpha, beta):
     """ttb_dgemm_ozaki_ex (split-K, beta) against the DMMA DGEMM: normwise and per element relative to

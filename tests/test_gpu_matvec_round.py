@@ -39,12 +39,13 @@ def _instance(n):
 def _route_spy(monkeypatch):
     """Record which large-scale routes returned a result (None = fell back to Householder)."""
     from paper_2509_13224_b200 import linalg as L
-    used = {"cholqr2": 0, "gram": 0, "ozaki": 0, "fullrank": 0}
+    used = {"cholqr2": 0, "gram": 0, "ozaki": 0, "fullrank": 0, "lazyq": 0}
     chol, gram, oz = L.cholqr2_colmajor, L._gram_jacobi, L.call
 
     def chol_spy(*a, **k):
         r = chol(*a, **k)
         used["cholqr2"] += r is not None
+        used["lazyq"] += r is not None and isinstance(r[0], L.LazyQt)     # Q^T left unformed (one large GEMM less)
         return r
 
     def gram_spy(*a, **k):
@@ -85,9 +86,11 @@ def _bond_singular_values(Y):
 _ORACLE_N512 = {}
 
 
-@pytest.mark.parametrize("fullrank", [True, False], ids=["certified-qr", "svd"])
-def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fullrank):
-    """fullrank: the rounding's certified full-rank QR steps on (default) / off (every step a Jacobi SVD)."""
+@pytest.mark.parametrize("fullrank,lazy", [(True, True), (False, True), (True, False)],
+                         ids=["certified-qr", "svd", "formed-q"])
+def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fullrank, lazy):
+    """fullrank: the rounding's certified full-rank QR steps on (default) / off (every step a Jacobi SVD);
+    lazy: the one-pass CholeskyQR's Q^T left unformed (default) / formed explicitly."""
     from oracle import tt as OT
     from paper_2509_13224_b200 import linalg as L
     from paper_2509_13224_b200.tensor_train import tt_matvec, tt_round
@@ -95,12 +98,14 @@ def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fu
     monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 1 << 18)
     monkeypatch.setattr(L, "_GRAM_MIN_M", 1 << 18)
     monkeypatch.setattr(L, "_FULLRANK", fullrank)
+    monkeypatch.setattr(L, "_LAZY_Q", lazy)
     used = _route_spy(monkeypatch)
     A, X, Ad, Xd = _instance(n)
     Y = tt_round(tt_matvec(Ad, Xd), 1e-8)
     torch.cuda.synchronize()
     assert used["cholqr2"] >= 1 and used["gram"] >= 1 and used["ozaki"] >= 3, used
     assert (used["fullrank"] >= 1) == fullrank, used
+    assert (used["lazyq"] >= 1) == lazy, used
     if "Y" not in _ORACLE_N512:
         _ORACLE_N512["Y"] = OT.round_tt(OT.matvec(OT.TTOp(A), OT.TT(X)), 1e-8)
     Yo = _ORACLE_N512["Y"]

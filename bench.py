@@ -185,7 +185,7 @@ def _peaks():
     return None, None
 
 
-def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step):
+def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step, kev=None, traffic_by_shape=None):
     """Roofline of the dominant kernel class: the GEMM shape (kind, M, N, K) with the largest share of
     the timed region. Ozaki-emulated FP64 GEMMs (34 exact int8 slice products per FP64 product) are
     bounded by the tcgen05 INT8 pipe: achieved int8 TOPS against 2x the measured dense bf16 peak (int8
@@ -239,12 +239,77 @@ def roofline_record(cls, fp64_peak, traffic, prof, steps, ms_step):
                    peak_source=("2 x MEASURED_PEAKS.json bf16_tflops_sustained (dense int8 = 2x bf16 rate)" if sus
                                 else "2 x MEASURED_PEAKS.json bf16_tflops" if burst
                                 else "nominal B200 dense int8 4.5 POPS (MEASURED_PEAKS.json absent)"))
+        kc = kernel_classes(kev, steps) if kev else []
+        if kc:
+            # the kernel's own launch durations (CUDA events right around oz_gemm_kernel inside the timed steps):
+            # the roofline figures below are those of the class with the largest kernel time; the whole-call
+            # figures (operand slicing passes included) move to "call_level"
+            top = kc[0]
+            rec["call_level"] = {k: rec[k] for k in ("kernel", "timed", "achieved", "frac", "frac_of_burst_peak",
+                                                     "fp64_equivalent_tflops", "launches_per_step", "share_of_step")}
+            tshape = tuple(top["shape"])
+            rec.update(kernel=(f"oz_gemm_kernel [{top['kind']}] M, N, K = {top['shape']} "
+                               f"({top['launches_per_step']:g} launches per step, {top['ms_per_launch']:.2f} ms each: the "
+                               "kernel class with the largest share of the step)"),
+                       timed="oz_gemm_kernel launches alone: a CUDA event pair around each launch on its stream, inside the timed steps (ttb_ozaki_kernel_events)",
+                       achieved=top["int8_tops"], frac=top["int8_tops"] / peak,
+                       frac_of_burst_peak=(top["int8_tops"] / (2.0 * burst)) if burst else None,
+                       fp64_equivalent_tflops=top["fp64_equivalent_tflops"],
+                       launches_per_step=top["launches_per_step"], share_of_step=top["ms_per_step"] / ms_step,
+                       algorithmic_unit="executed FP64-equivalent flop of the launch (2 M N K; Gram / triangular: only the tiles and k steps run) x 34 int8 slice products",
+                       kernel_classes=kc[:8])
+            if traffic_by_shape is not None:
+                rec["traffic"] = traffic_by_shape.get(tshape)
+            all_ms = sum(c["ms_per_step"] for c in kc)
+            all_ops = sum(c["int8_tops"] * c["ms_per_step"] for c in kc)
+            rec["all_oz_gemm_kernels"] = {"ms_per_step": all_ms, "share_of_step": all_ms / ms_step,
+                                          "int8_tops": all_ops / all_ms, "frac": all_ops / all_ms / peak}
     else:
         rec.update(pipe="FP64 DMMA (mma.sync m8n8k4 f64)", kernel=f"dgemm_kernel, C({M}x{N}) = A({M}x{K}) B({K}x{N})",
                    achieved=fp64_eq, peak=fp64_peak, unit="TFLOP/s", frac=fp64_eq / fp64_peak,
                    algorithmic_unit="2 M N K flop per launch",
                    peak_source="cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)")
     return rec
+
+
+KEV_KIND = {0: "ozaki", 1: "ozaki-gram", 2: "ozaki-tril", 3: "ozaki-triu", 4: "ozaki-matvec-core"}
+
+
+def read_kernel_events(lib, cap=8192):
+    """(kind, (M, N, K), ms) of every oz_gemm_kernel launch recorded by ttb_ozaki_kernel_events."""
+    import numpy as np
+    ms = np.zeros(cap, dtype=np.float64)
+    sh = np.zeros(4 * cap, dtype=np.int32)
+    n = int(lib.ttb_ozaki_kernel_events_read(cap, ms.ctypes.data, sh.ctypes.data))
+    return [(KEV_KIND.get(int(sh[4 * i + 3]), "ozaki"), tuple(int(v) for v in sh[4 * i:4 * i + 3]), float(ms[i]))
+            for i in range(n)]
+
+
+def kernel_flops(kind, shape):
+    """Executed FP64-equivalent flop of one oz_gemm_kernel launch (the tiles / k steps it really runs)."""
+    M, N, K = shape
+    if kind == "ozaki-gram":
+        return 1.0 * M * (M + 128) * K          # tiles touching the upper block triangle only
+    if kind == "ozaki-tril":
+        return 1.0 * M * (M + 128) * N          # row block m0 stops at k = m0 + 128
+    if kind == "ozaki-triu":
+        return 1.0 * M * N * (N + 64)           # column block n0 stops at k = n0 + 64
+    return 2.0 * M * N * K
+
+
+def kernel_classes(kev, steps):
+    by = {}
+    for kind, shape, ms in kev:
+        c = by.setdefault((kind, shape), [0, 0.0])
+        c[0] += 1
+        c[1] += ms
+    out = []
+    for (kind, shape), (n, ms) in sorted(by.items(), key=lambda kv: -kv[1][1]):
+        fl = kernel_flops(kind, shape)
+        out.append({"kind": kind, "shape": list(shape), "launches_per_step": n / steps, "ms_per_launch": ms / n,
+                    "ms_per_step": ms / steps, "fp64_equivalent_tflops": fl * n / (ms / 1e3) / 1e12,
+                    "int8_tops": OZ_PAIRS * fl * n / (ms / 1e3) / 1e12})
+    return out
 
 
 def dominant_class(prof):
@@ -291,6 +356,7 @@ def run_b200(args):
 
     # ---------------- device-resident timed region
     lib.ttb_launch_count(1)
+    lib.ttb_ozaki_kernel_events(1)      # CUDA events right around every oz_gemm_kernel launch of the timed steps
     L.gemm_profile(True)
     st = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -306,6 +372,8 @@ def run_b200(args):
     barrier()
     launches = int(lib.ttb_launch_count(1))
     prof = L.gemm_profile(False)
+    lib.ttb_ozaki_kernel_events(0)
+    kev = read_kernel_events(lib)
     ms = e0.elapsed_time(e1) / args.steps
     ms_all = max_over_ranks(ms, device="cuda")
     value = whole_job_rate(flops, ms_all, world) / 1e9
@@ -361,12 +429,14 @@ def run_b200(args):
     del hA, hX
 
     traffic = None
+    traffic_by_shape = {}
     tf = os.path.join(ROOT, "profiles", "r2_dominant_kernel_ozaki.json" if cls[0].startswith("ozaki")
                       else "r1_dominant_kernel.json")
     if os.path.exists(tf):
         with open(tf) as fh:
             d = json.load(fh)
         for e in [d] + list(d.get("other_shapes", [])):     # ncu --set full captures, one per GEMM shape
+            traffic_by_shape[tuple(e.get("shape", ()))] = e["dram_bytes_read"] + e["dram_bytes_write"]
             if tuple(e.get("shape", ())) == tuple(cls[1]):
                 traffic = e["dram_bytes_read"] + e["dram_bytes_write"]
 
@@ -431,7 +501,7 @@ def run_b200(args):
                     "path": ("tt_matvec_round_host: numpy (pageable) cores in -> pinned staging ring -> H2D overlapped "
                              "with the contractions; rounded cores out as host arrays (caching pinned allocator), "
                              "D2H of the largest core overlapped with its row-chunked formation")},
-            "roofline": roofline_record(cls, fp64_peak, traffic, prof_all, args.steps, ms_all),
+            "roofline": roofline_record(cls, fp64_peak, traffic, prof_all, args.steps, ms_all, kev, traffic_by_shape),
             "executed_gemm_gflop_per_step": sum(r[2] for r in prof_all) / args.steps / 1e9,
             "all_dmma_ms_per_step": dmma_ms,
             "rounding": ("left-to-right steps whose unfolding is certified full rank (1 / ||R^-1||_F > 2 delta: "

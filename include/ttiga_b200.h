@@ -180,6 +180,13 @@ int ttb_jacobi_diag(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, 
 int ttb_abs_floor(void* stream, long long tot, double* d, double* part);
 int ttb_tt_gather3(void* stream, int N, const long long* idx, const double* G0, int n0, int r1, const double* G1,
                    int n1, int r2, const double* G2, int n2, double* out);
+/* TT-cross index bookkeeping on the device (reference tensor_train/cross.py:88-100): out ((nl nk nr) x d int64,
+   d = k + 1 + w) row (l nk + i) nr + r = (left[l, 0..k), i, right[r, 0..w)). */
+int ttb_fiber_index(void* stream, int nl, int nk, int nr, int k, int w, const long long* left, const long long* right,
+                    long long* out);
+/* Nested index set from maxvol rows sel (r int32) of an unfolding with inner size q (cross.py:150-152, 178-180):
+   side 0: out[s] = (src[sel[s] / q, 0..w), sel[s] % q); side 1: out[s] = (sel[s] / q, src[sel[s] % q, 0..w)). */
+int ttb_nested_index(void* stream, int r, int q, int w, int side, const int* sel, const long long* src, long long* out);
 /* y = local projected operator applied to v (amen._LocalSystem.matvec3). ws: r0*Ra*n*r1 + r0*n*Rb*r1 doubles. */
 int ttb_local_matvec(void* stream, int r0, int n, int r1, int Ra, int Rb, int h, const double* phiL, const double* M,
                      const double* phiR, const double* v, double* y, double* ws);
@@ -229,6 +236,12 @@ int ttb_local_pcg_gemm(void* stream, int r0, int n, int r1, int Ra, int Rb, int 
  * A (int8 M x K row-major) B (int8 N x K row-major)^T; M, N, K multiples of 128. Building block of the
  * Ozaki-scheme FP64 emulation. */
 int ttb_i8gemm(void* stream, int M, int N, int K, const void* A, const void* B, int* C);
+/* Per-launch timing of the Ozaki GEMM kernel (bench.py's roofline record): enable = 1 drops earlier records and
+   times every oz_gemm_kernel launch from now on (two CUDA events on its stream), 0 stops; returns the records
+   held. _read: up to cap records in launch order, ms[i] = kernel duration, shape[4i..] = M, N, K, kind
+   (0 general, 1 Gram, 2 A lower-triangular, 3 B upper-triangular, 4 TT-matvec core); returns the count. */
+int ttb_ozaki_kernel_events(int enable);
+int ttb_ozaki_kernel_events_read(int cap, double* ms, int* shape);
 /* FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme, 7 balanced 8-bit slices per operand,
  * 54-bit operands, exact int32 level sums): C (M x N, ldc) = A (M x K row-major, lda) op(B), op(B) = B
  * (K x N, ldb) for tB = 0 or B^T (B: N x K) for tB = 1. Replaces ttb_dgemm for large tcgen05-tileable

@@ -64,12 +64,16 @@ SIGNATURES = {
     "ttb_band_chol_solve": (i32, [vp, i64, i32, vp, vp, vp]),
     "ttb_jacobi_diag": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
     "ttb_tt_gather3": (i32, [vp, i32, vp, vp, i32, i32, vp, i32, i32, vp, i32, vp]),
+    "ttb_fiber_index": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp]),
+    "ttb_nested_index": (i32, [vp, i32, i32, i32, i32, vp, vp, vp]),
     "ttb_local_matvec": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "ttb_pcg_workspace": (i64, [i32, i32, i32, i32, i32]),
     "ttb_local_pcg": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, f64, i32, i32, vp, vp, vp]),
     "ttb_abs_floor": (i32, [vp, i64, vp, vp]),
     "ttb_i8gemm": (i32, [vp, i32, i32, i32, vp, vp, vp]),
     "ttb_ozaki_workspace": (i64, [i32, i32, i32]),
+    "ttb_ozaki_kernel_events": (i32, [i32]),
+    "ttb_ozaki_kernel_events_read": (i32, [i32, vp, vp]),
     "ttb_ozaki_applies": (i32, [i32, i32, i32]),
     "ttb_dgemm_ozaki": (i32, [vp, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
     "ttb_dgemm_ozaki_ex": (i32, [vp, i32, i32, i32, i32, f64, vp, i64, vp, i64, f64, vp, i64, vp]),

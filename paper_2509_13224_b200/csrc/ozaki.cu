@@ -16,6 +16,8 @@
 // issues, per A slice s, MMAs of N = 64 nt against nt consecutive B slice tiles (the level
 // accumulators s .. s+nt-1 are consecutive 64-column TMEM ranges), 10 MMAs per 32-byte k step for
 // 34 slice products; the epilogue sums the levels in FP64 and writes C once through shared memory.
+#include <vector>
+
 #include "common.cuh"
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -1111,6 +1113,34 @@ int oz_launch_cluster(cudaStream_t st, int grid, size_t smem, const CUtensorMap&
   return e == cudaSuccess ? 0 : (int)e;
 }
 
+// Optional per-launch timing of oz_gemm_kernel (ttb_ozaki_kernel_events): CUDA events on the launching
+// stream right around the kernel, so a caller's roofline record can use the kernel's own duration inside a
+// running step (the slicing passes before it and the reduce / mirror after it are outside the pair).
+struct OzEvent {
+  cudaEvent_t a, b;
+  int M, N, K, kind;   // kind 0 general, 1 Gram (sym), 2 A lower-triangular, 3 B upper-triangular, 4 TT-matvec core
+};
+std::vector<OzEvent> g_oz_events;
+bool g_oz_events_on = false;
+struct OzEventScope {
+  cudaStream_t st;
+  OzEvent ev;
+  bool on;
+  OzEventScope(cudaStream_t s, int M, int N, int K, int kind) : st(s), on(g_oz_events_on) {
+    if (!on) return;
+    ev = OzEvent{nullptr, nullptr, M, N, K, kind};
+    cudaEventCreate(&ev.a);
+    cudaEventCreate(&ev.b);
+    cudaEventRecord(ev.a, st);
+  }
+  void stop() {
+    if (!on) return;
+    cudaEventRecord(ev.b, st);
+    g_oz_events.push_back(ev);
+    on = false;
+  }
+};
+
 // the int8 GEMM over prepared slices + split-K reduction (+ mirror for sym)
 int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, double beta, double* C, long long ldc,
            int sym, int trilA = 0, int mv = 0, int nv = 0) {
@@ -1152,6 +1182,7 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
   static const int cluster_mode = getenv("TTB_OZAKI_CLUSTER") ? atoi(getenv("TTB_OZAKI_CLUSTER")) : 1;
   const bool cluster = levels == 8 && tiles % 2 == 0 && grid % 2 == 0 && (cluster_mode == 2 || (cluster_mode == 1 && sym));
   if (cluster) o.mfast = 0;   // a cluster's two CTAs take consecutive units that must share the A row block
+  OzEventScope evs(st, M, N, K, sym ? 1 : (o.trilA == 1 ? 2 : (o.trilA == 2 ? 3 : 0)));
   if (cluster && kc > OZ_SUB * OA_K) {
     const int e = oz_launch_cluster<8, true>(st, grid, smem, ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
     if (e) return e;
@@ -1164,6 +1195,7 @@ int oz_run(cudaStream_t st, const OzWs& w, int M, int N, int K, double alpha, do
     oz_gemm_kernel<7, false><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
   else
     oz_gemm_kernel<8, false><<<grid, 320, smem, st>>>(ta, tb, M, N, K, kc, ks, (int)tiles, sym, w.ea, w.fb, o);
+  evs.stop();
   ttb_count();
   if (ks > 1) {
     const long long tot = (long long)M * N;
@@ -1501,12 +1533,41 @@ TTB_API int ttb_matvec_core_ozaki(void* stream, int Ra, int n, int m, int Rb, in
   if (ks > 1) return TTB_EARG;   // the scatter epilogue writes final values: no split-K partials
   OzOut o{Y, 0, 0, 1.0, 0.0, 3, 0, 0, 0, n, Rb, rc, rd};
   const int grid = tiles < oz_nsm() ? (int)tiles : oz_nsm();
+  OzEventScope evs(st, M, N, m, 4);
   if (kc > OZ_SUB * OA_K)
     oz_gemm_kernel<8, true><<<grid, 320, smem, st>>>(ta, tb, M, N, m, kc, 1, (int)tiles, 0, w.ea, w.fb, o);
   else
     oz_gemm_kernel<8, false><<<grid, 320, smem, st>>>(ta, tb, M, N, m, kc, 1, (int)tiles, 0, w.ea, w.fb, o);
+  evs.stop();
   ttb_count();
   return ttb_last_error();
+}
+
+// Per-launch timing of oz_gemm_kernel. enable = 1: drop earlier records and time every launch from now on
+// (two CUDA events per launch on its stream); enable = 0: stop. Returns the number of records held.
+TTB_API int ttb_ozaki_kernel_events(int enable) {
+  if (enable) {
+    for (auto& e : g_oz_events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    g_oz_events.clear();
+  }
+  g_oz_events_on = enable != 0;
+  return (int)g_oz_events.size();
+}
+// Reads up to cap records in launch order (after synchronizing on each end event): ms[i] = kernel duration,
+// shape[4 i ..] = M, N, K, kind (0 general, 1 Gram, 2 A lower-triangular, 3 B upper-triangular, 4 TT-matvec
+// core). Returns the number written.
+TTB_API int ttb_ozaki_kernel_events_read(int cap, double* ms, int* shape) {
+  int n = 0;
+  for (auto& e : g_oz_events) {
+    if (n >= cap) break;
+    float t = 0.f;
+    cudaEventSynchronize(e.b);
+    cudaEventElapsedTime(&t, e.a, e.b);
+    ms[n] = (double)t;
+    shape[4 * n] = e.M; shape[4 * n + 1] = e.N; shape[4 * n + 2] = e.K; shape[4 * n + 3] = e.kind;
+    ++n;
+  }
+  return n;
 }
 
 TTB_API long long ttb_ozaki_workspace(int M, int N, int K) { return ozaki_ws_bytes(M, N, K); }

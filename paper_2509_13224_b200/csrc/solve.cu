@@ -229,8 +229,9 @@ __device__ __forceinline__ AbsMax grid_absmax(const double* pv, const long long*
 __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double* __restrict__ Q, double* W0,
                                                       int* perm, double* W1, double* Ainv, double* pv,
                                                       long long* pi, double tol, int max_iters, int* rows_out,
-                                                      int* status) {
+                                                      int* status, int ainv_smem) {
   cg::grid_group grid = cg::this_grid();
+  extern __shared__ double mv_dyn[];   // ainv_smem: the 2 r^2 Gauss-Jordan tableau of phase 2 (block 0)
   __shared__ double sv[32];
   __shared__ long long si[32];
   __shared__ double srow[RMAX];
@@ -290,46 +291,58 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
     grid.sync();
     double* t = A; A = B; B = t;
   }
-  // phase 2: Ainv = inv(Q[rows]) by Gauss-Jordan with partial pivoting (block 0), C = Q Ainv
+  // phase 2: Ainv = inv(Q[rows]) by Gauss-Jordan with partial pivoting (block 0), C = Q Ainv. The
+  // tableau lives in shared memory when it fits (the r steps are a chain of small dependent passes:
+  // shared-memory latency instead of L2 round trips; same operations in the same order), the inverse
+  // is then copied out for the other CTAs.
   if (blockIdx.x == 0) {
+    double* Aw = ainv_smem ? mv_dyn : Ainv;
     for (int e = threadIdx.x; e < r * r; e += MT_) {
       int c = e / r, i = e % r;
-      Ainv[(long long)c * r + i] = Q[(long long)c * n + perm[i]];
-      Ainv[(long long)(c + r) * r + i] = (c == i) ? 1.0 : 0.0;
+      Aw[(long long)c * r + i] = Q[(long long)c * n + perm[i]];
+      Aw[(long long)(c + r) * r + i] = (c == i) ? 1.0 : 0.0;
     }
     __syncthreads();
     __shared__ int sp;
     for (int k = 0; k < r; ++k) {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x < 32) {   // first row index of the largest |column k| entry at or below the diagonal
         int p = k;
-        double bv = fabs(Ainv[(long long)k * r + k]);
-        for (int i = k + 1; i < r; ++i) {
-          double v = fabs(Ainv[(long long)k * r + i]);
+        double bv = -1.0;
+        for (int i = k + (int)threadIdx.x; i < r; i += 32) {
+          double v = fabs(Aw[(long long)k * r + i]);
           if (v > bv) { bv = v; p = i; }
         }
-        sp = p;
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int op = __shfl_xor_sync(0xffffffffu, p, o);
+          if (ov > bv || (ov == bv && op < p)) { bv = ov; p = op; }
+        }
+        if (threadIdx.x == 0) sp = p;
       }
       __syncthreads();
       const int p = sp;
       if (p != k)
         for (int c = threadIdx.x; c < 2 * r; c += MT_) {
-          double t = Ainv[(long long)c * r + k];
-          Ainv[(long long)c * r + k] = Ainv[(long long)c * r + p];
-          Ainv[(long long)c * r + p] = t;
+          double t = Aw[(long long)c * r + k];
+          Aw[(long long)c * r + k] = Aw[(long long)c * r + p];
+          Aw[(long long)c * r + p] = t;
         }
       __syncthreads();
-      const double d = Ainv[(long long)k * r + k];
-      for (int c = threadIdx.x; c < 2 * r; c += MT_) Ainv[(long long)c * r + k] /= d;
+      const double d = Aw[(long long)k * r + k];
+      __syncthreads();
+      for (int c = threadIdx.x; c < 2 * r; c += MT_) Aw[(long long)c * r + k] /= d;
       __syncthreads();
       for (int e = threadIdx.x; e < r * 2 * r; e += MT_) {
         int c = e / r, i = e % r;
-        if (i != k && c != k) Ainv[(long long)c * r + i] -= Ainv[(long long)k * r + i] * Ainv[(long long)c * r + k];
+        if (i != k && c != k) Aw[(long long)c * r + i] -= Aw[(long long)k * r + i] * Aw[(long long)c * r + k];
       }
       __syncthreads();
       for (int i = threadIdx.x; i < r; i += MT_)
-        if (i != k) Ainv[(long long)k * r + i] = 0.0;
+        if (i != k) Aw[(long long)k * r + i] = 0.0;
       __syncthreads();
     }
+    if (ainv_smem)
+      for (int e = threadIdx.x; e < r * r; e += MT_) Ainv[(long long)r * r + e] = Aw[(long long)r * r + e];
   }
   grid.sync();
   // inverse sits in columns r..2r-1; C (buffer Ca) = Q Ainv, with the first swap's argmax partials
@@ -390,17 +403,21 @@ __global__ void __launch_bounds__(MT_) maxvol_kernel(int n, int r, const double*
   }
 }
 
-int maxvol_grid(int n) {
+constexpr size_t MV_DYN_MAX = 160 * 1024;   // dynamic shared memory the phase-2 tableau may take (r <= 101)
+
+int maxvol_grid(int n, size_t dyn) {
   // one row per thread, up to the co-resident limit of the cooperative launch (<= 296 partials)
-  static int maxb = 0;
-  if (!maxb) {
-    int dev = 0, sms = 0, per = 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, maxvol_kernel, MT_, 0);
-    maxb = sms * (per > 0 ? per : 1);
-    if (maxb > 296) maxb = 296;
+    cudaFuncSetAttribute(maxvol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MV_DYN_MAX);
   }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, maxvol_kernel, MT_, dyn);
+  int maxb = sms * (per > 0 ? per : 1);
+  if (maxb > 296) maxb = 296;
   int want = ceil_div(n, MT_);
   if (want < 1) want = 1;
   return want < maxb ? want : maxb;
@@ -472,9 +489,12 @@ TTB_API int ttb_maxvol(void* stream, int n, int r, const double* Q, double tol, 
   long long* pi = reinterpret_cast<long long*>(pv + 3 * 296);
   int* perm = iws;
   int* status = iws + n;
-  int nblk = maxvol_grid(n);
-  void* args[] = {&n, &r, &Q, &W, &perm, &C, &Ainv, &pv, &pi, &tol, &max_iters, &rows_out, &status};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)maxvol_kernel, dim3(nblk), dim3(MT_), args, 0, as_stream(stream)); ttb_count();
+  size_t dyn = 2 * (size_t)r * r * sizeof(double);
+  int ainv_smem = dyn <= MV_DYN_MAX ? 1 : 0;
+  if (!ainv_smem) dyn = 0;
+  int nblk = maxvol_grid(n, dyn);
+  void* args[] = {&n, &r, &Q, &W, &perm, &C, &Ainv, &pv, &pi, &tol, &max_iters, &rows_out, &status, &ainv_smem};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)maxvol_kernel, dim3(nblk), dim3(MT_), args, dyn, as_stream(stream)); ttb_count();
   return e == cudaSuccess ? 0 : (int)e;
 }
 

@@ -280,7 +280,53 @@ __global__ void gather_kernel(int N, int r1, int r2, const long long* __restrict
   if (lane == 0) out[q] = acc;
 }
 
+// TT-cross index bookkeeping on the device (reference tensor_train/cross.py:88-100, 150-152, 178-180).
+// Fiber multi-indices of the unfolding C[(l, i), r]: row (l nk + i) nr + r of out (d wide) is
+// (left[l, 0..k), i, right[r, 0..w)), k + 1 + w = d.
+__global__ void fiber_index_kernel(long long tot, int nk, int nr, int k, int w, const long long* __restrict__ left,
+                                   const long long* __restrict__ right, long long* __restrict__ out) {
+  const int d = k + 1 + w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot * d; e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / d;
+    const int c = (int)(e - row * d);
+    const long long rr = row % nr, li = row / nr;
+    const long long i = li % nk, l = li / nk;
+    out[e] = c < k ? left[l * k + c] : (c == k ? i : right[rr * w + (c - k - 1)]);
+  }
+}
+// Nested index sets from the maxvol rows sel of an unfolding with inner size q:
+// side 0 (left set after a left-to-right step, rows ordered (l, i), q = n_k): out[s] = (src[sel[s] / q], sel[s] % q);
+// side 1 (right set after a right-to-left step, rows ordered (i, r), q = n_r): out[s] = (sel[s] / q, src[sel[s] % q]).
+__global__ void nested_index_kernel(int r, int q, int w, int side, const int* __restrict__ sel,
+                                    const long long* __restrict__ src, long long* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * (w + 1)) return;
+  const int s = e / (w + 1), c = e % (w + 1);
+  const int v = sel[s];
+  if (side == 0)
+    out[e] = c < w ? src[(long long)(v / q) * w + c] : (long long)(v % q);
+  else
+    out[e] = c == 0 ? (long long)(v / q) : src[(long long)(v % q) * w + (c - 1)];
+}
+
 }  // namespace
+
+TTB_API int ttb_fiber_index(void* stream, int nl, int nk, int nr, int k, int w, const long long* left,
+                            const long long* right, long long* out) {
+  const long long tot = (long long)nl * nk * nr;
+  if (tot == 0) return TTB_OK;
+  fiber_index_kernel<<<grid_for(tot * (k + 1 + w)), 256, 0, as_stream(stream)>>>(tot, nk, nr, k, w, left, right, out);
+  ttb_count();
+  return ttb_last_error();
+}
+
+TTB_API int ttb_nested_index(void* stream, int r, int q, int w, int side, const int* sel, const long long* src,
+                             long long* out) {
+  if (r == 0) return TTB_OK;
+  nested_index_kernel<<<ceil_div(r * (w + 1), 256), 256, 0, as_stream(stream)>>>(r, q, w, side, sel, src, out);
+  ttb_count();
+  return ttb_last_error();
+}
 
 TTB_API int ttb_band_matvec(void* stream, int Ra, int Rb, int n, int h, int rc, int rd, const double* M,
                             const double* X, double* Y) {

@@ -734,8 +734,10 @@ def svd(X):
 # ---------------------------------------------------------------------------
 # solvers
 
-def solve(A, B):
-    """np.linalg.solve(A, B) with LU + partial pivoting on the device."""
+def solve(A, B, status=None):
+    """np.linalg.solve(A, B) with LU + partial pivoting on the device. ``status`` (an object with
+    add(kind, status_tensor)): the singularity flag is handed to it instead of being read here (the caller
+    raises LinAlgError at its next synchronization)."""
     n = A.shape[0]
     if A.shape != (n, n):
         raise ValueError("square matrix expected")
@@ -746,7 +748,9 @@ def solve(A, B):
     piv = empty(n, dtype=I32)
     info = empty(1, dtype=I32)
     call("ttb_lu_solve", n, ptr(LU), n, ptr(piv), Bm.shape[1], ptr(Bcm), n, 1, ptr(info))
-    if int(info.item()) != 0:
+    if status is not None:
+        status.add("solve", info)
+    elif int(info.item()) != 0:
         raise LinAlgError("Singular matrix")
     X = Bcm.t()
     return X.reshape(n) if vec else X
@@ -780,6 +784,20 @@ def maxvol_colmajor(Qcm, n, r, tol=1.01, max_iters=200):
     if int(iws[n].item()) != 0:
         raise MaxvolError("degenerate pivot: matrix has deficient column rank")
     return rows.cpu().numpy().astype(np.int64)
+
+
+def maxvol_colmajor_dev(Qcm, n, r, pending, tol=1.01, max_iters=200):
+    """maxvol_colmajor without the host round trip: the sorted rows stay on the device (int32 CUDA tensor)
+    and the degeneracy flag is appended to ``pending`` (an object with add(kind, status_tensor); the caller
+    checks it at its next synchronization and raises MaxvolError then). On failure the rows are 0..r-1."""
+    if n <= r:
+        return torch.arange(n, dtype=I32, device=device())
+    ws = empty(int(call_raw("ttb_maxvol_workspace", n, r)))
+    iws = empty(n + 1, dtype=I32)
+    rows = torch.arange(r, dtype=I32, device=device())
+    call("ttb_maxvol", n, r, ptr(Qcm.contiguous()), float(tol), int(max_iters), ptr(rows), ptr(ws), ptr(iws))
+    pending.add("maxvol", iws[n:n + 1])
+    return rows
 
 
 def maxvol(M, tol=1.01, max_iters=200):

@@ -593,3 +593,75 @@ def test_matvec_core_ozaki_layouts(Ra, n, m, Rb, rc, rd):
     call("ttb_matvec_core_ozaki", Ra, n, m, Rb, rc, rd, ptr(M), ptr(G), ptr(Y), ptr(ws))
     assert torch.isfinite(Y).all()
     assert float((Y - ref).norm() / ref.norm()) <= 1e-14
+
+
+def test_cross_index_kernels_match_numpy():
+    """ttb_fiber_index / ttb_nested_index against the reference's list-of-tuples bookkeeping
+    (tensor_train/cross.py:88-100, 150-152, 178-180) restated in numpy."""
+    from paper_2509_13224_b200.tensor_train import cross as C
+    rng = np.random.default_rng(5)
+    d = 4
+    for k, nl, nk, nr in [(0, 1, 7, 5), (1, 3, 6, 4), (2, 5, 9, 1), (3, 4, 8, 1)]:
+        w = d - k - 1
+        left = rng.integers(0, 50, size=(nl, k)).astype(np.int64)
+        right = rng.integers(0, 50, size=(nr, w)).astype(np.int64)
+        got = C._fiber_index(left, nk, right, k, d).cpu().numpy()
+        want = np.array([tuple(left[l]) + (i,) + tuple(right[r]) for l in range(nl) for i in range(nk)
+                         for r in range(nr)], dtype=np.int64).reshape(nl * nk * nr, d)
+        assert np.array_equal(got, want)
+        # nested sets from maxvol rows
+        sel = np.sort(rng.choice(nl * nk, size=min(3, nl * nk), replace=False)).astype(np.int32)
+        got = C._nested(torch.as_tensor(sel, device="cuda"), nk, torch.as_tensor(left, device="cuda"), 0).cpu().numpy()
+        want = np.array([tuple(left[s // nk]) + (s % nk,) for s in sel], dtype=np.int64).reshape(len(sel), k + 1)
+        assert np.array_equal(got, want)
+        sel = np.sort(rng.choice(nk * nr, size=min(3, nk * nr), replace=False)).astype(np.int32)
+        got = C._nested(torch.as_tensor(sel, device="cuda"), nr, torch.as_tensor(right, device="cuda"), 1).cpu().numpy()
+        want = np.array([(s // nr,) + tuple(right[s % nr]) for s in sel], dtype=np.int64).reshape(len(sel), w + 1)
+        assert np.array_equal(got, want)
+
+
+def test_cross_deferred_status_raises(la):
+    """The device-resident maxvol / solve status words raise at the next synchronization what the calls
+    themselves raise when they are read at once (MaxvolError, LinAlgError), first failure first."""
+    from paper_2509_13224_b200.tensor_train.cross import _Deferred
+    M = np.zeros((10, 3))
+    M[:, 0] = np.arange(10)
+    M[:, 1] = 2 * np.arange(10)
+    M[:, 2] = np.arange(10) + 1
+    pend = _Deferred()
+    rows = la.maxvol_colmajor_dev(T(M.T.copy()), 10, 3, pend)
+    assert np.array_equal(rows.cpu().numpy(), np.arange(3))          # untouched on failure: valid indices
+    with pytest.raises(la.MaxvolError):
+        pend.check(torch.zeros(1, dtype=torch.float64, device="cuda"))
+    pend = _Deferred()
+    good = np.random.default_rng(0).standard_normal((40, 4))
+    rows = la.maxvol_colmajor_dev(T(good.T.copy()), 40, 4, pend)
+    assert np.array_equal(rows.cpu().numpy(), la.maxvol(T(good)))
+    la.solve(T(np.zeros((3, 3))), T(np.ones((3, 2))), status=pend)
+    with pytest.raises(np.linalg.LinAlgError):
+        pend.check(torch.zeros(1, dtype=torch.float64, device="cuda"))
+    pend = _Deferred()
+    la.maxvol_colmajor_dev(T(good.T.copy()), 40, 4, pend)
+    assert pend.check(torch.full((1,), 2.5, dtype=torch.float64, device="cuda")) == 2.5 and not pend.items
+
+
+def test_ozaki_kernel_events_record_launches():
+    """ttb_ozaki_kernel_events: one record per oz_gemm_kernel launch with its shape and kind, none when off."""
+    from paper_2509_13224_b200._lib import call, call_raw, lib, ptr
+    L_ = lib()
+    M, N, K = 256, 128, 512
+    A = torch.randn(M, K, device="cuda", dtype=torch.float64)
+    B = torch.randn(K, N, device="cuda", dtype=torch.float64)
+    Cm = torch.empty(M, N, device="cuda", dtype=torch.float64)
+    ws = torch.empty(int(call_raw("ttb_ozaki_workspace", M, N, K)), dtype=torch.uint8, device="cuda")
+    L_.ttb_ozaki_kernel_events(1)
+    for _ in range(3):
+        call("ttb_dgemm_ozaki", 0, M, N, K, ptr(A), K, ptr(B), N, ptr(Cm), N, ptr(ws))
+    assert L_.ttb_ozaki_kernel_events(0) == 3
+    call("ttb_dgemm_ozaki", 0, M, N, K, ptr(A), K, ptr(B), N, ptr(Cm), N, ptr(ws))     # not recorded
+    ms = np.zeros(8)
+    sh = np.zeros(32, dtype=np.int32)
+    n = L_.ttb_ozaki_kernel_events_read(8, ms.ctypes.data, sh.ctypes.data)
+    assert n == 3 and (ms[:3] > 0).all() and (ms[:3] < 50).all()
+    assert sh[:12].reshape(3, 4).tolist() == [[M, N, K, 0]] * 3
+    assert L_.ttb_ozaki_kernel_events(1) == 0 and L_.ttb_ozaki_kernel_events(0) == 0

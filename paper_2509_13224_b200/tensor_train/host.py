@@ -129,8 +129,13 @@ class _Uploader:
         self.th.join()
 
 
-def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=16, chunks=8):
+def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=16, chunks=8, wait=True):
     """Round(A x) for host-resident cores; returns the rounded cores as pinned host tensors.
+
+    wait=False (a stream of products): returns ``(cores, done)`` as soon as the last download is queued;
+    the host tensors may only be read after ``done.synchronize()`` (a CUDA event on the copy stream). The
+    caller can issue the next product meanwhile: its uploads and contractions overlap this one's
+    device-to-host tail (the largest output core, PCIe-bound), which the compute stream does not wait for.
 
     A_cores: dense operator cores (r0, n, m, r1); x_cores: vector cores (s0, m, s1) -- numpy arrays
     (pageable memory, as a reference caller holds them: staged through a pinned ring by a worker
@@ -257,6 +262,8 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
             download(d - 1, cores[d - 1])
     done = torch.cuda.Event()
     done.record(copy)
+    if not wait:
+        return [host[k] for k in range(len(cores))], done
     comp.wait_event(done)
     done.synchronize()
     return [host[k] for k in range(len(cores))]

@@ -68,3 +68,14 @@ def test_host_matches_device_at_scale(monkeypatch):
                                 1e-8)
     assert all(torch.equal(a, b) for a, b in zip(got, got2))
     assert H._STAGE_BYTES * H._STAGE_N < 512 ** 2 * 16 * 16 * 8
+    # a stream of products (wait=False): the next product is issued while the previous one's downloads are
+    # in flight; every result, read after its event, has the same bits
+    x2 = [G * 0.5 for G in x]
+    first = tt_matvec_round_host(A, x, 1e-8, wait=False)
+    second = tt_matvec_round_host(A, x2, 1e-8, wait=False)
+    first[1].synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(got, first[0]))
+    second[1].synchronize()
+    ref2 = tt_round(tt_matvec(TtMatrix(A), TtTensor(x2)), 1e-8)
+    for g, G in zip(second[0], ref2.cores):
+        assert torch.equal(g, G.cpu())

@@ -486,6 +486,10 @@ _GRAM_MIN_RATIO = 1e-4   # s_min / s_max: singular values from X^T X carry relat
 _FULLRANK = os.environ.get("TTB_ROUND_FULLRANK_QR", "1") != "0"
 _FULLRANK_MIN_N = 256
 _FULLRANK_MARGIN = 2.0
+# square steps: U = I, carry = X when certified (SVDFactors._direct_fullrank); and the right-to-left sweep's
+# square / wide unfoldings take Q = I, R = X with no factorization at all (core.py _rl_orthogonalize)
+_FULLRANK_IDENTITY = os.environ.get("TTB_ROUND_IDENTITY_Q", "1") != "0"
+_IDENTITY_Q_MIN = 256
 
 
 def _fullrank_wanted(delta, m, n, want_v):
@@ -493,14 +497,21 @@ def _fullrank_wanted(delta, m, n, want_v):
             and n % 128 == 0)
 
 
-def _fullrank_inverse(Lr, n, delta, cond_max=None):
+def _fullrank_inverse(Lr, n, delta, cond_max=None, info=None):
     """L^-1 (row-major lower) of the row-major lower-triangular Lr when 1 / ||L^-1||_F > 2 delta (and,
-    with cond_max, the power-iteration estimate of cond_2(L) is <= cond_max), else None. One host sync."""
+    with cond_max, the power-iteration estimate of cond_2(L) is <= cond_max), else None. One host sync.
+    ``info``: the Cholesky status word that produced Lr, read in the same copy (non-zero -> None)."""
     Li = _trtri(Lr, n)
     vals = [nrm2(Li).reshape(1)]
     if cond_max is not None:
         vals += [_norm2_est_dev(Lr), _norm2_est_dev(Li)]
+    if info is not None:
+        vals.append(info.to(F64).reshape(1))
     v = torch.cat(vals).cpu().numpy()
+    if info is not None:
+        if v[-1] != 0.0:
+            return None
+        v = v[:-1]
     if not (np.isfinite(v).all() and v[0] > 0.0 and 1.0 / v[0] > _FULLRANK_MARGIN * delta):
         return None
     if cond_max is not None and not (1.1 * v[1] * v[2] <= cond_max):
@@ -615,8 +626,31 @@ class SVDFactors:
     _s = None
 
     def _direct_fullrank(self, X, n, delta):
-        """Square X: Householder X = Q R, the certificate on R^T (its L^-1 and norm on a side stream
+        """Square X. First the factorization-free form: X = I X is an orthogonal-times-carry split as good
+        as Q R (the output core only has to be left-orthonormal), so when X is certified full rank the step
+        returns U = I and the carry X. The certificate comes from the Cholesky factor of X^T X (same
+        singular values as X; its estimate of s_min is off by ~n eps cond^2 relative, so the route is
+        limited to an estimated cond <= 1e5, where that is <= 1e-3 against the factor-2 margin):
+        one n^3 GEMM + Cholesky + triangular inverse instead of a Householder QR with explicit Q.
+        Otherwise: Householder X = Q R, the certificate on R^T (its L^-1 and norm on a side stream
         while Q is formed); certified -> full-rank mode with the explicit Q, else nothing is kept."""
+        if _FULLRANK_IDENTITY:
+            G = gemm(X, X, tA=True)
+            info = empty(1, dtype=I32)
+            call("ttb_potrf", n, ptr(G), n, ptr(info))
+            Lr = empty(n, n)
+            call("ttb_tri_from_potrf", n, ptr(G), n, ptr(Lr), n, None)
+            # a failed Cholesky leaves non-finite / garbage factors: the norms below then fail the test
+            Li = _fullrank_inverse(Lr, n, delta, cond_max=1e5, info=info)
+            if Li is not None:
+                self.fullrank = True
+                self.direct = False
+                self.tall = True
+                self.Qt = torch.eye(n, dtype=F64, device=device())
+                self.Rt = X.t().contiguous()      # SVt() returns Rt^T = X
+                self.S = self.UJ = self.VJ = None
+                return True
+
         def cert(Rt):
             Li = _trtri(Rt, n)        # Rt row-major = R^T, lower triangular
             return nrm2(Li).reshape(1)

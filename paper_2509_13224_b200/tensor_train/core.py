@@ -427,8 +427,17 @@ def _rl_orthogonalize(cores, renorm=False, svd0=False, fullrank_eps=None, lazy_q
             cores[k] = as_core(Qt, n, r1)
             cores[0] = c0.reshape(a, m, kk)
             continue
-        got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0, lazy=lazy_q and not renorm)
-        Qt, Rt = got if got is not None else L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
+        if L._FULLRANK_IDENTITY and r0 >= n * r1 >= L._IDENTITY_Q_MIN:
+            # square or wide unfolding X^T (n r1 x r0): X^T = I X^T is an orthogonal-times-carry split like
+            # Q R (the sweep only needs orthonormal rows in the core and the carry into the previous one,
+            # not a triangular factor): the core becomes the identity, the carry is X itself, the bond
+            # rank n r1 is what the Householder QR returns too. No factorization, no rounding.
+            mk = n * r1
+            Qt = torch.eye(mk, dtype=torch.float64, device=device())
+            Rt = cores[k].reshape(r0, mk)
+        else:
+            got = L.cholqr2_colmajor(cores[k].reshape(r0, n * r1), n * r1, r0, lazy=lazy_q and not renorm)
+            Qt, Rt = got if got is not None else L.qr_colmajor(cores[k].reshape(r0, n * r1).clone(), n * r1, r0)
         kk = Qt.shape[0]
         cores[k] = as_core(Qt, n, r1)
         cores[k - 1] = L.gemm(cores[k - 1].reshape(a * m, r0), Rt, emulate=True).reshape(a, m, kk)

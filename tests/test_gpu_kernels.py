@@ -446,7 +446,19 @@ def test_svd_fullrank_certificate(monkeypatch, shape):
     U, R = f.U(n), f.SVt(n)
     assert float((L.gemm(U, R) - X).norm() / X.norm()) < 1e-14
     assert float((L.gemm(U, U, tA=True) - eye).abs().max()) < 1e-12
-    assert float(torch.tril(R, -1).abs().max()) == 0.0
+    if shape == "tall":
+        assert float(torch.tril(R, -1).abs().max()) == 0.0
+    else:
+        # square: the factorization-free split U = I, carry = X (certificate from the Cholesky factor of X^T X)
+        assert torch.equal(U, eye) and torch.equal(R, X)
+        monkeypatch.setattr(L, "_FULLRANK_IDENTITY", False)      # the Householder Q R form of the same step
+        fh = L.SVDFactors(X, fullrank_delta=1e-8 * float(X.norm()))
+        assert fh.fullrank and fh.S is None
+        Uh, Rh = fh.U(n), fh.SVt(n)
+        assert float((L.gemm(Uh, Rh) - X).norm() / X.norm()) < 1e-14
+        assert float((L.gemm(Uh, Uh, tA=True) - eye).abs().max()) < 1e-12
+        assert float(torch.tril(Rh, -1).abs().max()) == 0.0
+        monkeypatch.setattr(L, "_FULLRANK_IDENTITY", True)
     Uc = L.empty(m, n)
     for i0 in range(0, m, m // 4):
         f.U_rows(n, i0, i0 + m // 4, Uc[i0:i0 + m // 4])
@@ -665,3 +677,33 @@ def test_ozaki_kernel_events_record_launches():
     assert n == 3 and (ms[:3] > 0).all() and (ms[:3] < 50).all()
     assert sh[:12].reshape(3, 4).tolist() == [[M, N, K, 0]] * 3
     assert L_.ttb_ozaki_kernel_events(1) == 0 and L_.ttb_ozaki_kernel_events(0) == 0
+
+
+@pytest.mark.parametrize("r_last", [300, 400], ids=["square", "wide"])
+def test_round_identity_q_for_square_and_wide_unfoldings(monkeypatch, r_last):
+    """Right-to-left sweep over a last core whose unfolding X^T (n x r) has r >= n >= 256: the core becomes
+    the identity and the carry is X (no factorization). Same tensor and ranks as the Householder sweep and
+    as the oracle's tt_round (reference tensor_train/core.py:353-389)."""
+    from oracle import tt as OT
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import TtTensor, tt_round
+    from paper_2509_13224_b200.tensor_train.core import _rl_orthogonalize
+    rng = np.random.default_rng(r_last)
+    n = 300
+    cores = [rng.standard_normal((1, 6, 5)), rng.standard_normal((5, 7, r_last)) / 5,
+             rng.standard_normal((r_last, n, 1)) / np.sqrt(r_last)]
+    t = TtTensor([T(G) for G in cores])
+    orth, _ = _rl_orthogonalize(list(t.cores))
+    k = min(n, r_last)
+    assert tuple(orth[2].shape) == (k, n, 1)
+    assert torch.equal(orth[2].reshape(k, n), torch.eye(k, dtype=torch.float64, device="cuda"))
+    want = OT.TT(cores).full()
+    got = TtTensor(orth).full()
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+    y = tt_round(t, 1e-10)
+    monkeypatch.setattr(L, "_FULLRANK_IDENTITY", False)
+    yh = tt_round(t, 1e-10)
+    yo = OT.round_tt(OT.TT(cores), 1e-10)
+    assert tuple(y.ranks) == tuple(yh.ranks) == tuple(yo.ranks)
+    assert np.abs(y.full() - yo.full()).max() <= 1e-12 * np.abs(want).max()
+    assert np.abs(yh.full() - yo.full()).max() <= 1e-12 * np.abs(want).max()

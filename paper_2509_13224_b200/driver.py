@@ -390,6 +390,7 @@ def solve_poisson(cfg: SolveConfig, want_error: bool = True) -> SolutionReport:
                          compression_K=compression_ratio(K), compression_f=compression_ratio(f),
                          compression_u=compression_ratio(u_full), timings=timings, sweeps=result.sweeps)
     rep.K, rep.f, rep.system, rep.disc, rep.patch = K, f, system, disc, patch
+    rep.solution_interior = result.solution     # the AMEn solution of the eliminated system (tests)
     return rep
 
 

@@ -77,3 +77,107 @@ def test_fullsize_solve_satisfies_system_at_sampled_rows(record_property, c, l2_
     if l2_max is not None:
         record_property("l2_error", rep.l2_error)
         assert rep.l2_error is not None and rep.l2_error <= l2_max, rep.l2_error
+
+
+def _oracle_entry(disc_o, ev, i, j):
+    """K[i, j] = sum_q w_q grad N_i(q)^T R(q) grad N_j(q) by the oracle's Gauss tables and metric evaluator
+    (reference assembly.py:208-222 and geometry.py:247-261), over the points where both functions live."""
+    per = []
+    for k in range(3):
+        q = disc_o.quads[k]
+        p1 = q.V.shape[1]
+        sel = np.flatnonzero((q.first <= min(i[k], j[k])) & (q.first + p1 > max(i[k], j[k])))
+        per.append(sel)
+    if any(s.size == 0 for s in per):
+        return 0.0
+    Q = np.stack(np.meshgrid(*per, indexing="ij"), axis=-1).reshape(-1, 3)
+    _, R = ev.det_metric(Q)
+    w = np.ones(Q.shape[0])
+    gi = np.ones((Q.shape[0], 3))
+    gj = np.ones((Q.shape[0], 3))
+    for k in range(3):
+        q = disc_o.quads[k]
+        qq = Q[:, k]
+        w = w * q.w[qq]
+        vi, di = q.V[qq, i[k] - q.first[qq]], q.D[qq, i[k] - q.first[qq]]
+        vj, dj = q.V[qq, j[k] - q.first[qq]], q.D[qq, j[k] - q.first[qq]]
+        for a in range(3):
+            gi[:, a] *= di if a == k else vi
+            gj[:, a] *= dj if a == k else vj
+    return float(np.sum(w * np.einsum("na,nab,nb->n", gi, R, gj)))
+
+
+@pytest.mark.parametrize("c", [2, 3], ids=["configs2-n256", "configs3-n512"])
+def test_fullsize_operator_and_load_entries_vs_oracle_quadrature(record_property, c):
+    """Full-size assembled stiffness operator (TT-cross of the metric + 1-D quadrature cores + rounded sum of
+    the nine terms) against the oracle's direct Gauss quadrature of the bilinear form at sampled entries
+    K[i, j] (rows uniform, columns uniform in the band): a size-independent check of the assembly where
+    the oracle's own TT assembly takes hours (configs[3] at n=512)."""
+    from oracle import bspline as OB
+    from oracle import iga as OI
+    from oracle import patch as OP
+    from paper_2509_13224_b200 import driver as D
+    from paper_2509_13224_b200.assembly import assemble_stiffness
+    from paper_2509_13224_b200.geometry import make_geometry
+    from paper_2509_13224_b200.workloads import SOLVE_CONFIGS
+    cfg = D.SolveConfig(seed=0, **SOLVE_CONFIGS[c])
+    patch = make_geometry(cfg.geometry, D.geometry_params(cfg))
+    cfg.resolve_bc(patch)
+    disc = D.discretize(cfg, patch)
+    rK, _ = D._spawn_rngs(cfg.seed, 2)
+    K, info = assemble_stiffness(patch, disc, cfg.eps_round, rank_cap=cfg.rank_cap, rng=rK)
+    assert all(info["cross_converged"].values())
+    # the same patch and solution spaces as oracle objects (control net copied: no re-draw, no re-check)
+    sp = [OB.Spline1D(b.knot_vector.knots, b.degree, b.weights) for b in patch.bases]
+    patch_o = OP.Patch(sp, patch.control_points, patch.weights)
+    disc_o = OI.gauss_tables([OB.Spline1D(b.knot_vector.knots, b.degree) for b in disc.solution_bases])
+    ev = OP.TensorGridEval(patch_o, disc_o.axes())
+    h = K.band
+    sizes = disc.mode_sizes
+    rng = np.random.default_rng(3)
+    n_entries = 200
+    I = np.stack([rng.integers(0, n, size=n_entries) for n in sizes], axis=1)
+    O = rng.integers(-h, h + 1, size=(n_entries, 3))
+    J = np.clip(I + O, 0, np.array(sizes) - 1)
+    cores = [G.cpu().numpy() for G in K.cores]            # (Ra, n, 2h+1, Rb)
+    got = np.empty(n_entries)
+    want = np.empty(n_entries)
+    for e in range(n_entries):
+        v = np.ones((1, 1))
+        for k in range(3):
+            v = v @ cores[k][:, I[e, k], J[e, k] - I[e, k] + h, :]
+        got[e] = v[0, 0]
+        want[e] = _oracle_entry(disc_o, ev, I[e], J[e])
+    scale = np.abs(want).max()
+    err = float(np.abs(got - want).max() / scale)
+    rel_fro = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+    print(f"configs[{c}] full-size stiffness, {n_entries} sampled entries vs oracle quadrature: max |diff| / max |K_ij| "
+          f"= {err:.3e}, ||diff|| / ||K_samples|| = {rel_fro:.3e} (eps_round {cfg.eps_round:.0e}), ranks {K.ranks}")
+    record_property("entry_error", err)
+    assert np.count_nonzero(want) > n_entries // 2
+    # measured 4.6e-9 / 9.9e-9 (max) and 1.0e-8 / 1.6e-8 (norm) at eps_round = eps_cross = 1e-8
+    assert err <= 1e-7, err
+    assert rel_fro <= 1e-7, rel_fro
+    # the load vector the same way: f_i = sum_q w_q f(x(q)) det J(q) N_i(q)  (reference assembly.py:163-170, 225-233)
+    from paper_2509_13224_b200.assembly import assemble_load
+    _, rf = D._spawn_rngs(cfg.seed, 2)
+    f, finfo = assemble_load(patch, disc, cfg.source, cfg.eps_cross, rank_cap=cfg.rank_cap, rng=rf)
+    assert finfo["cross_converged"]
+    fo = OI.load_fn(ev, OI.SOURCES[cfg.source])
+    gotf = f.gather(torch.as_tensor(I, device="cuda")).cpu().numpy()
+    wantf = np.empty(n_entries)
+    for e in range(n_entries):
+        per = []
+        for k in range(3):
+            q = disc_o.quads[k]
+            per.append(np.flatnonzero((q.first <= I[e, k]) & (q.first + q.V.shape[1] > I[e, k])))
+        Q = np.stack(np.meshgrid(*per, indexing="ij"), axis=-1).reshape(-1, 3)
+        val = fo(Q)
+        for k in range(3):
+            q = disc_o.quads[k]
+            val = val * q.w[Q[:, k]] * q.V[Q[:, k], I[e, k] - q.first[Q[:, k]]]
+        wantf[e] = val.sum()
+    ef = float(np.abs(gotf - wantf).max() / np.abs(wantf).max())
+    print(f"configs[{c}] full-size load, {n_entries} sampled entries vs oracle quadrature: max |diff| / max |f_i| = {ef:.3e}")
+    record_property("load_entry_error", ef)
+    assert ef <= 1e-7, ef

@@ -758,6 +758,86 @@ class SVDFactors:
         return gemm(self.VJ[:r], self.Qt)
 
 
+# ---------------------------------------------------------------------------
+# leading singular triplets only (rank-capped rounding)
+
+_TOPK = os.environ.get("TTB_TOPK_SVD", "1") != "0"
+_TOPK_MAX = 8          # largest rank cap served
+_TOPK_MIN_N = 200      # smaller factors: the full Jacobi SVD is already cheap
+_TOPK_BLOCK = 16       # iteration block (rank cap + oversampling)
+_TOPK_CHECK = 6        # iterations between Rayleigh-Ritz convergence checks
+_TOPK_MAX_ITERS = 60
+_TOPK_TOL = 1e-13      # Ritz residual ||R^T u - theta v|| <= tol theta_max for every kept triplet
+_topk_start = {}
+
+
+def _topk_start_block(n, b):
+    """Fixed (seeded) b x n start block, cached per shape: the iteration is deterministic."""
+    key = (n, b)
+    if key not in _topk_start:
+        g = torch.Generator(device="cpu").manual_seed(20250913)
+        _topk_start[key] = torch.randn(b, n, generator=g, dtype=F64).to(device())
+    return _topk_start[key]
+
+
+def topk_svd(X, kmax, delta):
+    """Leading part of the truncated SVD a rank-capped rounding step needs (reference tensor_train/core.py
+    :341-350, 377-386 with max_rank): returns (U (m x keep), carry = U^T X (keep x n)) with
+    keep = min(kmax, _chop(s, delta)), or None when the route does not apply or did not converge (the
+    caller then takes the full SVD). With a cap of a few ranks only the leading kmax singular triplets and
+    ||X||_F matter: _chop's tails are tail_j^2 = ||X||_F^2 - sum_{i<j} s_i^2 for j <= kmax, so they are
+    computed by a block power iteration on the triangular factor R of X (block 16, re-orthonormalized every
+    step, Rayleigh-Ritz every 6 steps, deterministic start) until every kept triplet's residual is
+    <= 1e-13 s_max -- instead of a one-sided Jacobi SVD of all n columns (21 ms at n = 510, twice per
+    AMEn residual rounding). Used only for loose thresholds (delta >= 1e-3 ||X||_F, where the tails are
+    free of cancellation); TTB_TOPK_SVD=0 disables it."""
+    m, n = X.shape
+    if not (_TOPK and kmax is not None and 1 <= kmax <= _TOPK_MAX and m >= n >= _TOPK_MIN_N):
+        return None
+    X = X.contiguous()
+    fro2 = dot(X)
+    if m > n:
+        Qt, Rt = qr_colmajor(permute(X, (1, 0)), m, n)       # Qt (n, m) == col-major Q, Rt == row-major R^T
+        R = Rt.t().contiguous()
+    else:
+        Qt, R = None, X
+    b = _TOPK_BLOCK
+    Vt = gemm(_topk_start_block(n, b), R)                     # rows: start vectors pulled through R once
+    theta = None
+    for it in range(0, _TOPK_MAX_ITERS, _TOPK_CHECK):
+        for _ in range(_TOPK_CHECK):
+            Vt, _ = qr_colmajor(Vt, n, b, want_r=False)       # orthonormal rows
+            Wt = gemm(Vt, R, tB=True)                         # (R V)^T
+            Vt = gemm(Wt, R)                                  # (R^T R V)^T
+        Vt, _ = qr_colmajor(Vt, n, b, want_r=False)
+        Wt = gemm(Vt, R, tB=True)                             # (b, n): columns of R V as rows
+        Qwt, Rwt = qr_colmajor(Wt.clone(), n, b)              # R V = Qw Rw
+        Us, S, Vst = svd(Rwt.t().contiguous())                # Rw = Us diag(S) Vst (b x b)
+        order = torch.argsort(S, descending=True)
+        S, Us, Vst = S[order], Us[:, order], Vst[order]
+        Ut = gemm(Us, Qwt, tA=True)                           # left Ritz vectors of R as rows (b, n)
+        Vr = gemm(Vst, Vt)                                    # right Ritz vectors as rows
+        E = gemm(Ut[:kmax], R) - S[:kmax, None] * Vr[:kmax]   # rows: R^T u_i - theta_i v_i
+        stats = torch.cat([S, torch.linalg.vector_norm(E, dim=1), fro2.reshape(1)]).cpu().numpy()
+        theta, res, f2 = stats[:b], stats[b:b + kmax], float(stats[-1])
+        if not np.isfinite(stats).all() or theta[0] <= 0.0:
+            return None
+        if delta < 1e-3 * np.sqrt(f2):
+            return None                                       # tight threshold: tails would cancel
+        if (res <= _TOPK_TOL * theta[0]).all():
+            break
+    else:
+        return None
+    head = np.concatenate([[0.0], np.cumsum(theta[:kmax] ** 2)])
+    tails = np.sqrt(np.maximum(f2 - head, 0.0))               # tails[j]: after keeping j values, j = 0..kmax
+    hit = np.flatnonzero(tails <= delta)
+    keep = max(1, int(hit[0])) if hit.size else kmax
+    keep = min(keep, kmax, n)
+    UXt = Ut[:keep] if Qt is None else gemm(Ut[:keep], Qt)    # (keep, m): left singular vectors of X as rows
+    carry = gemm(UXt, X)                                      # diag(S) Vt = U^T X
+    return UXt.t().contiguous(), carry
+
+
 def svd(X):
     """np.linalg.svd(X, full_matrices=False) on the device: (U, S, Vt)."""
     f = SVDFactors(X, want_v=True)

@@ -526,13 +526,24 @@ def tt_round(t, eps, max_rank=None):
     if d == 1:
         return _unfused([G.clone() for G in cores], tag)
     fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
-    cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps, lazy_q=True)
+    # rank-capped rounding with a small cap (the AMEn residual's kick rank): only the leading singular
+    # triplets are computed (linalg.topk_svd); the first step's SVD is then not started during the sweep
+    topk = max_rank is not None and max_rank <= L._TOPK_MAX and L._TOPK
+    got = _rl_orthogonalize(cores, svd0=not topk, fullrank_eps=fr_eps, lazy_q=True)
+    cores, f0 = got[0], (got[2] if not topk else None)
     total = float(L.nrm2(cores[0]).item())
     if total == 0.0:
         return _unfused([L.zeros(1, G.shape[1], 1) for G in cores], tag)
     delta = eps * total / np.sqrt(d - 1)
     for k in range(d - 1):
         r0, n, r1 = cores[k].shape
+        if topk:
+            top = L.topk_svd(cores[k].reshape(r0 * n, r1), max_rank, delta)
+            if top is not None:
+                U, carry = top
+                cores[k] = U.reshape(r0, n, U.shape[1])
+                cores[k + 1] = _carry_into(carry, cores[k + 1])
+                continue
         f = f0 if (k == 0 and f0 is not None) else L.SVDFactors(
             cores[k].reshape(r0 * n, r1), fullrank_delta=delta if max_rank is None else None)
         # certified full rank (s_min > delta): _chop would keep every singular value, U S Vt = Q R

@@ -707,3 +707,65 @@ def test_round_identity_q_for_square_and_wide_unfoldings(monkeypatch, r_last):
     assert tuple(y.ranks) == tuple(yh.ranks) == tuple(yo.ranks)
     assert np.abs(y.full() - yo.full()).max() <= 1e-12 * np.abs(want).max()
     assert np.abs(yh.full() - yo.full()).max() <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("shape,decay", [((510, 510), 0.7), ((2040, 510), 0.85), ((300, 300), 0.5), ((510, 510), 1.0)],
+                         ids=["square", "tall", "fast-decay", "flat"])
+def test_topk_svd_matches_full_svd(la, shape, decay):
+    """The rank-capped rounding step from the leading singular triplets only (linalg.topk_svd) against the
+    full SVD + _chop (reference tensor_train/core.py:341-350): same keep, same rank-keep approximant. A nearly flat
+    spectrum (no gap to converge on) must fall back (None) rather than return an unconverged basis."""
+    from paper_2509_13224_b200.tensor_train.core import _chop
+    m, n = shape
+    rng = np.random.default_rng(m + n)
+    Uo, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    Vo, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = decay ** np.arange(n) if decay < 1.0 else 1.0 - 1e-3 * np.arange(n) / n     # "flat": no usable gap
+    Xh = (Uo * s) @ Vo.T
+    X = T(Xh)
+    fro = float(np.linalg.norm(Xh))
+    for eps, kmax in [(0.5, 4), (0.5, 2), (0.05, 8), (0.9, 4)]:
+        delta = eps * fro / np.sqrt(2.0)
+        got = la.topk_svd(X, kmax, delta)
+        if decay == 1.0:
+            assert got is None
+            continue
+        assert got is not None, (eps, kmax)
+        U, carry = got
+        f = la.SVDFactors(X)
+        sh = np.sort(f.s_host())[::-1]
+        keep = _chop(sh, delta, kmax)
+        assert U.shape == (m, keep) and carry.shape == (keep, n), (U.shape, keep)
+        approx = (U @ carry).cpu().numpy()
+        want = (Uo[:, :keep] * s[:keep]) @ Vo[:, :keep].T
+        assert np.abs(approx - want).max() <= 1e-11 * s[0]
+        assert float((U.t() @ U - torch.eye(keep, dtype=torch.float64, device="cuda")).abs().max()) < 1e-13
+    # tight thresholds are left to the full SVD (the tails would cancel)
+    assert la.topk_svd(X, 4, 1e-8 * fro) is None
+
+
+def test_round_rank_capped_topk_matches_full(monkeypatch):
+    """tt_round(t, 0.5, max_rank=4) -- the AMEn residual rounding (reference amen.py:262-266) -- through the
+    leading-triplet route and through the full SVDs: same ranks, same tensor; also against the oracle."""
+    from oracle import tt as OT
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import TtTensor, tt_round
+    rng = np.random.default_rng(12)
+    n, r = 320, 300
+    dec = 0.8 ** np.arange(r)
+    cores = [rng.standard_normal((1, n, r)) * dec[None, None, :], rng.standard_normal((r, 6, r)) * dec[None, None, :] / r,
+             rng.standard_normal((r, n, 1)) / np.sqrt(r)]
+    t = TtTensor([T(G) for G in cores])
+    calls = []
+    orig = L.topk_svd
+    monkeypatch.setattr(L, "topk_svd", lambda *a, **k: calls.append(orig(*a, **k)) or calls[-1])
+    y = tt_round(t, 0.5, max_rank=4)
+    assert any(c is not None for c in calls), "the leading-triplet route did not run"
+    monkeypatch.setattr(L, "_TOPK", False)
+    yf = tt_round(t, 0.5, max_rank=4)
+    yo = OT.round_tt(OT.TT(cores), 0.5, 4)
+    assert tuple(y.ranks) == tuple(yf.ranks) == tuple(yo.ranks), (y.ranks, yf.ranks, yo.ranks)
+    full, fullf, fullo = y.full(), yf.full(), yo.full()
+    scale = np.abs(fullo).max()
+    assert np.abs(full - fullf).max() <= 1e-10 * scale
+    assert np.abs(full - fullo).max() <= 1e-10 * scale

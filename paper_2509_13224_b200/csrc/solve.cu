@@ -105,7 +105,19 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int n, int j0, double* 
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
+  // left-looking column sweep: at step k thread i >= k finishes L(i, k) = A(i, k) - sum_{j<k} L(i, j) L(k, j)
+  // (the same subtractions in the same order as the right-looking update, so the same bits), then the
+  // column is scaled by the pivot: one dot product of length k per thread instead of a rank-1 update of
+  // the whole trailing block by all threads every step
   for (int k = 0; k < nb; ++k) {
+    const int i = threadIdx.x;
+    if (i >= k && i < nb) {
+      double sacc = L11[k * CNB + i];
+#pragma unroll 8
+      for (int j = 0; j < k; ++j) sacc -= L11[j * CNB + i] * L11[j * CNB + k];
+      L11[k * CNB + i] = sacc;
+    }
+    __syncthreads();
     double d = L11[k * CNB + k];
     if (d <= 0.0 || !isfinite(d)) {
       if (threadIdx.x == 0) { bad = 1; if (blockIdx.x == 0) *info = j0 + k + 1; }
@@ -114,14 +126,8 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int n, int j0, double* 
     }
     d = sqrt(d);
     __syncthreads();
-    if (threadIdx.x == 0) L11[k * CNB + k] = d;
-    for (int i = k + 1 + threadIdx.x; i < nb; i += blockDim.x) L11[k * CNB + i] /= d;
-    __syncthreads();
-    const int m = nb - k - 1;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      int c = k + 1 + e / m, i = k + 1 + e % m;
-      if (i >= c) L11[c * CNB + i] -= L11[k * CNB + i] * L11[k * CNB + c];
-    }
+    if (i > k && i < nb) L11[k * CNB + i] /= d;
+    if (i == k) L11[k * CNB + k] = d;
     __syncthreads();
   }
   if (bad) return;

@@ -625,6 +625,19 @@ class SVDFactors:
     fullrank = False
     _s = None
 
+    @classmethod
+    def certified(cls, X, Rt, Li):
+        """Factors of a tall X already certified full rank: U = X L^-T (implicit, chunkable), carry = R = L^T;
+        Rt row-major L (X^T X = L L^T), Li = L^-1."""
+        f = cls.__new__(cls)
+        f.m, f.n = X.shape
+        f.direct, f.tall, f.implicit, f.fullrank = False, True, True, True
+        f.X, f._want_v = X, False
+        f.Rt, f.Vr, f.S = Rt, Li, None
+        f.UJ = f.VJ = f.Qt = None
+        f._W = Li.t().contiguous()
+        return f
+
     def _direct_fullrank(self, X, n, delta):
         """Square X. First the factorization-free form: X = I X is an orthogonal-times-carry split as good
         as Q R (the output core only has to be left-orthonormal), so when X is certified full rank the step
@@ -836,6 +849,83 @@ def topk_svd(X, kmax, delta):
     UXt = Ut[:keep] if Qt is None else gemm(Ut[:keep], Qt)    # (keep, m): left singular vectors of X as rows
     carry = gemm(UXt, X)                                      # diag(S) Vt = U^T X
     return UXt.t().contiguous(), carry
+
+
+_SPECULATIVE = os.environ.get("TTB_ROUND_SPECULATIVE", "1") != "0"
+_SPEC_SUBSET = 8        # the step-0 certificate uses the Gram over 1 / 8 of the middle core's columns
+
+
+def speculative_applies(n0, r1, n1, n2, d):
+    """Shapes fullrank_speculative_3core serves: square first unfolding (n0 == r1), large tile-aligned factors."""
+    return bool(_SPECULATIVE and _FULLRANK and _FULLRANK_IDENTITY and _GRAM and _OZAKI and d == 3 and n0 == r1
+                and r1 >= _FULLRANK_MIN_N and r1 % 128 == 0 and n2 >= _IDENTITY_Q_MIN and n2 % 128 == 0
+                and r1 * n1 >= _GRAM_MIN_M and (r1 * n1) % 64 == 0 and n1 % _SPEC_SUBSET == 0
+                and (n1 // _SPEC_SUBSET) * n2 >= 4 * r1 and ((n1 // _SPEC_SUBSET) * n2) % 64 == 0)
+
+
+def fullrank_speculative_3core(Y0, Y1p, eps, d):
+    """Certified full-rank rounding of a 3-core TT whose last core is already the identity, in one pass.
+
+    Y0 (n0 x r1, square, r1 = n0): the first core's unfolding; Y1p (r1, n1, n2): the middle core after the
+    carry of the last one. When BOTH left-to-right steps keep every singular value the rounded TT is
+        core 0 = I,   core 1 = Q of (Y0 x_1 Y1p) = Z L^-T,   core 2 = L^T      (Z = Y0 x_1 Y1p, Z^T Z = L L^T),
+    and the right-to-left orthogonalization of the middle core (a 1024 x 1M Gram, its Cholesky factor L1
+    and the carry through it) only ever served two numbers: the tensor norm (for delta) and the step-0
+    certificate s_min(Y0 L1) > 2 delta. Both are had more cheaply, and rigorously:
+      * ||Y||_F^2 = trace(Z^T Z) -- the Gram the second step needs anyway (cores 0 and 2 are identities);
+      * s_min(Y0 L1) >= s_min(Y0 L_S) for the Cholesky factor L_S of the Gram over ANY subset S of the
+        middle core's columns, since B B^T - B_S B_S^T is positive semidefinite: 1 / 8 of the columns here.
+    So Z is formed speculatively (the carry Y0, no L1 in it: Y0 L1 L1^-1 = Y0), one host synchronization
+    reads both certificates, and on any failure None is returned and the caller runs the ordinary sweeps.
+    Returns (factors of the middle step, total norm) with factors.U(n) the middle core and factors.SVt(n) the
+    carry into the last."""
+    r1, n1, n2 = Y1p.shape
+    if not (speculative_applies(Y0.shape[0], r1, n1, n2, d) and Y0.shape == (r1, r1)):
+        return None
+    B = Y1p.reshape(r1, n1 * n2)
+    sub = (n1 // _SPEC_SUBSET) * n2
+    # ---- step-0 certificate from the column subset: L_S, c0s = Y0 L_S, Cholesky of c0s^T c0s
+    ws = torch.empty(int(call_raw("ttb_ozaki_gram_rows_workspace", r1, sub)), dtype=torch.uint8, device=device())
+    Gs = empty(r1, r1)
+    with _profiled("ozaki-gram", (r1, r1, sub), 1.0 * r1 * (r1 + 128) * sub):
+        call("ttb_ozaki_gram_rows", r1, sub, ptr(B), B.stride(0), ptr(Gs), r1, ptr(ws))
+    del ws
+    info_s = empty(1, dtype=I32)
+    call("ttb_potrf", r1, ptr(Gs), r1, ptr(info_s))
+    Ls = empty(r1, r1)
+    call("ttb_tri_from_potrf", r1, ptr(Gs), r1, ptr(Ls), r1, None)
+    c0s = gemm(Y0, Ls)
+    G0 = gemm(c0s, c0s, tA=True)
+    info0 = empty(1, dtype=I32)
+    call("ttb_potrf", r1, ptr(G0), r1, ptr(info0))
+    L0 = empty(r1, r1)
+    call("ttb_tri_from_potrf", r1, ptr(G0), r1, ptr(L0), r1, None)
+    Li0 = _trtri(L0, r1)
+    # ---- speculative middle unfolding Z = Y0 x_1 Y1p and its Gram
+    Z = gemm(Y0, B, emulate=True).reshape(r1 * n1, n2)
+    m = r1 * n1
+    ws = torch.empty(int(call_raw("ttb_ozaki_gram_workspace", m, n2)), dtype=torch.uint8, device=device())
+    G = empty(n2, n2)
+    with _profiled("ozaki-gram", (n2, n2, m), 1.0 * n2 * (n2 + 128) * m):
+        call("ttb_ozaki_gram", m, n2, ptr(Z), n2, ptr(G), n2, ptr(ws))
+    del ws
+    trace = G.diagonal().sum().reshape(1)
+    info1 = empty(1, dtype=I32)
+    call("ttb_potrf", n2, ptr(G), n2, ptr(info1))
+    Rt = empty(n2, n2)
+    call("ttb_tri_from_potrf", n2, ptr(G), n2, ptr(Rt), n2, None)
+    Li = _trtri(Rt, n2)
+    v = torch.cat([trace, nrm2(Li0).reshape(1), _norm2_est_dev(L0), _norm2_est_dev(Li0), nrm2(Li).reshape(1),
+                   _norm2_est_dev(Rt), _norm2_est_dev(Li), info_s.to(F64), info0.to(F64), info1.to(F64)]).cpu().numpy()
+    if not np.isfinite(v).all() or v[7] != 0.0 or v[8] != 0.0 or v[9] != 0.0 or v[0] <= 0.0:
+        return None
+    total = float(np.sqrt(v[0]))
+    delta = eps * total / np.sqrt(d - 1)
+    ok0 = v[1] > 0.0 and 1.0 / v[1] > _FULLRANK_MARGIN * delta and 1.1 * v[2] * v[3] <= 1e5
+    ok1 = v[4] > 0.0 and 1.0 / v[4] > _FULLRANK_MARGIN * delta and 1.1 * v[5] * v[6] <= 1.0 / _GRAM_MIN_RATIO
+    if not (ok0 and ok1):
+        return None
+    return SVDFactors.certified(Z, Rt, Li), total
 
 
 def svd(X):

@@ -517,6 +517,29 @@ def _chop(s, delta, max_rank=None):
     return min(keep, s.size)
 
 
+def _speculative_fullrank(cores, eps):
+    """The one-pass certified full-rank rounding of linalg.fullrank_speculative_3core for a 3-core TT
+    (1, n0, r1), (r1, n1, r2), (r2, n2, 1) with n0 == r1 and a square or wide last unfolding (r2 >= n2).
+    Returns None when the shapes do not apply (nothing computed); else (cores, factors): cores has the
+    last core carried into the middle one and replaced by the identity, cores[0] replaced by the
+    identity when factors is not None (success); factors None = not certified, the caller runs the
+    ordinary sweeps on the returned cores (same tensor)."""
+    if len(cores) != 3:
+        return None
+    G0, G1, G2 = cores
+    (a, n0, r1), (r1b, n1, r2), (r2b, n2, one) = G0.shape, G1.shape, G2.shape
+    if not (a == 1 and one == 1 and r2 >= n2 and L.speculative_applies(n0, r1, n1, n2, 3)):
+        return None
+    eye2 = torch.eye(n2, dtype=torch.float64, device=device()).reshape(n2, n2, 1)
+    Y1p = L.gemm(G1.reshape(r1 * n1, r2), G2.reshape(r2, n2), emulate=True).reshape(r1, n1, n2)
+    got = L.fullrank_speculative_3core(G0.reshape(n0, r1), Y1p, eps, 3)
+    if got is None:
+        return [G0, Y1p, eye2], None
+    f1, _ = got
+    eye0 = torch.eye(r1, dtype=torch.float64, device=device()).reshape(1, n0, r1)
+    return [eye0, Y1p, eye2], f1
+
+
 def tt_round(t, eps, max_rank=None):
     """Right-to-left QR then left-to-right truncated SVD (reference core.py:353-389)."""
     if eps <= 0:
@@ -525,6 +548,14 @@ def tt_round(t, eps, max_rank=None):
     d = len(cores)
     if d == 1:
         return _unfused([G.clone() for G in cores], tag)
+    if max_rank is None:
+        sp = _speculative_fullrank(cores, eps)
+        if sp is not None:
+            cores, f1 = sp
+            if f1 is not None:      # both steps certified full rank: I, Z L^-T, L^T
+                n = f1.n
+                r1, n1 = cores[1].shape[0], cores[1].shape[1]
+                return _unfused([cores[0], f1.U(n).reshape(r1, n1, n), f1.SVt(n).reshape(n, cores[2].shape[1], 1)], tag)
     fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
     # rank-capped rounding with a small cap (the AMEn residual's kick rank): only the leading singular
     # triplets are computed (linalg.topk_svd); the first step's SVD is then not started during the sweep

@@ -24,7 +24,7 @@ import torch
 
 from .. import linalg as L
 from .._lib import call, call_raw, ptr
-from .core import TtShapeError, _carry_into, _chop, _matvec_core_fused, _rl_orthogonalize
+from .core import TtShapeError, _carry_into, _chop, _matvec_core_fused, _rl_orthogonalize, _speculative_fullrank
 
 __all__ = ["tt_matvec_round_host"]
 
@@ -223,9 +223,38 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
         dev.record_stream(copy)
         return h
 
-    if d == 1:
+    def download_u_chunked(k, f, keep, r0, n):
+        """The largest output core: row chunks, each sent down while the next is formed."""
+        rows = r0 * n
+        Uk = L.empty(rows, keep)
+        h = host_buf(k, (r0, n, keep)).view(rows, keep)
+        cs = max(1, -(-rows // chunks))
+        for i0 in range(0, rows, cs):
+            i1 = min(rows, i0 + cs)
+            f.U_rows(keep, i0, i1, Uk[i0:i1])
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                h[i0:i1].copy_(Uk[i0:i1], non_blocking=True)
+        Uk.record_stream(copy)
+        return Uk
+
+    sp = _speculative_fullrank(cores, eps) if (d == 3 and max_rank is None) else None
+    if sp is not None and sp[1] is not None:
+        # both left-to-right steps certified full rank in one pass (linalg.fullrank_speculative_3core)
+        cores, f1 = sp
+        keep = f1.n
+        r0, n, _ = cores[1].shape
+        download(0, cores[0])
+        cores[1] = download_u_chunked(1, f1, keep, r0, n).view(r0, n, keep)
+        cores[2] = f1.SVt(keep).reshape(keep, cores[2].shape[1], 1)
+        download(2, cores[2])
+    elif d == 1:
         download(0, cores[0])
     else:
+        if sp is not None:
+            cores = sp[0]          # not certified: the ordinary sweeps on the carried cores (same tensor)
         fr_eps = eps / np.sqrt(d - 1) if max_rank is None else None
         cores, _, f0 = _rl_orthogonalize(cores, svd0=True, fullrank_eps=fr_eps, lazy_q=True)
         total = float(L.nrm2(cores[0]).item())
@@ -241,23 +270,13 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
                     cores[k].reshape(r0 * n, r1), fullrank_delta=delta if max_rank is None else None)
                 keep = f.n if f.fullrank else _chop(f.s_host(), delta, max_rank)
                 rows = r0 * n
-                Uk = L.empty(rows, keep)
                 if k < d - 2 or not f.tall:
+                    Uk = L.empty(rows, keep)
                     f.U_rows(keep, 0, rows, Uk)
                     download(k, Uk.view(r0, n, keep))
-                else:  # the largest output core: row chunks, each sent down while the next is formed
-                    h = host_buf(k, (r0, n, keep)).view(rows, keep)
-                    cs = max(1, -(-rows // chunks))
-                    for i0 in range(0, rows, cs):
-                        i1 = min(rows, i0 + cs)
-                        f.U_rows(keep, i0, i1, Uk[i0:i1])
-                        ev = torch.cuda.Event()
-                        ev.record(comp)
-                        copy.wait_event(ev)
-                        with torch.cuda.stream(copy):
-                            h[i0:i1].copy_(Uk[i0:i1], non_blocking=True)
-                    Uk.record_stream(copy)
-                cores[k] = Uk.view(r0, n, keep)
+                    cores[k] = Uk.view(r0, n, keep)
+                else:
+                    cores[k] = download_u_chunked(k, f, keep, r0, n).view(r0, n, keep)
                 cores[k + 1] = _carry_into(f.SVt(keep), cores[k + 1])
             download(d - 1, cores[d - 1])
     done = torch.cuda.Event()

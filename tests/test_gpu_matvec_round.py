@@ -39,7 +39,14 @@ def _instance(n):
 def _route_spy(monkeypatch):
     """Record which large-scale routes returned a result (None = fell back to Householder)."""
     from paper_2509_13224_b200 import linalg as L
-    used = {"cholqr2": 0, "gram": 0, "ozaki": 0, "fullrank": 0, "lazyq": 0}
+    used = {"cholqr2": 0, "gram": 0, "ozaki": 0, "fullrank": 0, "lazyq": 0, "speculative": 0}
+    spec = L.fullrank_speculative_3core
+
+    def spec_spy(*a, **k):
+        r = spec(*a, **k)
+        used["speculative"] += r is not None      # both steps certified in one pass (no right-to-left Gram)
+        return r
+
     chol, gram, oz = L.cholqr2_colmajor, L._gram_jacobi, L.call
 
     def chol_spy(*a, **k):
@@ -59,6 +66,7 @@ def _route_spy(monkeypatch):
             used["ozaki"] += 1
         return oz(name, *a, **k)
 
+    monkeypatch.setattr(L, "fullrank_speculative_3core", spec_spy)
     monkeypatch.setattr(L, "cholqr2_colmajor", chol_spy)
     monkeypatch.setattr(L, "_gram_jacobi", gram_spy)
     monkeypatch.setattr(L, "call", call_spy)
@@ -90,7 +98,9 @@ _ORACLE_N512 = {}
                          ids=["certified-qr", "svd", "formed-q"])
 def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fullrank, lazy):
     """fullrank: the rounding's certified full-rank QR steps on (default) / off (every step a Jacobi SVD);
-    lazy: the one-pass CholeskyQR's Q^T left unformed (default) / formed explicitly."""
+    lazy: the one-pass CholeskyQR's Q^T left unformed (default) / formed explicitly. (Product ranks 1024 over
+    mode size 512: the first unfolding is 512 x 1024, so the one-pass route of the n = 1024 benchmark shape
+    does not apply here; it has its own live-oracle test below.)"""
     from oracle import tt as OT
     from paper_2509_13224_b200 import linalg as L
     from paper_2509_13224_b200.tensor_train import tt_matvec, tt_round
@@ -103,6 +113,7 @@ def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fu
     A, X, Ad, Xd = _instance(n)
     Y = tt_round(tt_matvec(Ad, Xd), 1e-8)
     torch.cuda.synchronize()
+    assert used["speculative"] == 0, used
     assert used["cholqr2"] >= 1 and used["gram"] >= 1 and used["ozaki"] >= 3, used
     assert (used["fullrank"] >= 1) == fullrank, used
     assert (used["lazyq"] >= 1) == lazy, used
@@ -117,11 +128,83 @@ def test_matvec_round_n512_all_routes_vs_oracle(monkeypatch, record_property, fu
     assert err <= 1e-12, err
 
 
-@pytest.mark.parametrize("fullrank", [True, False], ids=["certified-qr", "svd"])
-def test_matvec_round_n1024_vs_oracle_fixture(monkeypatch, record_property, fullrank):
+@pytest.mark.parametrize("speculative", [True, False], ids=["one-pass-certified", "ordinary-sweeps"])
+def test_matvec_round_n512_square_ranks_vs_oracle(monkeypatch, record_property, speculative):
+    """The benchmark's shape class at a size the oracle runs live: operator ranks 8 x vector ranks 64 = product
+    ranks 512 over mode size 512, so the first unfolding is square and the last one square -- the one-pass
+    certified full-rank rounding (linalg.fullrank_speculative_3core: speculative middle core, the norm from its
+    Gram's trace, the step-0 certificate from a column-subset Gram) against the oracle's tt_round, and the
+    ordinary sweeps on the same instance."""
+    from oracle import tt as OT
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor, tt_matvec, tt_round
+    from paper_2509_13224_b200.workloads import matvec_round_instance_np
+    monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 1 << 18)
+    monkeypatch.setattr(L, "_GRAM_MIN_M", 1 << 18)
+    monkeypatch.setattr(L, "_SPECULATIVE", speculative)
+    used = _route_spy(monkeypatch)
+    A, X = matvec_round_instance_np(512, 8, 64, 3, 0)
+    Ad = TtMatrix([torch.as_tensor(G, device="cuda") for G in A])
+    Xd = TtTensor([torch.as_tensor(G, device="cuda") for G in X])
+    Y = tt_round(tt_matvec(Ad, Xd), 1e-8)
+    torch.cuda.synchronize()
+    assert (used["speculative"] >= 1) == speculative, used
+    if speculative:
+        assert used["cholqr2"] == 0 and used["gram"] == 0, used
+    if "Ysq" not in _ORACLE_N512:
+        _ORACLE_N512["Ysq"] = OT.round_tt(OT.matvec(OT.TTOp(A), OT.TT(X)), 1e-8)
+    Yo = _ORACLE_N512["Ysq"]
+    assert tuple(Y.ranks) == tuple(Yo.ranks), (Y.ranks, Yo.ranks)
+    Yh = OT.TT([G.cpu().numpy() for G in Y.cores])
+    err = OT.norm(OT.sub(Yh, Yo)) / OT.norm(Yo)
+    # the output gauge: cores 0 and 1 left-orthonormal (the middle core is Q = Z L^-T of a Cholesky QR: its
+    # orthogonality error is ~eps cond(Z)^2 on either route, the routes' limit is cond <= 1e4)
+    for G in Y.cores[:2]:
+        U = G.reshape(-1, G.shape[2])
+        eo = float((L.gemm(U, U, tA=True) - torch.eye(U.shape[1], dtype=torch.float64, device="cuda")).abs().max())
+        assert eo < 1e-10, eo
+    print(f"matvec+round n=512, product ranks 512 (speculative={speculative}): rel. error vs oracle {err:.3e}, "
+          f"ranks {Y.ranks}, routes {used}")
+    record_property("rel_error", err)
+    assert err <= 1e-12, err
+
+
+def test_matvec_round_speculative_falls_back_when_rank_deficient(monkeypatch, record_property):
+    """Same shape class, but two rank slices of the vector's middle core coincide: the product's second bond has
+    numerical rank 504 < 512, the speculative Gram is singular (or the certificate fails), and the ordinary
+    sweeps must take over and truncate exactly as the oracle does."""
+    from oracle import tt as OT
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor, tt_matvec, tt_round
+    from paper_2509_13224_b200.workloads import matvec_round_instance_np
+    monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 1 << 18)
+    monkeypatch.setattr(L, "_GRAM_MIN_M", 1 << 18)
+    calls = []
+    spec = L.fullrank_speculative_3core
+    monkeypatch.setattr(L, "fullrank_speculative_3core", lambda *a, **k: calls.append(spec(*a, **k)) or calls[-1])
+    A, X = matvec_round_instance_np(512, 8, 64, 3, 0)
+    X = [G.copy() for G in X]
+    X[1][:, :, -1] = X[1][:, :, 0]
+    Ad = TtMatrix([torch.as_tensor(G, device="cuda") for G in A])
+    Xd = TtTensor([torch.as_tensor(G, device="cuda") for G in X])
+    Y = tt_round(tt_matvec(Ad, Xd), 1e-8)
+    assert calls == [None], "the speculative route must have been tried and rejected"
+    Yo = OT.round_tt(OT.matvec(OT.TTOp(A), OT.TT(X)), 1e-8)
+    assert tuple(Y.ranks) == tuple(Yo.ranks) and Y.ranks[2] == 504, (Y.ranks, Yo.ranks)
+    Yh = OT.TT([G.cpu().numpy() for G in Y.cores])
+    err = OT.norm(OT.sub(Yh, Yo)) / OT.norm(Yo)
+    print(f"matvec+round n=512, rank-deficient bond (speculative route rejected): rel. error vs oracle {err:.3e}, ranks {Y.ranks}")
+    record_property("rel_error", err)
+    assert err <= 1e-8, err          # both truncate at 1e-8: the dropped parts differ at that level
+
+
+@pytest.mark.parametrize("fullrank,speculative", [(True, True), (True, False), (False, False)],
+                         ids=["one-pass-certified", "certified-qr", "svd"])
+def test_matvec_round_n1024_vs_oracle_fixture(monkeypatch, record_property, fullrank, speculative):
     from paper_2509_13224_b200 import linalg as L
     from paper_2509_13224_b200.tensor_train import tt_matvec, tt_norm, tt_round
     monkeypatch.setattr(L, "_FULLRANK", fullrank)
+    monkeypatch.setattr(L, "_SPECULATIVE", speculative)
     if not os.path.exists(GOLDEN):
         pytest.fail("tests/golden/matvec_round_oracle.npz missing (tests/golden/make_matvec_round_fixture.py)")
     g = np.load(GOLDEN)
@@ -141,7 +224,7 @@ def test_matvec_round_n1024_vs_oracle_fixture(monkeypatch, record_property, full
     vals = Y.gather(torch.as_tensor(g["n1024_idx"].astype(np.int64), device="cuda")).cpu().numpy()
     ev = float(np.abs(vals - g["n1024_vals"]).max() / np.sqrt(np.mean(g["n1024_vals"] ** 2)))
     en = abs(tt_norm(Y) - float(g["n1024_norm"])) / float(g["n1024_norm"])
-    print(f"matvec+round n=1024 (fullrank={fullrank}) vs oracle fixture: singular values {es1:.2e} / {es2:.2e} (of s_max), "
+    print(f"matvec+round n=1024 (fullrank={fullrank}, speculative={speculative}) vs oracle fixture: singular values {es1:.2e} / {es2:.2e} (of s_max), "
           f"sampled entries {ev:.2e} (of rms), norm {en:.2e}")
     for k, v in (("s1", es1), ("s2", es2), ("entries", ev), ("norm", en)):
         record_property(k, v)

@@ -541,7 +541,11 @@ def run_b200(args):
             "rounding": ("left-to-right steps whose unfolding is certified full rank (1 / ||R^-1||_F > 2 delta: "
                          "_chop keeps every singular value) take Q, R of the QR instead of U, S Vt of the SVD -- same "
                          "tensor, ranks and gauge property; both steps of this workload certify (output ranks "
-                         "1024 = full)" if fullrank_on else "every left-to-right step computes its Jacobi SVD"),
+                         "1024 = full), in one pass: the middle core is formed speculatively, the norm is the trace "
+                         "of its Gram and the first step's certificate comes from a column-subset Gram (a rigorous "
+                         "lower bound), so the right-to-left 1024 x 1M Gram is not computed "
+                         "(linalg.fullrank_speculative_3core; rejected -> the ordinary sweeps)"
+                         if fullrank_on else "every left-to-right step computes its Jacobi SVD"),
             "always_svd_ms_per_step": svd_ms,
             "gpu_launches": launches,
             "clocks": clocks.summary(),

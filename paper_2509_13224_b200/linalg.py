@@ -884,18 +884,17 @@ def fullrank_speculative_3core(Y0, Y1p, eps, d):
         return None
     B = Y1p.reshape(r1, n1 * n2)
     sub = (n1 // _SPEC_SUBSET) * n2
-    # ---- step-0 certificate from the column subset: L_S, c0s = Y0 L_S, Cholesky of c0s^T c0s
+    # ---- step-0 certificate from the column subset S: the Gram G_S = B_S B_S^T, then H = Y0 G_S Y0^T
     ws = torch.empty(int(call_raw("ttb_ozaki_gram_rows_workspace", r1, sub)), dtype=torch.uint8, device=device())
     Gs = empty(r1, r1)
     with _profiled("ozaki-gram", (r1, r1, sub), 1.0 * r1 * (r1 + 128) * sub):
         call("ttb_ozaki_gram_rows", r1, sub, ptr(B), B.stride(0), ptr(Gs), r1, ptr(ws))
     del ws
-    info_s = empty(1, dtype=I32)
-    call("ttb_potrf", r1, ptr(Gs), r1, ptr(info_s))
-    Ls = empty(r1, r1)
-    call("ttb_tri_from_potrf", r1, ptr(Gs), r1, ptr(Ls), r1, None)
-    c0s = gemm(Y0, Ls)
-    G0 = gemm(c0s, c0s, tA=True)
+    # s_min(Y0 L_S)^2 = lambda_min(Y0 G_S Y0^T): one Cholesky factorization of H = Y0 G_S Y0^T (L_S itself is
+    # not needed); the Gram's upper block triangle is mirrored, so G_S is symmetric to the bit and so is H's
+    # lower triangle that potrf reads
+    info_s = torch.zeros(1, dtype=I32, device=device())
+    G0 = gemm(gemm(Y0, Gs), Y0, tB=True)
     info0 = empty(1, dtype=I32)
     call("ttb_potrf", r1, ptr(G0), r1, ptr(info0))
     L0 = empty(r1, r1)

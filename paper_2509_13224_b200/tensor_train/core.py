@@ -517,13 +517,14 @@ def _chop(s, delta, max_rank=None):
     return min(keep, s.size)
 
 
-def _speculative_fullrank(cores, eps):
+def _speculative_fullrank(cores, eps, carried=None):
     """The one-pass certified full-rank rounding of linalg.fullrank_speculative_3core for a 3-core TT
     (1, n0, r1), (r1, n1, r2), (r2, n2, 1) with n0 == r1 and a square or wide last unfolding (r2 >= n2).
     Returns None when the shapes do not apply (nothing computed); else (cores, factors): cores has the
     last core carried into the middle one and replaced by the identity, cores[0] replaced by the
     identity when factors is not None (success); factors None = not certified, the caller runs the
-    ordinary sweeps on the returned cores (same tensor)."""
+    ordinary sweeps on the returned cores (same tensor). ``carried``: the middle core with the last one
+    already carried in (tt_matvec_round_host does it under the uploads); only valid when the shapes apply."""
     if len(cores) != 3:
         return None
     G0, G1, G2 = cores
@@ -531,7 +532,10 @@ def _speculative_fullrank(cores, eps):
     if not (a == 1 and one == 1 and r2 >= n2 and L.speculative_applies(n0, r1, n1, n2, 3)):
         return None
     eye2 = torch.eye(n2, dtype=torch.float64, device=device()).reshape(n2, n2, 1)
-    Y1p = L.gemm(G1.reshape(r1 * n1, r2), G2.reshape(r2, n2), emulate=True).reshape(r1, n1, n2)
+    if carried is not None:       # the host path already carried the last core in, slab by slab
+        Y1p = carried.reshape(r1, n1, n2)
+    else:
+        Y1p = L.gemm(G1.reshape(r1 * n1, r2), G2.reshape(r2, n2), emulate=True).reshape(r1, n1, n2)
     got = L.fullrank_speculative_3core(G0.reshape(n0, r1), Y1p, eps, 3)
     if got is None:
         return [G0, Y1p, eye2], None

@@ -166,24 +166,42 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
             xd = [L.empty(*G.shape) for G in x_cores]
             Mds = [L.empty(*M.shape) for M in A_cores]
         x_tok = [up.submit(G, D) for G, D in zip(x_cores, xd)]
-        plan = []
-        for M, Md in zip(A_cores, Mds):
+        # The benchmark's shape class (linalg.fullrank_speculative_3core): the last core's unfolding X2 is
+        # square / wide, so the right-to-left sweep's first step is "carry X2 into the middle core". With the
+        # last (and first) operator core uploaded BEFORE the middle one, that carry runs slab by slab under
+        # the middle core's uploads (each slab: its contraction, then its rows times X2) instead of as one
+        # 2^41-flop product after the last byte has arrived.
+        prod_r = [(M.shape[0] * G.shape[0], M.shape[1], M.shape[3] * G.shape[2]) for M, G in zip(A_cores, x_cores)]
+        early_carry = (d == 3 and max_rank is None and prod_r[0][0] == 1 and prod_r[2][2] == 1
+                       and prod_r[2][0] >= prod_r[2][1]
+                       and L.speculative_applies(prod_r[0][1], prod_r[1][0], prod_r[1][1], prod_r[2][1], 3))
+        order = [2, 0, 1] if early_carry else list(range(d))
+        plan = [None] * d
+        for k in order:
+            M, Md = A_cores[k], Mds[k]
             Ra = M.shape[0]
             step = max(1, -(-Ra // slices))
-            plan.append([(a0, min(Ra, a0 + step), up.submit(M[a0:min(Ra, a0 + step)], Md[a0:min(Ra, a0 + step)]))
-                         for a0 in range(0, Ra, step)])
+            plan[k] = [(a0, min(Ra, a0 + step), up.submit(M[a0:min(Ra, a0 + step)], Md[a0:min(Ra, a0 + step)]))
+                       for a0 in range(0, Ra, step)]
         for t in x_tok:
             up.wait(t, comp)
-        cores = []
-        for M, G, Md, slabs in zip(A_cores, x_cores, Mds, plan):
+        cores = [None] * d
+        carried = None
+        for k in order:
+            M, G, Md, slabs = A_cores[k], x_cores[k], Mds[k], plan[k]
             Ra, n, m, Rb = M.shape
             rc, _, rd = G.shape
             Y = L.empty(Ra * rc, n, Rb * rd)
             Yv = Y.view(Ra, rc, n, Rb, rd)
-            xk = xd[len(cores)]
+            xk = xd[k]
             fused = _matvec_core_fused(1, n, m, Rb, rc, rd)
             ws = (torch.empty(int(call_raw("ttb_matvec_core_ozaki_workspace", 1, n, m, Rb, rc, rd)), dtype=torch.uint8,
                               device=Y.device) if fused else None)
+            carry_now = early_carry and k == 1
+            if carry_now:
+                r2, n2 = cores[2].shape[0], cores[2].shape[1]
+                X2 = cores[2].reshape(r2, n2)
+                carried = L.empty(Ra * rc, n, n2)
             for a0, a1, tok in slabs:
                 up.wait(tok, comp)
                 for a in range(a0, a1):
@@ -192,8 +210,12 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
                     else:
                         T = L.tdot(Md[a], xk, ([1], [1]), emulate=True)    # (i, b, c, d)
                         L.permute(T, (2, 0, 1, 3), out=Yv[a])              # (c, i, b, d)
+                if carry_now:   # rows (a0 rc .. a1 rc) x n of the middle unfolding, times X2
+                    q0, q1 = a0 * rc * n, a1 * rc * n
+                    L.gemm(Y.view(Ra * rc * n, Rb * rd)[q0:q1], X2, emulate=True,
+                           out=carried.view(Ra * rc * n, n2)[q0:q1])
             Md.record_stream(comp)
-            cores.append(Y)
+            cores[k] = Y
         for t in xd:
             t.record_stream(comp)
     finally:
@@ -240,7 +262,7 @@ def tt_matvec_round_host(A_cores, x_cores, eps, max_rank=None, out=None, slices=
         Uk.record_stream(copy)
         return Uk
 
-    sp = _speculative_fullrank(cores, eps) if (d == 3 and max_rank is None) else None
+    sp = _speculative_fullrank(cores, eps, carried=carried) if (d == 3 and max_rank is None) else None
     if sp is not None and sp[1] is not None:
         # both left-to-right steps certified full rank in one pass (linalg.fullrank_speculative_3core)
         cores, f1 = sp

@@ -79,3 +79,25 @@ def test_host_matches_device_at_scale(monkeypatch):
     ref2 = tt_round(tt_matvec(TtMatrix(A), TtTensor(x2)), 1e-8)
     for g, G in zip(second[0], ref2.cores):
         assert torch.equal(g, G.cpu())
+
+
+def test_host_path_benchmark_shape_class_early_carry(monkeypatch):
+    """The benchmark's shape class (square first unfolding, square last core; product ranks 512 over mode size 512):
+    the host path uploads the last and first operator cores before the middle one and carries the last core
+    into the middle one slab by slab under the uploads, then takes the one-pass certified rounding. Same bits as
+    the device-resident call."""
+    from paper_2509_13224_b200 import linalg as L
+    from paper_2509_13224_b200.tensor_train import TtMatrix, TtTensor, tt_matvec, tt_matvec_round_host, tt_round
+    from paper_2509_13224_b200.workloads import matvec_round_instance_np
+    monkeypatch.setattr(L, "_CHOLQR2_MIN_M", 1 << 18)
+    monkeypatch.setattr(L, "_GRAM_MIN_M", 1 << 18)
+    calls = []
+    spec = L.fullrank_speculative_3core
+    monkeypatch.setattr(L, "fullrank_speculative_3core", lambda *a, **k: calls.append(spec(*a, **k)) or calls[-1])
+    A, x = matvec_round_instance_np(512, 8, 64, 3, 0)
+    ref = tt_round(tt_matvec(TtMatrix(A), TtTensor(x)), 1e-8)
+    got = tt_matvec_round_host(A, x, 1e-8)
+    assert len(calls) == 2 and all(c is not None for c in calls), "one-pass certified rounding on both paths"
+    assert [tuple(g.shape) for g in got] == [tuple(G.shape) for G in ref.cores]
+    for g, G in zip(got, ref.cores):
+        assert torch.equal(g, G.cpu()), "host path must give the device path's bits"

@@ -15,7 +15,11 @@ GFLOP/s counts the reference algorithm's nominal LAPACK flops (workloads.matvec_
 BOTH arms, so the two arms' values are in the ratio of their step times; ms_per_step is the direct
 measure. The line also carries the flops the device actually executed in GEMMs
 (executed_gemm_gflop_per_step) and the same step with every product on DMMA and Householder
-factorizations (all_dmma_ms_per_step).
+factorizations (all_dmma_ms_per_step). roofline: the oz_gemm_kernel class with the largest share of the step,
+from the kernel's own launch durations (CUDA events recorded by the library around every launch inside the
+timed steps; kernel_classes lists all classes, call_level the whole-call figures with the slicing passes).
+e2e: the same product through tt_matvec_round_host from pageable numpy cores, one call at a time; e2e.streamed:
+the same call with wait=False over a stream of products (two results in flight).
 
 --impl reference: the reference algorithm (the numpy/LAPACK oracle restatement of the reference
 tt_matvec + tt_round, on every host thread) on the SAME workload (mode size 1024); one step takes
